@@ -1,0 +1,28 @@
+# Builds the sm_100a fused multi-LoRA library and the CPU oracle.
+# Usage: make            (library + oracle)
+#        make ref        (reference-built golden-vector tool, needs /root/reference)
+NVCC     ?= nvcc
+CXX      ?= g++
+CC       ?= gcc
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+PKG      := paper_2602_07263_b200
+CSRC     := $(PKG)/csrc
+LIB      := $(PKG)/libtlora.so
+ORACLE   := oracle/liboracle.so
+
+all: $(LIB) $(ORACLE)
+
+$(LIB): $(CSRC)/tlora_capi.cu $(CSRC)/lora_gemm.cuh $(CSRC)/sm100_ptx.cuh $(CSRC)/tlora_plan.hpp include/tlora.h
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/tlora_capi.cu 2> build_ptxas.log || (cat build_ptxas.log; false)
+
+$(ORACLE): oracle/tlora_oracle.c oracle/tlora_oracle.h
+	$(CC) -O3 -march=x86-64-v3 -fopenmp -fPIC -shared -std=c11 -o $@ oracle/tlora_oracle.c -lm
+
+ref:
+	$(MAKE) -C oracle ref
+
+clean:
+	rm -f $(LIB) $(ORACLE) build_ptxas.log
+
+.PHONY: all clean ref

@@ -1,0 +1,145 @@
+/*
+ * tlora.h — C-ABI of the B200-native fused multi-LoRA linear layer (tLoRA hot path).
+ *
+ * This is the drop-in boundary for the reference's header-only C++ operator API
+ * (proj/include/lora_fleet/fused_lora.hpp, nano_pipeline.hpp, ssm_plan.hpp). The
+ * C++ mirror of that API (include/lora_fleet/*.hpp) and the Python binding
+ * (paper_2602_07263_b200/capi.py) are both written on top of these entry points.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ *   - Every function returns an int status (TLORA_OK = 0). On failure a message is
+ *     available from tlora_last_error() (thread-local). Nothing throws across the ABI.
+ *   - Device-side compute entry points are enqueue-only on the given CUDA stream
+ *     (passed as void* = cudaStream_t; NULL = legacy default stream).
+ *   - Matrices are dense row-major. Activations/weights on device are bf16; adapter
+ *     gradients are fp32. Host-side loaders accept f64 / f32 / bf16.
+ *   - Distinct layers/plans are independent; calls on one layer are externally
+ *     serialised per stream (reference contract: pure and reentrant).
+ */
+#ifndef TLORA_H_
+#define TLORA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TLORA_ABI_VERSION 1
+
+enum tlora_status {
+  TLORA_OK = 0,
+  TLORA_ERR_ARG = 1,       /* bad argument (null pointer, negative size, bad enum)     */
+  TLORA_ERR_SHAPE = 2,     /* shape mismatch (fused_lora.hpp:66-76 messages)           */
+  TLORA_ERR_REGISTRY = 3,  /* unknown / unregistered adapter slot (":73 has no adapter") */
+  TLORA_ERR_PLAN = 4,      /* invalid plan / partition / AIMD arguments                  */
+  TLORA_ERR_CUDA = 5,      /* CUDA runtime / driver failure                              */
+  TLORA_ERR_NO_DEVICE = 6  /* no sm_100 device available: there is no CPU fallback      */
+};
+
+enum tlora_dtype { TLORA_F64 = 0, TLORA_F32 = 1, TLORA_BF16 = 2 };
+enum tlora_where { TLORA_HOST = 0, TLORA_DEVICE = 1 };
+
+typedef struct tlora_layer tlora_layer;
+typedef struct tlora_plan tlora_plan;
+
+/* One output tile of a plan launch and its (up to two) K-segments, in elements.
+ * Mirrors tlora::TileDesc in paper_2602_07263_b200/csrc/lora_gemm.cuh. */
+typedef struct tlora_tile {
+  int32_t m0, n0;
+  int32_t kb0, ke0;
+  int32_t kb1, ke1;
+  int32_t split;
+  int32_t pad;
+} tlora_tile;
+
+/* Which launch of a plan a tile table belongs to. */
+enum tlora_launch {
+  TLORA_L_SHRINK = 0,  /* H   = X·A_j (masked to job columns)             */
+  TLORA_L_FWD = 1,     /* Y   = X·W + H·B_j (K-extension over rank range)  */
+  TLORA_L_DH = 2,      /* dH  = dY·B_jᵀ (masked)                           */
+  TLORA_L_DX = 3,      /* dX  = dY·Wᵀ + dH·A_jᵀ                            */
+  TLORA_L_DB = 4,      /* dB_j = H_jᵀ·dY_j     (fp32, token-range K)       */
+  TLORA_L_DA = 5,      /* dA_jᵀ = dH_jᵀ·X_j    (fp32, token-range K)       */
+  TLORA_L_COUNT = 6
+};
+
+typedef struct tlora_plan_info {
+  int64_t tokens;          /* T                                                    */
+  int64_t d, k;            /* layer dims                                           */
+  int32_t num_slots;       /* registry size                                        */
+  int32_t rank_pad_total;  /* R: packed rank columns (sum of round_up(r_j, 8))     */
+  int32_t num_tiles[TLORA_L_COUNT];
+  int32_t splits_db, splits_da; /* max split-K planes of the gradient launches    */
+  int64_t useful_ext_cols;  /* sum over fwd M-tiles of ranks actually owned         */
+  int64_t packed_ext_cols;  /* sum over fwd M-tiles of K-extension columns issued   */
+} tlora_plan_info;
+
+/* ---- library / errors -------------------------------------------------------- */
+const char* tlora_last_error(void);
+int tlora_abi_version(void);
+/* Fails with TLORA_ERR_NO_DEVICE unless device `device` is an sm_100 GPU. */
+int tlora_device_check(int device, int* sm_count);
+
+/* ---- layer: one adapted projection (frozen base W + adapter registry) --------- */
+/* ranks[num_slots]: registry layout in reference adapter order (std::map by job_id,
+ * fused_lora.hpp:48-53). Slot s owns packed rank columns [off_s, off_s + ranks[s]). */
+int tlora_layer_create(int device, int64_t d, int64_t k, int32_t num_slots,
+                       const int32_t* ranks, tlora_layer** out);
+int tlora_layer_destroy(tlora_layer* layer);
+/* Base weight W: d x k row-major. Stored frozen as bf16 in both K-major layouts. */
+int tlora_layer_set_base(tlora_layer* layer, const void* W, int dtype, int where, void* stream);
+/* Adapter of `slot`: A is d x r, B is r x k (row-major), r = ranks[slot]. */
+int tlora_layer_set_adapter(tlora_layer* layer, int32_t slot, const void* A, const void* B,
+                            int dtype, int where, void* stream);
+/* Packed-rank column offset of each slot (num_slots entries) and R. */
+int tlora_layer_layout(const tlora_layer* layer, int32_t* offsets, int32_t* rank_pad_total);
+/* Zero the fp32 adapter-gradient accumulators. */
+int tlora_layer_zero_grad(tlora_layer* layer, void* stream);
+/* Device pointers of the packed fp32 gradients: dAᵀcat (R x d) and dBcat (R x k). */
+int tlora_layer_grad_ptrs(tlora_layer* layer, float** dAT, float** dB);
+/* Copy one slot's gradients out: dA is d x r, dB is r x k (row-major fp32). */
+int tlora_layer_read_grad(tlora_layer* layer, int32_t slot, float* dA, float* dB, int where,
+                          void* stream);
+
+/* ---- plan: the rank-aware tile-packing / indexing plan of one (nano-)batch ------ */
+/* token_slot[T] (host): owning slot of each token row, any interleaving allowed
+ * (fused_lora.hpp:28-31). Errors: slot out of range -> TLORA_ERR_REGISTRY. */
+int tlora_plan_create(tlora_layer* layer, int64_t tokens, const int32_t* token_slot,
+                      tlora_plan** out);
+int tlora_plan_destroy(tlora_plan* plan);
+int tlora_plan_get_info(const tlora_plan* plan, tlora_plan_info* info);
+/* Copy the tile table of `launch` into out[cap]; *count gets the table length. */
+int tlora_plan_get_tiles(const tlora_plan* plan, int launch, tlora_tile* out, int32_t cap,
+                         int32_t* count);
+
+/* ---- compute (enqueue-only) ----------------------------------------------------- */
+/* Forward: Y = X·W + scatter_j((X_j·A_j)·B_j). X: T x d bf16, Y: T x k (bf16 or f32),
+ * H_stash: T x R bf16 (the per-token low-rank intermediate, kept for backward). */
+int tlora_forward(tlora_layer* layer, const tlora_plan* plan, const void* X, void* Y,
+                  int y_dtype, void* H_stash, void* stream);
+/* Backward: dX = dY·Wᵀ + scatter_j(dH_j·A_jᵀ) (skipped when dX == NULL);
+ * grads  (fp32, packed)  = beta·grads + [dA_j = X_jᵀ·dH_j, dB_j = H_jᵀ·dY_j].
+ * dY: T x k bf16, X: T x d bf16, H_stash from tlora_forward. */
+int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, const void* X,
+                   const void* H_stash, void* dX, float beta, void* stream);
+
+/* ---- reference cost model (bit-identical to fused_lora.hpp:95-116, :139-163) ----- */
+/* tokens_per_slot[num_slots], ranks[num_slots], in reference adapter order. */
+int tlora_op_cost(int64_t tokens, int64_t d, int64_t k, int32_t num_slots,
+                  const int64_t* tokens_per_slot, const int32_t* ranks, int fused,
+                  double* flops, double* bytes_moved, long long* kernel_launches);
+
+/* ---- nano-batch plan + AIMD (nano_pipeline.hpp:51-60, 99-112) --------------------- */
+/* per_nano must hold min(n, group_batch) entries; *n_out receives the clamped N. */
+int tlora_partition(int32_t group_batch, int32_t n, int32_t* n_out, int32_t* per_nano);
+/* has_prev/t_prev carry std::optional<double>; updates n / has_prev / t_prev in place. */
+int tlora_aimd_step(int32_t* n, int32_t* has_prev, double* t_prev, int32_t alpha, double beta,
+                    double tau_rel, double t_t);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TLORA_H_ */

@@ -1,0 +1,112 @@
+"""ctypes binding of the C-ABI declared in include/tlora.h.
+
+This is the Python view of the drop-in boundary: the same entry points a cgo / JNI /
+N-API stub would bind.  There is no CPU fallback: if the shared
+library is missing, loading fails loudly; if there is no sm_100 device, every compute
+entry point returns TLORA_ERR_NO_DEVICE and this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_PKG_DIR = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("TLORA_LIB", _PKG_DIR / "libtlora.so"))
+
+OK, ERR_ARG, ERR_SHAPE, ERR_REGISTRY, ERR_PLAN, ERR_CUDA, ERR_NO_DEVICE = range(7)
+F64, F32, BF16 = 0, 1, 2
+HOST, DEVICE = 0, 1
+L_SHRINK, L_FWD, L_DH, L_DX, L_DB, L_DA = range(6)
+LAUNCH_NAMES = ("shrink", "fwd", "dH", "dX", "dB", "dA")
+
+
+class TileC(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("m0", "n0", "kb0", "ke0", "kb1", "ke1", "split", "pad")]
+
+
+class PlanInfoC(C.Structure):
+    _fields_ = [
+        ("tokens", C.c_int64),
+        ("d", C.c_int64),
+        ("k", C.c_int64),
+        ("num_slots", C.c_int32),
+        ("rank_pad_total", C.c_int32),
+        ("num_tiles", C.c_int32 * 6),
+        ("splits_db", C.c_int32),
+        ("splits_da", C.c_int32),
+        ("useful_ext_cols", C.c_int64),
+        ("packed_ext_cols", C.c_int64),
+    ]
+
+
+# exported symbol -> (restype, argtypes); also the list the CPU test checks against the header
+SIGNATURES = {
+    "tlora_last_error": (C.c_char_p, []),
+    "tlora_abi_version": (C.c_int, []),
+    "tlora_device_check": (C.c_int, [C.c_int, C.POINTER(C.c_int)]),
+    "tlora_layer_create": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int32,
+                                     C.POINTER(C.c_int32), C.POINTER(C.c_void_p)]),
+    "tlora_layer_destroy": (C.c_int, [C.c_void_p]),
+    "tlora_layer_set_base": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "tlora_layer_set_adapter": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                          C.c_int, C.c_int, C.c_void_p]),
+    "tlora_layer_layout": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "tlora_layer_zero_grad": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "tlora_layer_grad_ptrs": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "tlora_layer_read_grad": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int,
+                                        C.c_void_p]),
+    "tlora_plan_create": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int32),
+                                    C.POINTER(C.c_void_p)]),
+    "tlora_plan_destroy": (C.c_int, [C.c_void_p]),
+    "tlora_plan_get_info": (C.c_int, [C.c_void_p, C.POINTER(PlanInfoC)]),
+    "tlora_plan_get_tiles": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(TileC), C.c_int32,
+                                       C.POINTER(C.c_int32)]),
+    "tlora_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                C.c_void_p, C.c_void_p]),
+    "tlora_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_float, C.c_void_p]),
+    "tlora_op_cost": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int32,
+                                C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.c_int,
+                                C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                C.POINTER(C.c_longlong)]),
+    "tlora_partition": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_int32)]),
+    "tlora_aimd_step": (C.c_int, [C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_double), C.c_int32, C.c_double, C.c_double,
+                                  C.c_double]),
+}
+
+
+class TloraError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[tlora status {code}] {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libtlora.so (built in-tree by `make` / __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} not built: run `make` (there is no CPU fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(code: int) -> None:
+    if code != OK:
+        msg = lib().tlora_last_error().decode(errors="replace")
+        raise TloraError(code, msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))

@@ -1,0 +1,754 @@
+// tlora_capi.cu — implementation of the C-ABI in include/tlora.h.
+//
+// Host side: layer registry (frozen base + packed adapters), plan upload, launch
+// sequencing of the six tcgen05 GEMM launches per fused fwd+bwd, and the reference
+// cost model / nano-batch plan / AIMD restated bit-exactly.  No CPU compute path:
+// every numeric entry point enqueues sm_100a kernels and fails if there is no device.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tlora.h"
+#include "lora_gemm.cuh"
+#include "tlora_plan.hpp"
+
+using tlora::GemmArgs;
+using tlora::TileDesc;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Status : std::runtime_error {
+  int code;
+  Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define TL_CUDA(x)                                                                         \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw Status(TLORA_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TLORA_OK;
+  } catch (const Status& s) {
+    g_last_error = s.what();
+    return s.code;
+  } catch (const std::out_of_range& e) {
+    g_last_error = e.what();
+    return TLORA_ERR_REGISTRY;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return TLORA_ERR_PLAN;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TLORA_ERR_ARG;
+  }
+}
+
+void require(bool ok, int code, const std::string& msg) {
+  if (!ok) throw Status(code, msg);
+}
+
+// ------------------------------------------------------------------ TMA descriptors
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  require(fn != nullptr, TLORA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2-D bf16 row-major [outer x inner] with leading dimension ld (elements), 128B swizzle.
+CUtensorMap make_tmap(const void* ptr, int64_t inner, int64_t outer, int64_t ld, int box_inner,
+                      int box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  require(r == CUDA_SUCCESS, TLORA_ERR_CUDA,
+          "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+// K-major operand tile: [rows x 64] boxes.
+CUtensorMap tmap_k(const void* p, int64_t K, int64_t rows, int box_rows) {
+  return make_tmap(p, K, rows, K, tlora::kBK, box_rows);
+}
+// MN-major operand tile: [64 K-rows x 64 MN] boxes over a [K x MN] row-major matrix.
+CUtensorMap tmap_mn(const void* p, int64_t MN, int64_t K) {
+  return make_tmap(p, MN, K, MN, 64, tlora::kBK);
+}
+
+// ------------------------------------------------------------------ launch helpers
+template <int BN, bool AMN, bool BMN, int EPI, int ST>
+void launch_gemm(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1,
+                 const CUtensorMap& b1, const GemmArgs& args, int sm_count, cudaStream_t s) {
+  if (args.num_tiles == 0) return;
+  auto kern = tlora::lora_gemm_kernel<BN, AMN, BMN, EPI, ST>;
+  constexpr int smem = tlora::GemmSmem<BN, ST>::kDynamic;
+  TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int grid = std::min(args.num_tiles, sm_count);
+  kern<<<grid, tlora::kGemmThreads, smem, s>>>(a0, b0, a1, b1, args);
+  TL_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ small kernels
+template <typename T>
+__device__ __forceinline__ float load_as_float(const void* p, int64_t i, int dtype) {
+  if (dtype == TLORA_F64) return (float)reinterpret_cast<const double*>(p)[i];
+  if (dtype == TLORA_F32) return reinterpret_cast<const float*>(p)[i];
+  return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+}
+
+// W (d x k, any dtype) -> W16 (d x k) and Wt16 (k x d), bf16, tiled transpose.
+__global__ void pack_base_kernel(const void* W, int dtype, int64_t d, int64_t k,
+                                 __nv_bfloat16* W16, __nv_bfloat16* Wt16) {
+  __shared__ float tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < d && c < k) {
+      const float v = load_as_float<float>(W, r * k + c, dtype);
+      tile[i][threadIdx.x] = v;
+      W16[r * k + c] = __float2bfloat16_rn(v);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < d && c < k) Wt16[c * d + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+  }
+}
+
+// Adapter of one slot (A: d x r, B: r x k) -> the four packed bf16 layouts.
+__global__ void pack_adapter_kernel(const void* A, const void* B, int dtype, int64_t d, int64_t k,
+                                    int r, int off, int R, __nv_bfloat16* AT, __nv_bfloat16* Acat,
+                                    __nv_bfloat16* BcatT, __nv_bfloat16* Bcat) {
+  const int64_t nA = d * r, nB = (int64_t)r * k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA + nB;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < nA) {
+      const int64_t row = i / r, j = i % r;  // A[row, j]
+      const __nv_bfloat16 v = __float2bfloat16_rn(load_as_float<float>(A, i, dtype));
+      AT[(off + j) * d + row] = v;
+      Acat[row * R + off + j] = v;
+    } else {
+      const int64_t q = i - nA, j = q / k, col = q % k;  // B[j, col]
+      const __nv_bfloat16 v = __float2bfloat16_rn(load_as_float<float>(B, q, dtype));
+      Bcat[(off + j) * k + col] = v;
+      BcatT[col * R + off + j] = v;
+    }
+  }
+}
+
+// dAT rows [off, off+r) (r x d) -> dA (d x r); dB rows -> dB (r x k).
+__global__ void read_grad_kernel(const float* dAT, const float* dBc, int64_t d, int64_t k, int r,
+                                 int off, float* dA, float* dB) {
+  const int64_t nA = d * r, nB = (int64_t)r * k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA + nB;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < nA) {
+      const int64_t row = i / r, j = i % r;
+      dA[i] = dAT[(off + j) * d + row];
+    } else {
+      const int64_t q = i - nA;
+      dB[q] = dBc[(int64_t)off * k + q];
+    }
+  }
+}
+
+// grads[R x N] = beta * grads + sum_{s < cnt[row/128]} partial[s][R x N]  (fixed order)
+__global__ void reduce_splits_kernel(const float* __restrict__ partial, int64_t plane,
+                                     const int32_t* __restrict__ cnt, int64_t R, int64_t N,
+                                     float beta, float* __restrict__ grads) {
+  const int64_t n4 = N / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R * n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / n4;
+    const int c = cnt[row / tlora::kBM];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < c; ++s) {
+      const float4 p = reinterpret_cast<const float4*>(partial + s * plane)[i];
+      acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+    }
+    float4* g = reinterpret_cast<float4*>(grads) + i;
+    if (beta != 0.f) {
+      const float4 o = *g;
+      acc.x += beta * o.x; acc.y += beta * o.y; acc.z += beta * o.z; acc.w += beta * o.w;
+    }
+    *g = acc;
+  }
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    release();
+    if (count) {
+      TL_CUDA(cudaMalloc(&p, count * sizeof(T)));
+      n = count;
+    }
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) TL_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int device_sm_count(int dev) {
+  int n = 0;
+  cudaDeviceProp prop;
+  TL_CUDA(cudaGetDeviceProperties(&prop, dev));
+  require(prop.major == 10 && prop.minor == 0, TLORA_ERR_NO_DEVICE,
+          "device " + std::to_string(dev) + " is sm_" + std::to_string(prop.major) +
+              std::to_string(prop.minor) + "; the fused LoRA kernels are built for sm_100a only");
+  n = prop.multiProcessorCount;
+  return n;
+}
+
+void check_align(const void* p, const char* what) {
+  require(p != nullptr, TLORA_ERR_ARG, std::string(what) + " is null");
+  require((reinterpret_cast<uintptr_t>(p) & 15) == 0, TLORA_ERR_ARG,
+          std::string(what) + " must be 16-byte aligned");
+}
+
+}  // namespace
+
+// ==================================================================== objects
+struct tlora_layer {
+  int device = 0;
+  int sm_count = 148;
+  tlora::RegistryLayout L;
+  std::vector<char> loaded;
+  DevBuf<__nv_bfloat16> W16, Wt16, AT, Acat, BcatT, Bcat;
+  DevBuf<float> dAT, dB;
+  DevBuf<int32_t> col_lo, col_hi;
+  bool base_set = false;
+};
+
+struct tlora_plan {
+  tlora_layer* layer = nullptr;
+  tlora::PlanTables P;
+  DevBuf<TileDesc> tiles[TLORA_L_COUNT];
+  DevBuf<int32_t> token_slot, cnt_db, cnt_da;
+  DevBuf<__nv_bfloat16> dH;
+  DevBuf<float> partial;
+};
+
+namespace {
+
+size_t dtype_size(int dtype) {
+  require(dtype == TLORA_F64 || dtype == TLORA_F32 || dtype == TLORA_BF16, TLORA_ERR_ARG,
+          "unknown dtype");
+  return dtype == TLORA_F64 ? 8 : dtype == TLORA_F32 ? 4 : 2;
+}
+
+// Returns a device pointer to `count` elements of `src`, staging host data if needed.
+const void* stage_input(const void* src, size_t count, int dtype, int where, DevBuf<char>& tmp,
+                        cudaStream_t s) {
+  require(src != nullptr, TLORA_ERR_ARG, "input pointer is null");
+  if (where == TLORA_DEVICE) return src;
+  require(where == TLORA_HOST, TLORA_ERR_ARG, "unknown memory location");
+  const size_t bytes = count * dtype_size(dtype);
+  tmp.alloc(bytes);
+  TL_CUDA(cudaMemcpyAsync(tmp.p, src, bytes, cudaMemcpyHostToDevice, s));
+  return tmp.p;
+}
+
+}  // namespace
+
+// ==================================================================== C-ABI
+extern "C" {
+
+const char* tlora_last_error(void) { return g_last_error.c_str(); }
+int tlora_abi_version(void) { return TLORA_ABI_VERSION; }
+
+int tlora_device_check(int device, int* sm_count) {
+  return guarded([&] {
+    int n = 0;
+    TL_CUDA(cudaGetDeviceCount(&n));
+    require(device >= 0 && device < n, TLORA_ERR_NO_DEVICE,
+            "no CUDA device " + std::to_string(device));
+    const int sms = device_sm_count(device);
+    if (sm_count) *sm_count = sms;
+  });
+}
+
+int tlora_layer_create(int device, int64_t d, int64_t k, int32_t num_slots, const int32_t* ranks,
+                       tlora_layer** out) {
+  return guarded([&] {
+    require(out != nullptr, TLORA_ERR_ARG, "out is null");
+    *out = nullptr;
+    require(d >= 1 && k >= 1, TLORA_ERR_SHAPE, "d and k must be >= 1");
+    require(d % 8 == 0 && k % 8 == 0, TLORA_ERR_SHAPE,
+            "d and k must be multiples of 8 (16-byte TMA row pitch); pad on the host");
+    require(num_slots >= 1 && ranks != nullptr, TLORA_ERR_ARG, "need at least one adapter slot");
+    std::vector<int32_t> rv(ranks, ranks + num_slots);
+    for (int s = 0; s < num_slots; ++s)
+      require(rv[s] >= 1 && rv[s] <= std::min<int64_t>(d, k), TLORA_ERR_SHAPE,
+              "slot " + std::to_string(s) + ": rank must be in [1, min(d, k)]");
+    int n = 0;
+    TL_CUDA(cudaGetDeviceCount(&n));
+    require(device >= 0 && device < n, TLORA_ERR_NO_DEVICE,
+            "no CUDA device " + std::to_string(device) + " (there is no CPU fallback)");
+    auto layer = std::make_unique<tlora_layer>();
+    layer->device = device;
+    DeviceGuard g(device);
+    layer->sm_count = device_sm_count(device);
+    layer->L = tlora::RegistryLayout::make(d, k, rv);
+    layer->loaded.assign(num_slots, 0);
+    const int64_t R = layer->L.R;
+    layer->W16.alloc(d * k);
+    layer->Wt16.alloc(d * k);
+    layer->AT.alloc(R * d);
+    layer->Acat.alloc(d * R);
+    layer->BcatT.alloc(k * R);
+    layer->Bcat.alloc(R * k);
+    layer->dAT.alloc(R * d);
+    layer->dB.alloc(R * k);
+    TL_CUDA(cudaMemset(layer->AT.p, 0, R * d * 2));
+    TL_CUDA(cudaMemset(layer->Acat.p, 0, R * d * 2));
+    TL_CUDA(cudaMemset(layer->BcatT.p, 0, R * k * 2));
+    TL_CUDA(cudaMemset(layer->Bcat.p, 0, R * k * 2));
+    TL_CUDA(cudaMemset(layer->dAT.p, 0, R * d * 4));
+    TL_CUDA(cudaMemset(layer->dB.p, 0, R * k * 4));
+    std::vector<int32_t> lo(num_slots), hi(num_slots);
+    for (int s = 0; s < num_slots; ++s) {
+      lo[s] = layer->L.offset[s];
+      hi[s] = layer->L.offset[s] + rv[s];
+    }
+    layer->col_lo.alloc(num_slots);
+    layer->col_hi.alloc(num_slots);
+    TL_CUDA(cudaMemcpy(layer->col_lo.p, lo.data(), num_slots * 4, cudaMemcpyHostToDevice));
+    TL_CUDA(cudaMemcpy(layer->col_hi.p, hi.data(), num_slots * 4, cudaMemcpyHostToDevice));
+    *out = layer.release();
+  });
+}
+
+int tlora_layer_destroy(tlora_layer* layer) {
+  return guarded([&] {
+    if (!layer) return;
+    DeviceGuard g(layer->device);
+    delete layer;
+  });
+}
+
+int tlora_layer_set_base(tlora_layer* layer, const void* W, int dtype, int where, void* stream) {
+  return guarded([&] {
+    require(layer != nullptr, TLORA_ERR_ARG, "layer is null");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t d = layer->L.d, k = layer->L.k;
+    DevBuf<char> tmp;
+    const void* src = stage_input(W, d * k, dtype, where, tmp, s);
+    dim3 grid((unsigned)tlora::ceil_div(k, 32), (unsigned)tlora::ceil_div(d, 32));
+    pack_base_kernel<<<grid, dim3(32, 8), 0, s>>>(src, dtype, d, k, layer->W16.p, layer->Wt16.p);
+    TL_CUDA(cudaGetLastError());
+    if (tmp.p) TL_CUDA(cudaStreamSynchronize(s));
+    layer->base_set = true;
+  });
+}
+
+int tlora_layer_set_adapter(tlora_layer* layer, int32_t slot, const void* A, const void* B,
+                            int dtype, int where, void* stream) {
+  return guarded([&] {
+    require(layer != nullptr, TLORA_ERR_ARG, "layer is null");
+    require(slot >= 0 && slot < (int)layer->L.rank.size(), TLORA_ERR_REGISTRY,
+            "slot " + std::to_string(slot) + " is not in the registry");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t d = layer->L.d, k = layer->L.k;
+    const int r = layer->L.rank[slot];
+    DevBuf<char> ta, tb;
+    const void* a = stage_input(A, d * r, dtype, where, ta, s);
+    const void* b = stage_input(B, (size_t)r * k, dtype, where, tb, s);
+    pack_adapter_kernel<<<256, 256, 0, s>>>(a, b, dtype, d, k, r, layer->L.offset[slot],
+                                            layer->L.R, layer->AT.p, layer->Acat.p,
+                                            layer->BcatT.p, layer->Bcat.p);
+    TL_CUDA(cudaGetLastError());
+    if (ta.p || tb.p) TL_CUDA(cudaStreamSynchronize(s));
+    layer->loaded[slot] = 1;
+  });
+}
+
+int tlora_layer_layout(const tlora_layer* layer, int32_t* offsets, int32_t* rank_pad_total) {
+  return guarded([&] {
+    require(layer != nullptr, TLORA_ERR_ARG, "layer is null");
+    if (offsets)
+      std::memcpy(offsets, layer->L.offset.data(), layer->L.offset.size() * sizeof(int32_t));
+    if (rank_pad_total) *rank_pad_total = layer->L.R;
+  });
+}
+
+int tlora_layer_zero_grad(tlora_layer* layer, void* stream) {
+  return guarded([&] {
+    require(layer != nullptr, TLORA_ERR_ARG, "layer is null");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    TL_CUDA(cudaMemsetAsync(layer->dAT.p, 0, layer->dAT.n * 4, s));
+    TL_CUDA(cudaMemsetAsync(layer->dB.p, 0, layer->dB.n * 4, s));
+  });
+}
+
+int tlora_layer_grad_ptrs(tlora_layer* layer, float** dAT, float** dB) {
+  return guarded([&] {
+    require(layer != nullptr, TLORA_ERR_ARG, "layer is null");
+    if (dAT) *dAT = layer->dAT.p;
+    if (dB) *dB = layer->dB.p;
+  });
+}
+
+int tlora_layer_read_grad(tlora_layer* layer, int32_t slot, float* dA, float* dB, int where,
+                          void* stream) {
+  return guarded([&] {
+    require(layer != nullptr, TLORA_ERR_ARG, "layer is null");
+    require(slot >= 0 && slot < (int)layer->L.rank.size(), TLORA_ERR_REGISTRY,
+            "slot " + std::to_string(slot) + " is not in the registry");
+    require(dA != nullptr && dB != nullptr, TLORA_ERR_ARG, "output pointer is null");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t d = layer->L.d, k = layer->L.k;
+    const int r = layer->L.rank[slot];
+    DevBuf<float> tmp;
+    float* oa = dA;
+    float* ob = dB;
+    if (where == TLORA_HOST) {
+      tmp.alloc(d * r + (int64_t)r * k);
+      oa = tmp.p;
+      ob = tmp.p + d * r;
+    }
+    read_grad_kernel<<<256, 256, 0, s>>>(layer->dAT.p, layer->dB.p, d, k, r,
+                                         layer->L.offset[slot], oa, ob);
+    TL_CUDA(cudaGetLastError());
+    if (where == TLORA_HOST) {
+      TL_CUDA(cudaMemcpyAsync(dA, oa, d * r * 4, cudaMemcpyDeviceToHost, s));
+      TL_CUDA(cudaMemcpyAsync(dB, ob, (size_t)r * k * 4, cudaMemcpyDeviceToHost, s));
+      TL_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+int tlora_plan_create(tlora_layer* layer, int64_t tokens, const int32_t* token_slot,
+                      tlora_plan** out) {
+  return guarded([&] {
+    require(out != nullptr && layer != nullptr, TLORA_ERR_ARG, "null argument");
+    *out = nullptr;
+    require(tokens >= 1, TLORA_ERR_SHAPE, "plan needs at least one token");
+    require(tokens < (int64_t(1) << 31) - 256, TLORA_ERR_SHAPE, "too many tokens for one plan");
+    require(token_slot != nullptr, TLORA_ERR_ARG, "token_slot is null");
+    DeviceGuard g(layer->device);
+    auto plan = std::make_unique<tlora_plan>();
+    plan->layer = layer;
+    plan->P = tlora::build_plan(layer->L, tokens, token_slot);
+    for (int64_t t = 0; t < tokens; ++t)
+      require(layer->loaded[token_slot[t]], TLORA_ERR_REGISTRY,
+              "slot " + std::to_string(token_slot[t]) + " has no adapter loaded");
+    for (int l = 0; l < TLORA_L_COUNT; ++l) {
+      auto& v = plan->P.tiles[l];
+      plan->tiles[l].alloc(v.size());
+      if (!v.empty())
+        TL_CUDA(cudaMemcpy(plan->tiles[l].p, v.data(), v.size() * sizeof(TileDesc),
+                           cudaMemcpyHostToDevice));
+    }
+    plan->token_slot.alloc(tokens);
+    TL_CUDA(cudaMemcpy(plan->token_slot.p, token_slot, tokens * 4, cudaMemcpyHostToDevice));
+    plan->cnt_db.alloc(plan->P.split_count_db.size());
+    TL_CUDA(cudaMemcpy(plan->cnt_db.p, plan->P.split_count_db.data(),
+                       plan->P.split_count_db.size() * 4, cudaMemcpyHostToDevice));
+    plan->cnt_da.alloc(plan->P.split_count_da.size());
+    TL_CUDA(cudaMemcpy(plan->cnt_da.p, plan->P.split_count_da.data(),
+                       plan->P.split_count_da.size() * 4, cudaMemcpyHostToDevice));
+    const int64_t R = layer->L.R;
+    plan->dH.alloc(tokens * R);
+    const int64_t nsplit = std::max(plan->P.splits_db, plan->P.splits_da);
+    if (nsplit > 1)
+      plan->partial.alloc(nsplit * R * std::max(layer->L.d, layer->L.k));
+    *out = plan.release();
+  });
+}
+
+int tlora_plan_destroy(tlora_plan* plan) {
+  return guarded([&] {
+    if (!plan) return;
+    DeviceGuard g(plan->layer->device);
+    delete plan;
+  });
+}
+
+int tlora_plan_get_info(const tlora_plan* plan, tlora_plan_info* info) {
+  return guarded([&] {
+    require(plan != nullptr && info != nullptr, TLORA_ERR_ARG, "null argument");
+    const auto& L = plan->layer->L;
+    info->tokens = plan->P.T;
+    info->d = L.d;
+    info->k = L.k;
+    info->num_slots = (int32_t)L.rank.size();
+    info->rank_pad_total = L.R;
+    for (int l = 0; l < TLORA_L_COUNT; ++l) info->num_tiles[l] = (int32_t)plan->P.tiles[l].size();
+    info->splits_db = plan->P.splits_db;
+    info->splits_da = plan->P.splits_da;
+    info->useful_ext_cols = plan->P.useful_ext_cols;
+    info->packed_ext_cols = plan->P.packed_ext_cols;
+  });
+}
+
+int tlora_plan_get_tiles(const tlora_plan* plan, int launch, tlora_tile* out, int32_t cap,
+                         int32_t* count) {
+  return guarded([&] {
+    require(plan != nullptr, TLORA_ERR_ARG, "plan is null");
+    require(launch >= 0 && launch < TLORA_L_COUNT, TLORA_ERR_ARG, "unknown launch id");
+    const auto& v = plan->P.tiles[launch];
+    if (count) *count = (int32_t)v.size();
+    if (out) std::memcpy(out, v.data(), std::min<size_t>(cap, v.size()) * sizeof(tlora_tile));
+  });
+}
+
+int tlora_forward(tlora_layer* layer, const tlora_plan* plan, const void* X, void* Y, int y_dtype,
+                  void* H_stash, void* stream) {
+  return guarded([&] {
+    require(layer != nullptr && plan != nullptr, TLORA_ERR_ARG, "null layer/plan");
+    require(plan->layer == layer, TLORA_ERR_PLAN, "plan was built for another layer");
+    require(layer->base_set, TLORA_ERR_ARG, "base weight not set");
+    check_align(X, "X");
+    check_align(Y, "Y");
+    check_align(H_stash, "H_stash");
+    require(y_dtype == TLORA_BF16 || y_dtype == TLORA_F32, TLORA_ERR_ARG,
+            "Y dtype must be bf16 or f32");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const auto& L = layer->L;
+    const int64_t T = plan->P.T, d = L.d, k = L.k, R = L.R;
+
+    // 1) shrink: H = X·Aᵀcatᵀ masked to each token's own packed columns
+    {
+      GemmArgs a{};
+      a.tiles = plan->tiles[TLORA_L_SHRINK].p;
+      a.num_tiles = (int)plan->P.tiles[TLORA_L_SHRINK].size();
+      a.M = (int)T;
+      a.N = (int)R;
+      a.out = H_stash;
+      a.ldo = R;
+      a.row_slot = plan->token_slot.p;
+      a.slot_col_lo = layer->col_lo.p;
+      a.slot_col_hi = layer->col_hi.p;
+      const CUtensorMap ma = tmap_k(X, d, T, tlora::kBM);
+      const CUtensorMap mb = tmap_k(layer->AT.p, d, R, tlora::kPlanBNLow);
+      launch_gemm<128, false, false, tlora::EPI_BF16_MASK, 6>(ma, mb, ma, mb, a, layer->sm_count, s);
+    }
+    // 2) fused base + expand: Y = X·W + H·Bᵀcatᵀ (K-extension over the tile's rank window)
+    {
+      GemmArgs a{};
+      a.tiles = plan->tiles[TLORA_L_FWD].p;
+      a.num_tiles = (int)plan->P.tiles[TLORA_L_FWD].size();
+      a.M = (int)T;
+      a.N = (int)k;
+      a.out = Y;
+      a.ldo = k;
+      a.beta = 0.f;
+      const CUtensorMap ma0 = tmap_k(X, d, T, tlora::kBM);
+      const CUtensorMap mb0 = tmap_k(layer->Wt16.p, d, k, 256);
+      const CUtensorMap ma1 = tmap_k(H_stash, R, T, tlora::kBM);
+      const CUtensorMap mb1 = tmap_k(layer->BcatT.p, R, k, 256);
+      if (y_dtype == TLORA_BF16)
+        launch_gemm<256, false, false, tlora::EPI_BF16, 4>(ma0, mb0, ma1, mb1, a, layer->sm_count, s);
+      else
+        launch_gemm<256, false, false, tlora::EPI_F32, 4>(ma0, mb0, ma1, mb1, a, layer->sm_count, s);
+    }
+  });
+}
+
+int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, const void* X,
+                   const void* H_stash, void* dX, float beta, void* stream) {
+  return guarded([&] {
+    require(layer != nullptr && plan != nullptr, TLORA_ERR_ARG, "null layer/plan");
+    require(plan->layer == layer, TLORA_ERR_PLAN, "plan was built for another layer");
+    require(layer->base_set, TLORA_ERR_ARG, "base weight not set");
+    check_align(dY, "dY");
+    check_align(X, "X");
+    check_align(H_stash, "H_stash");
+    if (dX) check_align(dX, "dX");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const auto& L = layer->L;
+    const int64_t T = plan->P.T, d = L.d, k = L.k, R = L.R;
+    __nv_bfloat16* dH = plan->dH.p;
+
+    // 1) dH = dY·Bᵀ (masked)
+    {
+      GemmArgs a{};
+      a.tiles = plan->tiles[TLORA_L_DH].p;
+      a.num_tiles = (int)plan->P.tiles[TLORA_L_DH].size();
+      a.M = (int)T;
+      a.N = (int)R;
+      a.out = dH;
+      a.ldo = R;
+      a.row_slot = plan->token_slot.p;
+      a.slot_col_lo = layer->col_lo.p;
+      a.slot_col_hi = layer->col_hi.p;
+      const CUtensorMap ma = tmap_k(dY, k, T, tlora::kBM);
+      const CUtensorMap mb = tmap_k(layer->Bcat.p, k, R, tlora::kPlanBNLow);
+      launch_gemm<128, false, false, tlora::EPI_BF16_MASK, 6>(ma, mb, ma, mb, a, layer->sm_count, s);
+    }
+    // 2) dX = dY·Wᵀ + dH·Aᵀ
+    if (dX) {
+      GemmArgs a{};
+      a.tiles = plan->tiles[TLORA_L_DX].p;
+      a.num_tiles = (int)plan->P.tiles[TLORA_L_DX].size();
+      a.M = (int)T;
+      a.N = (int)d;
+      a.out = dX;
+      a.ldo = d;
+      const CUtensorMap ma0 = tmap_k(dY, k, T, tlora::kBM);
+      const CUtensorMap mb0 = tmap_k(layer->W16.p, k, d, 256);
+      const CUtensorMap ma1 = tmap_k(dH, R, T, tlora::kBM);
+      const CUtensorMap mb1 = tmap_k(layer->Acat.p, R, d, 256);
+      launch_gemm<256, false, false, tlora::EPI_BF16, 4>(ma0, mb0, ma1, mb1, a, layer->sm_count, s);
+    }
+    // 3) dBcat = Hᵀ·dY and 4) dAᵀcat = dHᵀ·X over each rank tile's token range
+    for (int which = 0; which < 2; ++which) {
+      const int launch = which == 0 ? TLORA_L_DB : TLORA_L_DA;
+      const int64_t N = which == 0 ? k : d;
+      const int nsplit = which == 0 ? plan->P.splits_db : plan->P.splits_da;
+      float* grads = which == 0 ? layer->dB.p : layer->dAT.p;
+      GemmArgs a{};
+      a.tiles = plan->tiles[launch].p;
+      a.num_tiles = (int)plan->P.tiles[launch].size();
+      a.M = (int)R;
+      a.N = (int)N;
+      a.ldo = N;
+      if (nsplit > 1) {
+        a.out = plan->partial.p;
+        a.split_stride = R * N;
+        a.beta = 0.f;
+      } else {
+        a.out = grads;
+        a.beta = beta;
+      }
+      const CUtensorMap ma = tmap_mn(which == 0 ? H_stash : (const void*)dH, R, T);
+      const CUtensorMap mb = tmap_mn(which == 0 ? dY : X, N, T);
+      launch_gemm<128, true, true, tlora::EPI_F32, 6>(ma, mb, ma, mb, a, layer->sm_count, s);
+      if (nsplit > 1) {
+        const int32_t* cnt = which == 0 ? plan->cnt_db.p : plan->cnt_da.p;
+        const int64_t work = R * N / 4;
+        const int blocks = (int)std::min<int64_t>(tlora::ceil_div(work, 256), 4 * layer->sm_count);
+        reduce_splits_kernel<<<blocks, 256, 0, s>>>(plan->partial.p, R * N, cnt, R, N, beta, grads);
+        TL_CUDA(cudaGetLastError());
+      }
+    }
+  });
+}
+
+int tlora_op_cost(int64_t tokens, int64_t d, int64_t k, int32_t num_slots,
+                  const int64_t* tokens_per_slot, const int32_t* ranks, int fused, double* flops,
+                  double* bytes_moved, long long* kernel_launches) {
+  return guarded([&] {
+    require(num_slots >= 0 && (num_slots == 0 || (tokens_per_slot && ranks)), TLORA_ERR_ARG,
+            "bad slot arrays");
+    // fused_lora.hpp:95-100 / :148-151 — identical operation order, so bit-identical doubles
+    const double T = static_cast<double>(tokens);
+    const double dd = static_cast<double>(d), kk = static_cast<double>(k);
+    double f = 2.0 * T * dd * kk;
+    double b = 8.0 * (T * dd + dd * kk + T * kk);
+    long long l = 1;
+    for (int s = 0; s < num_slots; ++s) {
+      if (tokens_per_slot[s] == 0) continue;  // fused_lora.hpp:104 / :154
+      const double n = static_cast<double>(tokens_per_slot[s]);
+      const double r = static_cast<double>(ranks[s]);
+      f += 2.0 * n * dd * r + 2.0 * n * r * kk;
+      if (fused) {
+        b += 8.0 * (dd * r + r * kk + 2.0 * n * r);  // :116
+      } else {
+        b += 8.0 * (2.0 * n * dd + dd * r + r * kk + 4.0 * n * r + 2.0 * n * kk);  // :159
+        l += 4;                                                                  // :160
+      }
+    }
+    if (flops) *flops = f;
+    if (bytes_moved) *bytes_moved = b;
+    if (kernel_launches) *kernel_launches = l;
+  });
+}
+
+int tlora_partition(int32_t group_batch, int32_t n, int32_t* n_out, int32_t* per_nano) {
+  return guarded([&] {
+    // nano_pipeline.hpp:51-60
+    if (group_batch < 1) throw std::invalid_argument("partition: group_batch must be >= 1");
+    if (n < 1) throw std::invalid_argument("partition: N must be >= 1");
+    const int32_t nn = std::min(n, group_batch);
+    const int32_t base = group_batch / nn, extra = group_batch % nn;
+    if (n_out) *n_out = nn;
+    if (per_nano)
+      for (int32_t i = 0; i < nn; ++i) per_nano[i] = base + (i < extra ? 1 : 0);
+  });
+}
+
+int tlora_aimd_step(int32_t* n, int32_t* has_prev, double* t_prev, int32_t alpha, double beta,
+                    double tau_rel, double t_t) {
+  return guarded([&] {
+    require(n && has_prev && t_prev, TLORA_ERR_ARG, "null AIMD state");
+    // nano_pipeline.hpp:43-46 (validate) and :99-112
+    if (*n < 1 || alpha < 1 || beta <= 0.0 || beta >= 1.0 || tau_rel < 0.0)
+      throw std::invalid_argument("AimdState: invalid controller parameters");
+    if (t_t < 0.0) throw std::invalid_argument("aimd_step: negative iteration time");
+    int32_t next = *n;
+    if (*has_prev) {
+      const double margin = tau_rel * (*t_prev);
+      if (t_t <= *t_prev - margin)
+        next = *n + alpha;
+      else
+        next = std::max(1, static_cast<int>(std::floor(beta * *n)));
+    }
+    *n = next;
+    *has_prev = 1;
+    *t_prev = t_t;
+  });
+}
+
+}  // extern "C"

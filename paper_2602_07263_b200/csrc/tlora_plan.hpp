@@ -1,0 +1,176 @@
+// tlora_plan.hpp — host-side rank-aware tile packer (pure C++, no CUDA).
+//
+// Given the registry layout (rank r_s and packed column offset off_s of every slot,
+// slots in reference adapter order = std::map by job_id, fused_lora.hpp:48-53) and the
+// owning slot of every token (TokenBatch::segment_map, fused_lora.hpp:28-31), build the
+// tile tables of the six launches of one fused fwd+bwd:
+//
+//   packed rank space: slot s owns columns [off_s, off_s + r_s), off_{s+1} = off_s +
+//   round_up(r_s, 8). Jobs of rank 8..128 therefore share 64-wide K blocks instead of
+//   each padding to a full MMA tile.  For an M-tile of 128 tokens the K-extension of the
+//   fused GEMM covers only [floor64(off_min), ceil64(off_max + r_max)) of the slots
+//   present in that tile — for job-contiguous batches one or two jobs' ranks.
+//
+// Because H (and dH) are masked to each token's own columns, any K-range that is a
+// superset of a tile's own columns gives the exact result; the plan only decides how
+// much zero work is issued.  The plan is deterministic and bit-exactly checkable
+// (tests/test_plan.py re-derives it from oracle/tlora_oracle.c).
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace tlora {
+
+struct PlanTile {
+  int32_t m0, n0, kb0, ke0, kb1, ke1, split, pad;
+};
+
+struct RegistryLayout {
+  int64_t d = 0, k = 0;
+  std::vector<int32_t> rank;    // per slot
+  std::vector<int32_t> offset;  // per slot, packed rank column offset
+  int32_t R = 0;                // packed rank columns (multiple of 8)
+
+  static RegistryLayout make(int64_t d, int64_t k, const std::vector<int32_t>& ranks) {
+    RegistryLayout L;
+    L.d = d;
+    L.k = k;
+    L.rank = ranks;
+    int32_t off = 0;
+    for (int32_t r : ranks) {
+      L.offset.push_back(off);
+      off += (r + 7) / 8 * 8;
+    }
+    L.R = std::max<int32_t>(off, 8);
+    return L;
+  }
+};
+
+constexpr int kPlanBM = 128;      // MMA M tile (tokens or packed-rank rows)
+constexpr int kPlanBK = 64;       // K block
+constexpr int kPlanBNBase = 256;  // N tile of the fused base GEMMs (fwd, dX)
+constexpr int kPlanBNLow = 128;   // N tile of the low-rank launches (shrink, dH, dA, dB)
+constexpr int kPlanGradTargetTiles = 2 * 148;  // split-K target for the gradient launches
+constexpr int kPlanMinSplitTokens = 512;
+
+struct PlanTables {
+  int64_t T = 0;
+  std::vector<PlanTile> tiles[6];  // indexed by tlora_launch
+  std::vector<int32_t> split_count_db, split_count_da;  // per 128-row packed-rank tile
+  int32_t splits_db = 1, splits_da = 1;
+  int64_t useful_ext_cols = 0, packed_ext_cols = 0;
+  std::vector<int32_t> slot_col_lo, slot_col_hi;  // per slot: [off, off + r)
+  std::vector<int64_t> slot_first, slot_last;     // per slot token range, -1 if absent
+};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Gradient launches (dB: N = k, dA: N = d): rows = packed rank space, K = tokens.
+inline void build_grad_tiles(const RegistryLayout& L, const PlanTables& P, int64_t N,
+                             std::vector<PlanTile>& out, std::vector<int32_t>& split_cnt,
+                             int32_t& max_split) {
+  const int64_t n_rt = ceil_div(L.R, kPlanBM);
+  const int64_t n_nt = ceil_div(N, kPlanBNLow);
+  const int64_t target_split = std::max<int64_t>(1, ceil_div(kPlanGradTargetTiles, n_rt * n_nt));
+  max_split = 1;
+  split_cnt.assign(n_rt, 1);
+  for (int64_t rt = 0; rt < n_rt; ++rt) {
+    const int64_t r0 = rt * kPlanBM, r1 = r0 + kPlanBM;
+    int64_t tlo = -1, thi = -1;
+    for (size_t s = 0; s < L.rank.size(); ++s) {
+      const int64_t c0 = L.offset[s], c1 = c0 + L.rank[s];
+      if (c1 <= r0 || c0 >= r1 || P.slot_first[s] < 0) continue;
+      tlo = tlo < 0 ? P.slot_first[s] : std::min(tlo, P.slot_first[s]);
+      thi = std::max(thi, P.slot_last[s] + 1);
+    }
+    if (tlo < 0) {  // no token touches these rank rows: empty-K tiles write zeros
+      for (int64_t nt = 0; nt < n_nt; ++nt)
+        out.push_back({(int32_t)r0, (int32_t)(nt * kPlanBNLow), 0, 0, 0, 0, 0, 0});
+      continue;
+    }
+    const int64_t len = thi - tlo;
+    const int64_t nsplit =
+        std::max<int64_t>(1, std::min(target_split, len / kPlanMinSplitTokens));
+    const int64_t chunk = ceil_div(ceil_div(len, nsplit), kPlanBK) * kPlanBK;
+    int32_t used = 0;
+    for (int64_t s = 0; s < nsplit; ++s) {
+      const int64_t kb = tlo + s * chunk, ke = std::min(thi, kb + chunk);
+      if (kb >= ke) break;
+      for (int64_t nt = 0; nt < n_nt; ++nt)
+        out.push_back({(int32_t)r0, (int32_t)(nt * kPlanBNLow), (int32_t)kb, (int32_t)ke, 0, 0,
+                       (int32_t)s, 0});
+      ++used;
+    }
+    split_cnt[rt] = used;
+    max_split = std::max(max_split, used);
+  }
+}
+
+inline PlanTables build_plan(const RegistryLayout& L, int64_t T, const int32_t* token_slot) {
+  PlanTables P;
+  P.T = T;
+  const int S = (int)L.rank.size();
+  for (int64_t t = 0; t < T; ++t)
+    if (token_slot[t] < 0 || token_slot[t] >= S)
+      throw std::out_of_range("token " + std::to_string(t) + " has slot " +
+                              std::to_string(token_slot[t]) + " with no adapter");
+  P.slot_col_lo.resize(S);
+  P.slot_col_hi.resize(S);
+  for (int s = 0; s < S; ++s) {
+    P.slot_col_lo[s] = L.offset[s];
+    P.slot_col_hi[s] = L.offset[s] + L.rank[s];
+  }
+  P.slot_first.assign(S, -1);
+  P.slot_last.assign(S, -1);
+  for (int64_t t = 0; t < T; ++t) {
+    const int s = token_slot[t];
+    if (P.slot_first[s] < 0) P.slot_first[s] = t;
+    P.slot_last[s] = t;
+  }
+
+  const int64_t n_mt = ceil_div(T, kPlanBM);
+  std::vector<int32_t> c_lo(n_mt), c_hi(n_mt);
+  for (int64_t m = 0; m < n_mt; ++m) {
+    const int64_t t0 = m * kPlanBM, t1 = std::min(T, t0 + kPlanBM);
+    int smin = S, smax = -1;
+    std::vector<char> present(S, 0);
+    for (int64_t t = t0; t < t1; ++t) {
+      const int s = token_slot[t];
+      smin = std::min(smin, s);
+      smax = std::max(smax, s);
+      present[s] = 1;
+    }
+    c_lo[m] = L.offset[smin] / kPlanBK * kPlanBK;
+    c_hi[m] = (int32_t)(ceil_div(L.offset[smax] + L.rank[smax], kPlanBK) * kPlanBK);
+    for (int s = 0; s < S; ++s)
+      if (present[s]) P.useful_ext_cols += L.rank[s];
+    P.packed_ext_cols += c_hi[m] - c_lo[m];
+  }
+
+  // shrink / dH: per M-tile, N-tiles over that tile's packed rank window
+  for (int which = 0; which < 2; ++which) {
+    const int64_t K = which == 0 ? L.d : L.k;
+    auto& v = P.tiles[which == 0 ? 0 : 2];
+    for (int64_t m = 0; m < n_mt; ++m)
+      for (int32_t n0 = c_lo[m]; n0 < c_hi[m]; n0 += kPlanBNLow)
+        v.push_back({(int32_t)(m * kPlanBM), n0, 0, (int32_t)K, 0, 0, 0, 0});
+  }
+  // fused base GEMMs: fwd (N = k, K = d) and dX (N = d, K = k), K-extension = window
+  for (int which = 0; which < 2; ++which) {
+    const int64_t N = which == 0 ? L.k : L.d;
+    const int64_t K = which == 0 ? L.d : L.k;
+    auto& v = P.tiles[which == 0 ? 1 : 3];
+    for (int64_t m = 0; m < n_mt; ++m)
+      for (int64_t n = 0; n < ceil_div(N, kPlanBNBase); ++n)
+        v.push_back({(int32_t)(m * kPlanBM), (int32_t)(n * kPlanBNBase), 0, (int32_t)K, c_lo[m],
+                     c_hi[m], 0, 0});
+  }
+  build_grad_tiles(L, P, L.k, P.tiles[4], P.split_count_db, P.splits_db);
+  build_grad_tiles(L, P, L.d, P.tiles[5], P.split_count_da, P.splits_da);
+  return P;
+}
+
+}  // namespace tlora

@@ -1,0 +1,234 @@
+"""Torch-facing wrapper of the fused multi-LoRA layer (C-ABI in include/tlora.h).
+
+PyTorch is only plumbing here: device memory, streams and the process group. All
+arithmetic on the path runs in the sm_100a kernels of libtlora.so.
+
+Reference semantics: proj/include/lora_fleet/fused_lora.hpp:84-119 (forward; backward
+is new — the reference has none).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import capi
+from .capi import call
+
+
+def _stream_ptr(stream) -> C.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ view over a device pointer owned by the library."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {
+            "shape": tuple(shape), "typestr": typestr, "data": (ptr, False), "version": 3,
+            "strides": None,
+        }
+
+
+_DT = {torch.float64: capi.F64, torch.float32: capi.F32, torch.bfloat16: capi.BF16}
+
+
+@dataclass
+class PlanInfo:
+    tokens: int
+    d: int
+    k: int
+    num_slots: int
+    rank_pad_total: int
+    num_tiles: tuple
+    splits_db: int
+    splits_da: int
+    useful_ext_cols: int
+    packed_ext_cols: int
+
+
+class Plan:
+    """Rank-aware tile-packing / indexing plan of one (nano-)batch (opaque, immutable)."""
+
+    def __init__(self, layer: "FusedLoRALayer", token_slot: Sequence[int]):
+        ts = np.ascontiguousarray(np.asarray(token_slot, dtype=np.int32))
+        self.layer = layer
+        self.tokens = int(ts.shape[0])
+        self.token_slot = ts
+        h = C.c_void_p()
+        call("tlora_plan_create", layer._h, self.tokens,
+             ts.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(h))
+        self._h = h
+
+    def info(self) -> PlanInfo:
+        i = capi.PlanInfoC()
+        call("tlora_plan_get_info", self._h, C.byref(i))
+        return PlanInfo(i.tokens, i.d, i.k, i.num_slots, i.rank_pad_total, tuple(i.num_tiles),
+                        i.splits_db, i.splits_da, i.useful_ext_cols, i.packed_ext_cols)
+
+    def tiles(self, launch: int) -> np.ndarray:
+        n = C.c_int32()
+        call("tlora_plan_get_tiles", self._h, launch, None, 0, C.byref(n))
+        buf = (capi.TileC * max(1, n.value))()
+        call("tlora_plan_get_tiles", self._h, launch, buf, n.value, C.byref(n))
+        arr = np.frombuffer(buf, dtype=np.int32).reshape(-1, 8)[: n.value]
+        return arr.copy()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            capi.lib().tlora_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class FusedLoRALayer:
+    """One adapted projection of the Shared Super-Model: frozen W (d x k) + per-job adapters.
+
+    Slots follow the reference adapter order (std::map by job_id, fused_lora.hpp:48-53).
+    """
+
+    def __init__(self, d: int, k: int, ranks: Sequence[int], device: int = 0):
+        self.d, self.k, self.device = int(d), int(k), int(device)
+        self.ranks = [int(r) for r in ranks]
+        rk = (C.c_int32 * len(self.ranks))(*self.ranks)
+        h = C.c_void_p()
+        call("tlora_layer_create", self.device, self.d, self.k, len(self.ranks), rk, C.byref(h))
+        self._h = h
+        offs = (C.c_int32 * len(self.ranks))()
+        R = C.c_int32()
+        call("tlora_layer_layout", self._h, offs, C.byref(R))
+        self.offsets = list(offs)
+        self.R = R.value
+
+    # ---------------------------------------------------------------- registry
+    def set_base(self, W: torch.Tensor, stream=None):
+        W = W.contiguous()
+        assert tuple(W.shape) == (self.d, self.k)
+        where = capi.DEVICE if W.is_cuda else capi.HOST
+        call("tlora_layer_set_base", self._h, _ptr(W), _DT[W.dtype], where, _stream_ptr(stream))
+
+    def set_adapter(self, slot: int, A: torch.Tensor, B: torch.Tensor, stream=None):
+        A, B = A.contiguous(), B.contiguous()
+        assert A.dtype == B.dtype and A.is_cuda == B.is_cuda
+        where = capi.DEVICE if A.is_cuda else capi.HOST
+        call("tlora_layer_set_adapter", self._h, int(slot), _ptr(A), _ptr(B), _DT[A.dtype], where,
+             _stream_ptr(stream))
+
+    def zero_grad(self, stream=None):
+        call("tlora_layer_zero_grad", self._h, _stream_ptr(stream))
+
+    def packed_grads(self):
+        """(dAᵀcat [R x d], dBcat [R x k]) fp32 device tensors aliasing the layer's buffers."""
+        a, b = C.c_void_p(), C.c_void_p()
+        call("tlora_layer_grad_ptrs", self._h, C.byref(a), C.byref(b))
+        dev = torch.device("cuda", self.device)
+        dAT = torch.as_tensor(_CudaArray(a.value, (self.R, self.d), "<f4"), device=dev)
+        dB = torch.as_tensor(_CudaArray(b.value, (self.R, self.k), "<f4"), device=dev)
+        return dAT, dB
+
+    def read_grad(self, slot: int, stream=None):
+        r = self.ranks[slot]
+        dev = torch.device("cuda", self.device)
+        dA = torch.empty(self.d, r, dtype=torch.float32, device=dev)
+        dB = torch.empty(r, self.k, dtype=torch.float32, device=dev)
+        call("tlora_layer_read_grad", self._h, int(slot), _ptr(dA), _ptr(dB), capi.DEVICE,
+             _stream_ptr(stream))
+        return dA, dB
+
+    # ---------------------------------------------------------------- compute
+    def plan(self, token_slot: Sequence[int]) -> Plan:
+        return Plan(self, token_slot)
+
+    def forward(self, plan: Plan, X: torch.Tensor, Y: torch.Tensor | None = None,
+                H: torch.Tensor | None = None, y_dtype=torch.bfloat16, stream=None):
+        T = plan.tokens
+        assert X.dtype == torch.bfloat16 and X.is_contiguous() and tuple(X.shape) == (T, self.d)
+        if Y is None:
+            Y = torch.empty(T, self.k, dtype=y_dtype, device=X.device)
+        if H is None:
+            H = torch.empty(T, self.R, dtype=torch.bfloat16, device=X.device)
+        call("tlora_forward", self._h, plan._h, _ptr(X), _ptr(Y), _DT[Y.dtype], _ptr(H),
+             _stream_ptr(stream))
+        return Y, H
+
+    def backward(self, plan: Plan, dY: torch.Tensor, X: torch.Tensor, H: torch.Tensor,
+                 dX: torch.Tensor | None | bool = True, beta: float = 0.0, stream=None):
+        T = plan.tokens
+        assert dY.dtype == torch.bfloat16 and tuple(dY.shape) == (T, self.k)
+        if dX is True:
+            dX = torch.empty(T, self.d, dtype=torch.bfloat16, device=dY.device)
+        elif dX is False:
+            dX = None
+        call("tlora_backward", self._h, plan._h, _ptr(dY), _ptr(X), _ptr(H), _ptr(dX),
+             C.c_float(beta), _stream_ptr(stream))
+        return dX
+
+    def close(self):
+        if getattr(self, "_h", None):
+            capi.lib().tlora_layer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def op_cost(tokens: int, d: int, k: int, tokens_per_slot, ranks, fused: bool = True):
+    """Reference OpCost (fused_lora.hpp:95-116 fused, :139-163 unfused), bit-identical."""
+    n = len(ranks)
+    tp = (C.c_int64 * n)(*[int(x) for x in tokens_per_slot])
+    rk = (C.c_int32 * n)(*[int(x) for x in ranks])
+    f, b, l = C.c_double(), C.c_double(), C.c_longlong()
+    call("tlora_op_cost", int(tokens), int(d), int(k), n, tp, rk, int(bool(fused)), C.byref(f),
+         C.byref(b), C.byref(l))
+    return f.value, b.value, l.value
+
+
+def partition(group_batch: int, n: int):
+    """nano_pipeline.hpp:51-60 — returns (n, per_nano_samples)."""
+    out_n = C.c_int32()
+    buf = (C.c_int32 * max(1, min(max(n, 1), max(group_batch, 1))))()
+    code = capi.lib().tlora_partition(int(group_batch), int(n), C.byref(out_n), buf)
+    if code == capi.ERR_PLAN:
+        raise ValueError(capi.lib().tlora_last_error().decode())
+    capi.check(code)
+    return out_n.value, list(buf)[: out_n.value]
+
+
+@dataclass
+class AimdState:
+    """nano_pipeline.hpp:36-47 (defaults n=4, alpha=4, beta=0.5, tau_rel=0)."""
+    n: int = 4
+    t_prev: float | None = None
+    alpha: int = 4
+    beta: float = 0.5
+    tau_rel: float = 0.0
+
+
+def aimd_step(state: AimdState, t_t: float) -> AimdState:
+    """nano_pipeline.hpp:99-112, via the C-ABI (bit-exact)."""
+    n = C.c_int32(state.n)
+    hp = C.c_int32(0 if state.t_prev is None else 1)
+    tp = C.c_double(0.0 if state.t_prev is None else state.t_prev)
+    code = capi.lib().tlora_aimd_step(C.byref(n), C.byref(hp), C.byref(tp), state.alpha,
+                                      state.beta, state.tau_rel, float(t_t))
+    if code == capi.ERR_PLAN:
+        raise ValueError(capi.lib().tlora_last_error().decode())
+    capi.check(code)
+    return AimdState(n.value, tp.value, state.alpha, state.beta, state.tau_rel)
