@@ -2,8 +2,8 @@
 # Usage: make            (library + oracle)
 #        make ref        (reference-built golden-vector tool, needs /root/reference)
 NVCC     ?= nvcc
-CXX      ?= g++
-CC       ?= gcc
+CXX      := g++
+CC       := gcc
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 PKG      := paper_2602_07263_b200

@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""bench.py — aggregate LoRA training tokens/s of the fused multi-LoRA layer on B200.
+
+Contract (see task / DESIGN.md §Measurement):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+One step = fwd+bwd of every adapted projection of the configured layer set over the
+whole multi-job token batch (BASELINE.json configs[1] = C2 by default). Rank 0 prints
+ONE JSON line. Under torchrun each rank runs one GPU (weak scaling: data-parallel
+replicas, adapter-gradient all-reduce over NCCL — the path's only exchange step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "aggregate LoRA training tokens/sec (all jobs) at 1/2/4/8 B200; tensor-pipe %"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                  "source": "fallback (B200_PROFILING.md)"}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    return dict(FALLBACK_PEAKS)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.out, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.out.flush()
+        rows = []
+        for line in Path(self.out.name).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.out.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------ CPU arm
+def cpu_reference_sample(wl, tokens_per_job: int, seconds_budget: float, threads: int):
+    """Time the reference CPU implementation of the path on a bounded sample.
+
+    Uses oracle/_ref/ref_bench (the UNMODIFIED reference fused_forward compiled against
+    a self-written Eigen-subset header; backward restated with the same GEMM shim, since
+    the reference has none) when present, else the oracle port (oracle/liboracle.so).
+    Returns dict(value tokens/s, cores, kind, sample) or None.
+    """
+    from paper_2602_07263_b200 import cpu_baseline
+    return cpu_baseline.measure(wl, tokens_per_job=tokens_per_job, seconds_budget=seconds_budget,
+                                threads=threads)
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2602_07263_b200 import capi
+    from paper_2602_07263_b200.runner import LayerSetStep
+    from paper_2602_07263_b200.workload import config
+    import ctypes as C
+
+    torch.cuda.set_device(local_rank)
+    capi.call("tlora_device_check", local_rank, None)
+    wl = config(args.config)
+    step = LayerSetStep(wl, device=local_rank, seed=wl.seed + rank, shuffle=args.shuffle)
+    stream = torch.cuda.current_stream()
+
+    comm_stream = torch.cuda.Stream() if world > 1 else None
+    pending = []
+
+    def allreduce_grads(name, layer):
+        # DP replicas: all-reduce this projection's packed fp32 adapter grads on a comm
+        # stream while the next projection's backward runs.
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        with torch.cuda.stream(comm_stream):
+            comm_stream.wait_event(ev)
+            dAT, dB = layer.packed_grads()
+            pending.append(dist.all_reduce(dAT, async_op=True))
+            pending.append(dist.all_reduce(dB, async_op=True))
+
+    def one_step():
+        step.step(stream=stream, on_layer_done=allreduce_grads if world > 1 else None)
+        if world > 1:
+            for w in pending:
+                w.wait()
+            pending.clear()
+            stream.wait_stream(comm_stream)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    lib = capi.lib()
+    n0 = lib.tlora_launch_count()
+    capi.call("tlora_profile_begin")
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n_launch = lib.tlora_launch_count() - n0
+    cnt = (C.c_int32 * 6)()
+    ms6 = (C.c_double * 6)()
+    fl6 = (C.c_double * 6)()
+    capi.call("tlora_profile_end", cnt, ms6, fl6)
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    ms_per_step = ms / args.steps
+    tokens = wl.tokens * world
+    value = tokens / (ms_per_step / 1e3)
+
+    # ---- e2e: the same step through the public API with HOST buffers: H2D of every
+    # input (activations + upstream grads) from pinned memory and D2H of the gradients.
+    host_in = [t.cpu().pin_memory() for t in step.input_tensors()]
+    dev_in = step.input_tensors()
+    grads = [g for lay in step.layers.values() for g in lay.packed_grads()]
+    host_out = [torch.empty(g.shape, dtype=g.dtype, pin_memory=True) for g in grads]
+    h2d = sum(t.numel() * t.element_size() for t in host_in)
+    d2h = sum(t.numel() * t.element_size() for t in host_out)
+
+    def e2e_step():
+        for h, d in zip(host_in, dev_in):
+            d.copy_(h, non_blocking=True)
+        one_step()
+        for g, h in zip(grads, host_out):
+            h.copy_(g, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(2, min(args.steps, 10))
+    f0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+
+    # ---- roofline of the dominant kernel family: the fused base+LoRA GEMM (fwd and dX)
+    peaks = load_peaks()
+    fam_ms = ms6[capi.L_FWD] + ms6[capi.L_DX]
+    fam_fl = fl6[capi.L_FWD] + fl6[capi.L_DX]
+    achieved = fam_fl / (fam_ms / 1e3) / 1e12 if fam_ms > 0 else 0.0
+    peak = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+    total_ms = sum(ms6)
+    per_launch = {capi.LAUNCH_NAMES[i]: {
+        "launches": cnt[i], "ms_total": round(ms6[i], 3),
+        "tflops": round(fl6[i] / (ms6[i] / 1e3) / 1e12, 1) if ms6[i] > 0 else None,
+        "share_of_gemm_time": round(ms6[i] / total_ms, 4) if total_ms > 0 else None}
+        for i in range(6)}
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("fwd_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak else None,
+                "frac_of_burst": round(achieved / float(peaks["bf16_tflops"]), 4),
+                "traffic": traffic, "kernel": "lora_gemm_kernel<256,K,K> (fwd + dX)",
+                "peak_source": peaks["source"] + " sustained bf16", "per_launch": per_launch}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_sample(wl, tokens_per_job=args.cpu_tokens_per_job,
+                                   seconds_budget=args.cpu_seconds, threads=os.cpu_count() or 1)
+
+    flops_step = wl.flops_fwd_bwd() * world
+    out = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded normal activations/grads, random-init W and adapters)",
+        "config": {"workload": f"{wl.name}: {wl.notes}", "tokens_per_gpu": wl.tokens,
+                   "jobs": [[j.job_id, j.rank, j.tokens] for j in wl.jobs],
+                   "projections": wl.projections, "token_order": "shuffled" if args.shuffle else "job-contiguous",
+                   "parallelism": f"dp{world}", "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)",
+                   "algorithmic_tflop_per_step": round(flops_step / 1e12, 3),
+                   "achieved_tflops_step": round(flops_step / (ms_per_step / 1e3) / 1e12, 1)},
+        "e2e": {"value": round(tokens / (e2e_ms / 1e3), 1), "unit": "tokens/s",
+                "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "path": "host pinned inputs -> tlora C-ABI fwd/bwd -> host grads"},
+        "gpu_launches": int(n_launch),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+    }
+    return out
+
+
+def run_reference(args, rank, world):
+    from paper_2602_07263_b200.workload import config
+    wl = config(args.config)
+    if rank != 0:
+        return None
+    from paper_2602_07263_b200 import cpu_baseline
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_baseline.measure(wl, tokens_per_job=args.ref_tokens_per_job, seconds_budget=0.0,
+                             threads=threads, repeats=1)
+    t0 = time.perf_counter()
+    res = None
+    tokens = 0
+    for _ in range(args.steps):
+        res = cpu_baseline.measure(wl, tokens_per_job=args.ref_tokens_per_job, seconds_budget=0.0,
+                                   threads=threads, repeats=1)
+        if res is None:
+            break
+        tokens += res["tokens"]
+    dt = time.perf_counter() - t0
+    if res is None:
+        return {"impl": "reference", "unavailable": "reference CPU build missing (run make ref)"}
+    value = tokens / dt
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": res["dtype"],
+        "data": "synthetic (seeded normal)",
+        "config": {"workload": f"{wl.name}: {wl.notes}", "sample": res["sample"]},
+        "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": res["cores"],
+                         "kind": res["kind"], "sample": res["sample"]},
+        "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--shuffle", action="store_true", help="interleave jobs' tokens")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-tokens-per-job", type=int, default=4)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-tokens-per-job", type=int, default=2)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if rank == 0 and out is not None:
+            print(json.dumps(out), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -115,6 +115,13 @@ int tlora_plan_get_info(const tlora_plan* plan, tlora_plan_info* info);
 int tlora_plan_get_tiles(const tlora_plan* plan, int launch, tlora_tile* out, int32_t cap,
                          int32_t* count);
 
+/* Host-only plan builder (no device needed): the same tile table tlora_plan_create
+ * uploads, for the registry layout `ranks` and the token->slot map. For bit-exact checks
+ * against the plan oracle and for planning on a host without a GPU. */
+int tlora_plan_tiles_host(int64_t d, int64_t k, int32_t num_slots, const int32_t* ranks,
+                          int64_t tokens, const int32_t* token_slot, int launch, tlora_tile* out,
+                          int32_t cap, int32_t* count);
+
 /* ---- compute (enqueue-only) ----------------------------------------------------- */
 /* Forward: Y = X·W + scatter_j((X_j·A_j)·B_j). X: T x d bf16, Y: T x k (bf16 or f32),
  * H_stash: T x R bf16 (the per-token low-rank intermediate, kept for backward). */
@@ -125,6 +132,16 @@ int tlora_forward(tlora_layer* layer, const tlora_plan* plan, const void* X, voi
  * dY: T x k bf16, X: T x d bf16, H_stash from tlora_forward. */
 int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, const void* X,
                    const void* H_stash, void* dX, float beta, void* stream);
+
+/* ---- live launch profiling (CUDA events on each launch's own stream) ------------- */
+/* Between begin and end every GEMM launch is bracketed by CUDA events. end() waits for
+ * them and returns, per tlora_launch kind, the launch count, summed device ms and the
+ * summed algorithmic FLOPs (padding and packing waste excluded). Arrays have
+ * TLORA_L_COUNT entries; any may be NULL. */
+int tlora_profile_begin(void);
+/* Total number of kernels this library has enqueued since load (monotonic). */
+long long tlora_launch_count(void);
+int tlora_profile_end(int32_t* counts, double* total_ms, double* total_flops);
 
 /* ---- reference cost model (bit-identical to fused_lora.hpp:95-116, :139-163) ----- */
 /* tokens_per_slot[num_slots], ranks[num_slots], in reference adapter order. */

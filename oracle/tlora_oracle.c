@@ -1,0 +1,323 @@
+/*
+ * tlora_oracle.c — CPU oracle for the fused multi-LoRA layer. TEST INFRASTRUCTURE ONLY.
+ * See tlora_oracle.h for the contract and the parity pinning. Each function cites the
+ * reference lines it restates (paths relative to /root/reference/proj/include/lora_fleet).
+ */
+#include "tlora_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+double orc_round_bf16(double x) {
+  float f = (float)x;
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return (double)f; /* inf / nan */
+  const uint32_t lsb = (u >> 16) & 1u;
+  u += 0x7fffu + lsb;
+  u &= 0xffff0000u;
+  memcpy(&f, &u, 4);
+  return (double)f;
+}
+
+/* rows of slot s, ascending (fused_lora.hpp:56-61) */
+static int64_t segment_rows(int64_t T, const int32_t* slot, int32_t s, int64_t* rows) {
+  int64_t n = 0;
+  for (int64_t t = 0; t < T; ++t)
+    if (slot[t] == s) rows[n++] = t;
+  return n;
+}
+
+static int check_slots(int64_t T, int32_t S, const int32_t* slot) {
+  for (int64_t t = 0; t < T; ++t)
+    if (slot[t] < 0 || slot[t] >= S) return -1; /* fused_lora.hpp:72-73 */
+  return 0;
+}
+
+/* C[m x n] = A[m x p] · B[p x n], row-major, OpenMP over rows */
+static void gemm_nn(int64_t m, int64_t p, int64_t n, const double* A, const double* B, double* C) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < m; ++i) {
+    double* c = C + i * n;
+    for (int64_t j = 0; j < n; ++j) c[j] = 0.0;
+    for (int64_t q = 0; q < p; ++q) {
+      const double a = A[i * p + q];
+      const double* b = B + q * n;
+      for (int64_t j = 0; j < n; ++j) c[j] += a * b[j];
+    }
+  }
+}
+
+/* C[m x n] = A[m x p] · B[n x p]ᵀ */
+static void gemm_nt(int64_t m, int64_t p, int64_t n, const double* A, const double* B, double* C) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double acc = 0.0;
+      const double* a = A + i * p;
+      const double* b = B + j * p;
+      for (int64_t q = 0; q < p; ++q) acc += a[q] * b[q];
+      C[i * n + j] = acc;
+    }
+}
+
+/* C[p x n] = A[m x p]ᵀ · B[m x n] */
+static void gemm_tn(int64_t m, int64_t p, int64_t n, const double* A, const double* B, double* C) {
+#pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < p; ++q) {
+    double* c = C + q * n;
+    for (int64_t j = 0; j < n; ++j) c[j] = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+      const double a = A[i * p + q];
+      const double* b = B + i * n;
+      for (int64_t j = 0; j < n; ++j) c[j] += a * b[j];
+    }
+  }
+}
+
+int orc_fused_forward(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t* ranks,
+                      const double* const* A, const double* const* B, const double* X,
+                      const double* W, const int32_t* slot, int32_t round_bf16, double* Y,
+                      double* H) {
+  if (check_slots(T, S, slot)) return -1;
+  int64_t R = 0;
+  for (int32_t s = 0; s < S; ++s) R += ranks[s];
+  gemm_nn(T, d, k, X, W, Y); /* :93 shared base term, computed once */
+  if (H) memset(H, 0, sizeof(double) * (size_t)(T * R));
+  int64_t* rows = (int64_t*)malloc(sizeof(int64_t) * (size_t)(T > 0 ? T : 1));
+  int64_t hoff = 0;
+  for (int32_t s = 0; s < S; ++s) { /* :102 map order */
+    const int64_t n = segment_rows(T, slot, s, rows);
+    const int64_t r = ranks[s];
+    if (n > 0) { /* :104 empty segments skipped */
+      double* g = (double*)malloc(sizeof(double) * (size_t)(n * d));
+      double* mid = (double*)malloc(sizeof(double) * (size_t)(n * r));
+      double* delta = (double*)malloc(sizeof(double) * (size_t)(n * k));
+      for (int64_t i = 0; i < n; ++i) memcpy(g + i * d, X + rows[i] * d, sizeof(double) * d); /* :108-109 */
+      gemm_nn(n, d, r, g, A[s], mid); /* :111 */
+      if (round_bf16)
+        for (int64_t i = 0; i < n * r; ++i) mid[i] = orc_round_bf16(mid[i]);
+      gemm_nn(n, r, k, mid, B[s], delta); /* :112 */
+      for (int64_t i = 0; i < n; ++i) /* :113 scatter-add */
+        for (int64_t j = 0; j < k; ++j) Y[rows[i] * k + j] += delta[i * k + j];
+      if (H)
+        for (int64_t i = 0; i < n; ++i)
+          memcpy(H + rows[i] * R + hoff, mid + i * r, sizeof(double) * r);
+      free(g);
+      free(mid);
+      free(delta);
+    }
+    hoff += r;
+  }
+  free(rows);
+  return 0;
+}
+
+int orc_materialized(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t* ranks,
+                     const double* const* A, const double* const* B, const double* X,
+                     const double* W, const int32_t* slot, double* Y) {
+  if (check_slots(T, S, slot)) return -1;
+  double* Wi = (double*)malloc(sizeof(double) * (size_t)(d * k));
+  for (int32_t s = 0; s < S; ++s) { /* :130-133 */
+    gemm_nn(d, ranks[s], k, A[s], B[s], Wi);
+    for (int64_t i = 0; i < d * k; ++i) Wi[i] += W[i];
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < T; ++t) {
+      if (slot[t] != s) continue;
+      for (int64_t j = 0; j < k; ++j) {
+        double acc = 0.0;
+        for (int64_t q = 0; q < d; ++q) acc += X[t * d + q] * Wi[q * k + j];
+        Y[t * k + j] = acc;
+      }
+    }
+  }
+  free(Wi);
+  return 0;
+}
+
+int orc_fused_backward(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t* ranks,
+                       const double* const* A, const double* const* B, const double* X,
+                       const double* W, const int32_t* slot, const double* dY,
+                       int32_t round_bf16, double* dX, double* const* dA, double* const* dB) {
+  if (check_slots(T, S, slot)) return -1;
+  if (dX) gemm_nt(T, k, d, dY, W, dX); /* dX = dY·Wᵀ */
+  int64_t* rows = (int64_t*)malloc(sizeof(int64_t) * (size_t)(T > 0 ? T : 1));
+  for (int32_t s = 0; s < S; ++s) {
+    const int64_t r = ranks[s];
+    const int64_t n = segment_rows(T, slot, s, rows);
+    if (n == 0) {
+      memset(dA[s], 0, sizeof(double) * (size_t)(d * r));
+      memset(dB[s], 0, sizeof(double) * (size_t)(r * k));
+      continue;
+    }
+    double* xs = (double*)malloc(sizeof(double) * (size_t)(n * d));
+    double* gs = (double*)malloc(sizeof(double) * (size_t)(n * k));
+    double* h = (double*)malloc(sizeof(double) * (size_t)(n * r));
+    double* dh = (double*)malloc(sizeof(double) * (size_t)(n * r));
+    for (int64_t i = 0; i < n; ++i) {
+      memcpy(xs + i * d, X + rows[i] * d, sizeof(double) * d);
+      memcpy(gs + i * k, dY + rows[i] * k, sizeof(double) * k);
+    }
+    gemm_nn(n, d, r, xs, A[s], h);    /* H_j = X_j·A_j (forward intermediate) */
+    gemm_nt(n, k, r, gs, B[s], dh);   /* dH_j = dY_j·B_jᵀ */
+    if (round_bf16)
+      for (int64_t i = 0; i < n * r; ++i) {
+        h[i] = orc_round_bf16(h[i]);
+        dh[i] = orc_round_bf16(dh[i]);
+      }
+    gemm_tn(n, r, k, h, gs, dB[s]);   /* dB_j = H_jᵀ·dY_j */
+    gemm_tn(n, d, r, xs, dh, dA[s]);  /* dA_j = X_jᵀ·dH_j */
+    if (dX) {                         /* dX_j += dH_j·A_jᵀ */
+      double* t = (double*)malloc(sizeof(double) * (size_t)(n * d));
+      gemm_nt(n, r, d, dh, A[s], t);
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < d; ++j) dX[rows[i] * d + j] += t[i * d + j];
+      free(t);
+    }
+    free(xs);
+    free(gs);
+    free(h);
+    free(dh);
+  }
+  free(rows);
+  return 0;
+}
+
+void orc_op_cost(int64_t T, int64_t d, int64_t k, int32_t S, const int64_t* tokens_per_slot,
+                 const int32_t* ranks, int32_t fused, double* flops, double* bytes,
+                 long long* launches) {
+  const double tt = (double)T, dd = (double)d, kk = (double)k;
+  double f = 2.0 * tt * dd * kk;                     /* :96 / :149 */
+  double b = 8.0 * (tt * dd + dd * kk + tt * kk);    /* :97-99 / :150 */
+  long long l = 1;                                   /* :100 / :151 */
+  for (int32_t s = 0; s < S; ++s) {
+    if (tokens_per_slot[s] == 0) continue;           /* :104 / :154 */
+    const double n = (double)tokens_per_slot[s], r = (double)ranks[s];
+    f += 2.0 * n * dd * r + 2.0 * n * r * kk;        /* :115 / :157 */
+    if (fused) {
+      b += 8.0 * (dd * r + r * kk + 2.0 * n * r);    /* :116 */
+    } else {
+      b += 8.0 * (2.0 * n * dd + dd * r + r * kk + 4.0 * n * r + 2.0 * n * kk); /* :159 */
+      l += 4;                                        /* :160 */
+    }
+  }
+  *flops = f;
+  *bytes = b;
+  *launches = l;
+}
+
+int orc_partition(int32_t group_batch, int32_t n, int32_t* n_out, int32_t* per_nano) {
+  if (group_batch < 1 || n < 1) return -1; /* :52-53 */
+  const int32_t nn = n < group_batch ? n : group_batch;
+  *n_out = nn;
+  for (int32_t i = 0; i < nn; ++i) per_nano[i] = group_batch / nn + (i < group_batch % nn ? 1 : 0);
+  return 0;
+}
+
+int orc_aimd_step(int32_t* n, int32_t* has_prev, double* t_prev, int32_t alpha, double beta,
+                  double tau_rel, double t_t) {
+  if (*n < 1 || alpha < 1 || beta <= 0.0 || beta >= 1.0 || tau_rel < 0.0) return -1; /* :43-46 */
+  if (t_t < 0.0) return -1;                                                            /* :101 */
+  if (*has_prev) {
+    if (t_t <= *t_prev - tau_rel * *t_prev)
+      *n = *n + alpha;
+    else {
+      const int32_t m = (int32_t)floor(beta * *n);
+      *n = m > 1 ? m : 1;
+    }
+  }
+  *has_prev = 1;
+  *t_prev = t_t;
+  return 0;
+}
+
+/* ---------------------------------------------------------------- plan oracle */
+enum { BM = 128, BK = 64, BN_BASE = 256, BN_LOW = 128, GRAD_TARGET = 2 * 148, MIN_SPLIT = 512 };
+
+static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+typedef struct {
+  int32_t* out;
+  int64_t cap, n;
+} TileSink;
+
+static void emit(TileSink* s, int32_t m0, int32_t n0, int32_t kb0, int32_t ke0, int32_t kb1,
+                 int32_t ke1, int32_t split) {
+  if (s->n < s->cap) {
+    int32_t* t = s->out + 8 * s->n;
+    t[0] = m0; t[1] = n0; t[2] = kb0; t[3] = ke0; t[4] = kb1; t[5] = ke1; t[6] = split; t[7] = 0;
+  }
+  s->n++;
+}
+
+int64_t orc_plan_tiles(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t* ranks,
+                       const int32_t* slot, int32_t which, int32_t* out, int64_t cap) {
+  if (T < 1 || S < 1 || which < 0 || which > 5 || check_slots(T, S, slot)) return -1;
+  int32_t* off = (int32_t*)malloc(sizeof(int32_t) * S);
+  int32_t R = 0;
+  for (int32_t s = 0; s < S; ++s) {
+    off[s] = R;
+    R += (ranks[s] + 7) / 8 * 8;
+  }
+  if (R < 8) R = 8;
+  TileSink sink = {out, cap, 0};
+  const int64_t n_mt = cdiv(T, BM);
+  if (which <= 3) {
+    for (int64_t m = 0; m < n_mt; ++m) {
+      /* brute force: smallest / largest packed column owned by any token of the tile */
+      int64_t lo = -1, hi = -1;
+      for (int64_t c = 0; c < R; ++c) {
+        int owned = 0;
+        for (int64_t t = m * BM; t < T && t < (m + 1) * BM && !owned; ++t)
+          owned = c >= off[slot[t]] && c < off[slot[t]] + ranks[slot[t]];
+        if (owned) {
+          if (lo < 0) lo = c;
+          hi = c + 1;
+        }
+      }
+      const int32_t c_lo = (int32_t)(lo / BK * BK), c_hi = (int32_t)(cdiv(hi, BK) * BK);
+      if (which == 0 || which == 2) {
+        for (int32_t n0 = c_lo; n0 < c_hi; n0 += BN_LOW)
+          emit(&sink, (int32_t)(m * BM), n0, 0, (int32_t)(which == 0 ? d : k), 0, 0, 0);
+      } else {
+        const int64_t N = which == 1 ? k : d, K = which == 1 ? d : k;
+        for (int64_t n = 0; n < cdiv(N, BN_BASE); ++n)
+          emit(&sink, (int32_t)(m * BM), (int32_t)(n * BN_BASE), 0, (int32_t)K, c_lo, c_hi, 0);
+      }
+    }
+  } else {
+    const int64_t N = which == 4 ? k : d;
+    const int64_t n_rt = cdiv(R, BM), n_nt = cdiv(N, BN_LOW);
+    int64_t target = cdiv(GRAD_TARGET, n_rt * n_nt);
+    if (target < 1) target = 1;
+    for (int64_t rt = 0; rt < n_rt; ++rt) {
+      int64_t tlo = -1, thi = -1;
+      for (int64_t t = 0; t < T; ++t) {
+        const int64_t c0 = off[slot[t]], c1 = c0 + ranks[slot[t]];
+        if (c1 <= rt * BM || c0 >= (rt + 1) * BM) continue;
+        if (tlo < 0) tlo = t;
+        thi = t + 1;
+      }
+      if (tlo < 0) {
+        for (int64_t nt = 0; nt < n_nt; ++nt)
+          emit(&sink, (int32_t)(rt * BM), (int32_t)(nt * BN_LOW), 0, 0, 0, 0, 0);
+        continue;
+      }
+      const int64_t len = thi - tlo;
+      int64_t nsplit = len / MIN_SPLIT < target ? len / MIN_SPLIT : target;
+      if (nsplit < 1) nsplit = 1;
+      const int64_t chunk = cdiv(cdiv(len, nsplit), BK) * BK;
+      for (int64_t s = 0; s < nsplit; ++s) {
+        const int64_t kb = tlo + s * chunk;
+        const int64_t ke = thi < kb + chunk ? thi : kb + chunk;
+        if (kb >= ke) break;
+        for (int64_t nt = 0; nt < n_nt; ++nt)
+          emit(&sink, (int32_t)(rt * BM), (int32_t)(nt * BN_LOW), (int32_t)kb, (int32_t)ke, 0, 0,
+               (int32_t)s);
+      }
+    }
+  }
+  free(off);
+  return sink.n;
+}

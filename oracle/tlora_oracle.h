@@ -1,0 +1,75 @@
+/*
+ * tlora_oracle.h — CPU oracle for the fused multi-LoRA layer. TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may load this.
+ * It is the checker, never the thing measured or shipped; the product path
+ * (paper_2602_07263_b200/libtlora.so) has no CPU fallback.
+ *
+ * Parity pinning: the forward restatement is checked against golden vectors produced by
+ * the UNMODIFIED reference (oracle/ref_harness.cpp -> tests/golden/), at the reference's
+ * own tolerance (1e-9 relative, acceptance.cpp:91-94). The backward has no reference
+ * (SPEC.md:146); it is pinned to the reference forward by bilinearity identities
+ * (tests/test_oracle.py).
+ *
+ * Conventions: row-major doubles; slots are in reference adapter order (std::map by
+ * job_id, fused_lora.hpp:48-53); A[s] is d x r_s, B[s] is r_s x k.
+ * round_bf16 != 0 emulates the device numerics: operands are taken as given (callers
+ * pass bf16-representable values) and the low-rank intermediates H = X_j·A_j and
+ * dH = dY_j·B_jᵀ are rounded to bf16 (round-to-nearest-even) before use, as the
+ * kernels stash them in bf16.
+ */
+#ifndef TLORA_ORACLE_H_
+#define TLORA_ORACLE_H_
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* fused_lora.hpp:84-119 — Y = X·W, then for each slot with >= 1 token (in slot order):
+ * gather rows, mid = X_j·A_j, delta = mid·B_j, scatter-add. Returns 0, or -1 when a
+ * token names a slot outside [0, S) ("has no adapter", :72-73). */
+int orc_fused_forward(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t* ranks,
+                      const double* const* A, const double* const* B, const double* X,
+                      const double* W, const int32_t* token_slot, int32_t round_bf16,
+                      double* Y, double* H /* optional T x sum(r) packed, may be NULL */);
+
+/* fused_lora.hpp:124-135 — Y[t] = X[t]·(W + A_j·B_j), materialising W_j. */
+int orc_materialized(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t* ranks,
+                     const double* const* A, const double* const* B, const double* X,
+                     const double* W, const int32_t* token_slot, double* Y);
+
+/* Backward of the forward above for L = <dY, Y> (new; the reference has none):
+ *   dH_j = dY_j·B_jᵀ,  dX = dY·Wᵀ + scatter_j(dH_j·A_jᵀ),
+ *   dB_j = H_jᵀ·dY_j,  dA_j = X_jᵀ·dH_j   (H_j = X_j·A_j).
+ * dX may be NULL; dA[s] (d x r_s) and dB[s] (r_s x k) are overwritten. */
+int orc_fused_backward(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t* ranks,
+                       const double* const* A, const double* const* B, const double* X,
+                       const double* W, const int32_t* token_slot, const double* dY,
+                       int32_t round_bf16, double* dX, double* const* dA, double* const* dB);
+
+/* fused_lora.hpp:95-116 (fused != 0) and :139-163 (unfused): OpCost, bit-identical. */
+void orc_op_cost(int64_t T, int64_t d, int64_t k, int32_t S, const int64_t* tokens_per_slot,
+                 const int32_t* ranks, int32_t fused, double* flops, double* bytes,
+                 long long* launches);
+
+/* nano_pipeline.hpp:51-60. Returns 0, or -1 for group_batch < 1 / n < 1. */
+int orc_partition(int32_t group_batch, int32_t n, int32_t* n_out, int32_t* per_nano);
+
+/* nano_pipeline.hpp:99-112 (+ validate :43-46). Returns 0 or -1 (invalid_argument). */
+int orc_aimd_step(int32_t* n, int32_t* has_prev, double* t_prev, int32_t alpha, double beta,
+                  double tau_rel, double t_t);
+
+/* Plan oracle: brute-force restatement of the rank-aware tile tables of one plan, in the
+ * documented enumeration order. `which` is a tlora_launch id. Writes up
+ * to cap tiles of 8 int32 each into out; returns the table length (or -1 on bad input). */
+int64_t orc_plan_tiles(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t* ranks,
+                       const int32_t* token_slot, int32_t which, int32_t* out, int64_t cap);
+
+/* bf16 round-to-nearest-even of a double (via fp32), returned as a double. */
+double orc_round_bf16(double x);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

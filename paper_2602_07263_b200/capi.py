@@ -62,10 +62,17 @@ SIGNATURES = {
     "tlora_plan_get_info": (C.c_int, [C.c_void_p, C.POINTER(PlanInfoC)]),
     "tlora_plan_get_tiles": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(TileC), C.c_int32,
                                        C.POINTER(C.c_int32)]),
+    "tlora_plan_tiles_host": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_int32),
+                                        C.c_int64, C.POINTER(C.c_int32), C.c_int,
+                                        C.POINTER(TileC), C.c_int32, C.POINTER(C.c_int32)]),
     "tlora_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                 C.c_void_p, C.c_void_p]),
     "tlora_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_float, C.c_void_p]),
+    "tlora_profile_begin": (C.c_int, []),
+    "tlora_launch_count": (C.c_longlong, []),
+    "tlora_profile_end": (C.c_int, [C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double)]),
     "tlora_op_cost": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int32,
                                 C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.c_int,
                                 C.POINTER(C.c_double), C.POINTER(C.c_double),

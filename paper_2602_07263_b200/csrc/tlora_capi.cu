@@ -13,6 +13,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <atomic>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -44,6 +45,7 @@ struct Status : std::runtime_error {
 template <class F>
 int guarded(F&& f) {
   try {
+    (void)cudaGetLastError();  // drop stale non-sticky errors of unrelated earlier calls
     f();
     return TLORA_OK;
   } catch (const Status& s) {
@@ -111,16 +113,54 @@ CUtensorMap tmap_mn(const void* p, int64_t MN, int64_t K) {
   return make_tmap(p, MN, K, MN, 64, tlora::kBK);
 }
 
+// ------------------------------------------------------------------ launch profiling
+// Optional CUDA-event brackets around every GEMM launch, recorded on the launch stream
+// (tlora_profile_begin/_end). Used by bench.py for the live roofline of each launch kind.
+struct ProfRec {
+  int launch;
+  double flops;
+  cudaEvent_t e0, e1;
+};
+std::mutex g_prof_mu;
+std::atomic<long long> g_launches{0};  // every kernel this library enqueues
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+
+struct ProfScope {
+  ProfRec rec{};
+  cudaStream_t s;
+  bool on = false;
+  ProfScope(int launch, double flops, cudaStream_t st) : s(st) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof_on) return;
+    on = true;
+    rec.launch = launch;
+    rec.flops = flops;
+    TL_CUDA(cudaEventCreate(&rec.e0));
+    TL_CUDA(cudaEventCreate(&rec.e1));
+    TL_CUDA(cudaEventRecord(rec.e0, s));
+  }
+  ~ProfScope() {
+    if (!on) return;
+    cudaEventRecord(rec.e1, s);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.push_back(rec);
+  }
+};
+
 // ------------------------------------------------------------------ launch helpers
 template <int BN, bool AMN, bool BMN, int EPI, int ST>
 void launch_gemm(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1,
-                 const CUtensorMap& b1, const GemmArgs& args, int sm_count, cudaStream_t s) {
+                 const CUtensorMap& b1, const GemmArgs& args, int sm_count, cudaStream_t s,
+                 int launch_kind = -1, double flops = 0.0) {
   if (args.num_tiles == 0) return;
   auto kern = tlora::lora_gemm_kernel<BN, AMN, BMN, EPI, ST>;
   constexpr int smem = tlora::GemmSmem<BN, ST>::kDynamic;
   TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = std::min(args.num_tiles, sm_count);
+  ProfScope ps(launch_kind, flops, s);
   kern<<<grid, tlora::kGemmThreads, smem, s>>>(a0, b0, a1, b1, args);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   TL_CUDA(cudaGetLastError());
 }
 
@@ -263,7 +303,10 @@ void check_align(const void* p, const char* what) {
 }  // namespace
 
 // ==================================================================== objects
+std::atomic<uint64_t> g_next_layer_id{1};
+
 struct tlora_layer {
+  uint64_t id = g_next_layer_id.fetch_add(1);
   int device = 0;
   int sm_count = 148;
   tlora::RegistryLayout L;
@@ -275,7 +318,9 @@ struct tlora_layer {
 };
 
 struct tlora_plan {
-  tlora_layer* layer = nullptr;
+  tlora_layer* layer = nullptr;  // only dereferenced after checking layer_id (see bound())
+  uint64_t layer_id = 0;
+  int device = 0;
   tlora::PlanTables P;
   DevBuf<TileDesc> tiles[TLORA_L_COUNT];
   DevBuf<int32_t> token_slot, cnt_db, cnt_da;
@@ -333,8 +378,10 @@ int tlora_layer_create(int device, int64_t d, int64_t k, int32_t num_slots, cons
     require(num_slots >= 1 && ranks != nullptr, TLORA_ERR_ARG, "need at least one adapter slot");
     std::vector<int32_t> rv(ranks, ranks + num_slots);
     for (int s = 0; s < num_slots; ++s)
-      require(rv[s] >= 1 && rv[s] <= std::min<int64_t>(d, k), TLORA_ERR_SHAPE,
-              "slot " + std::to_string(s) + ": rank must be in [1, min(d, k)]");
+      // fused_forward accepts any r >= 1 (fused_lora.hpp:75 checks only consistency);
+      // r <= min(d, k) is a JobSpec invariant (workload.hpp:54-56), not a layer one.
+      require(rv[s] >= 1 && rv[s] <= 65536, TLORA_ERR_SHAPE,
+              "slot " + std::to_string(s) + ": rank must be in [1, 65536]");
     int n = 0;
     TL_CUDA(cudaGetDeviceCount(&n));
     require(device >= 0 && device < n, TLORA_ERR_NO_DEVICE,
@@ -487,6 +534,8 @@ int tlora_plan_create(tlora_layer* layer, int64_t tokens, const int32_t* token_s
     DeviceGuard g(layer->device);
     auto plan = std::make_unique<tlora_plan>();
     plan->layer = layer;
+    plan->layer_id = layer->id;
+    plan->device = layer->device;
     plan->P = tlora::build_plan(layer->L, tokens, token_slot);
     for (int64_t t = 0; t < tokens; ++t)
       require(layer->loaded[token_slot[t]], TLORA_ERR_REGISTRY,
@@ -518,7 +567,7 @@ int tlora_plan_create(tlora_layer* layer, int64_t tokens, const int32_t* token_s
 int tlora_plan_destroy(tlora_plan* plan) {
   return guarded([&] {
     if (!plan) return;
-    DeviceGuard g(plan->layer->device);
+    DeviceGuard g(plan->device);
     delete plan;
   });
 }
@@ -526,7 +575,7 @@ int tlora_plan_destroy(tlora_plan* plan) {
 int tlora_plan_get_info(const tlora_plan* plan, tlora_plan_info* info) {
   return guarded([&] {
     require(plan != nullptr && info != nullptr, TLORA_ERR_ARG, "null argument");
-    const auto& L = plan->layer->L;
+    const auto& L = plan->P.layout;
     info->tokens = plan->P.T;
     info->d = L.d;
     info->k = L.k;
@@ -551,11 +600,27 @@ int tlora_plan_get_tiles(const tlora_plan* plan, int launch, tlora_tile* out, in
   });
 }
 
+int tlora_plan_tiles_host(int64_t d, int64_t k, int32_t num_slots, const int32_t* ranks,
+                          int64_t tokens, const int32_t* token_slot, int launch, tlora_tile* out,
+                          int32_t cap, int32_t* count) {
+  return guarded([&] {
+    require(num_slots >= 1 && ranks != nullptr && token_slot != nullptr, TLORA_ERR_ARG,
+            "null argument");
+    require(tokens >= 1, TLORA_ERR_SHAPE, "plan needs at least one token");
+    require(launch >= 0 && launch < TLORA_L_COUNT, TLORA_ERR_ARG, "unknown launch id");
+    const auto L = tlora::RegistryLayout::make(d, k, std::vector<int32_t>(ranks, ranks + num_slots));
+    const auto P = tlora::build_plan(L, tokens, token_slot);
+    const auto& v = P.tiles[launch];
+    if (count) *count = (int32_t)v.size();
+    if (out) std::memcpy(out, v.data(), std::min<size_t>(cap, v.size()) * sizeof(tlora_tile));
+  });
+}
+
 int tlora_forward(tlora_layer* layer, const tlora_plan* plan, const void* X, void* Y, int y_dtype,
                   void* H_stash, void* stream) {
   return guarded([&] {
     require(layer != nullptr && plan != nullptr, TLORA_ERR_ARG, "null layer/plan");
-    require(plan->layer == layer, TLORA_ERR_PLAN, "plan was built for another layer");
+    require(plan->layer_id == layer->id, TLORA_ERR_PLAN, "plan was built for another layer");
     require(layer->base_set, TLORA_ERR_ARG, "base weight not set");
     check_align(X, "X");
     check_align(Y, "Y");
@@ -566,8 +631,13 @@ int tlora_forward(tlora_layer* layer, const tlora_plan* plan, const void* X, voi
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const auto& L = layer->L;
     const int64_t T = plan->P.T, d = L.d, k = L.k, R = L.R;
+    const double rt = (double)plan->P.tok_rank;
+    const double fwd_flops = 2.0 * T * d * k + 2.0 * rt * k;
 
-    // 1) shrink: H = X·Aᵀcatᵀ masked to each token's own packed columns
+    // 1) shrink: H = X·Aᵀcatᵀ masked to each token's own packed columns. Shrink tiles
+    //    write only their token tile's rank window; the gradient launches read H over
+    //    whole job token ranges, so every other column must be an exact zero.
+    TL_CUDA(cudaMemsetAsync(H_stash, 0, (size_t)T * R * 2, s));
     {
       GemmArgs a{};
       a.tiles = plan->tiles[TLORA_L_SHRINK].p;
@@ -581,7 +651,8 @@ int tlora_forward(tlora_layer* layer, const tlora_plan* plan, const void* X, voi
       a.slot_col_hi = layer->col_hi.p;
       const CUtensorMap ma = tmap_k(X, d, T, tlora::kBM);
       const CUtensorMap mb = tmap_k(layer->AT.p, d, R, tlora::kPlanBNLow);
-      launch_gemm<128, false, false, tlora::EPI_BF16_MASK, 6>(ma, mb, ma, mb, a, layer->sm_count, s);
+      launch_gemm<128, false, false, tlora::EPI_BF16_MASK, 6>(ma, mb, ma, mb, a, layer->sm_count, s,
+                                                              TLORA_L_SHRINK, 2.0 * rt * d);
     }
     // 2) fused base + expand: Y = X·W + H·Bᵀcatᵀ (K-extension over the tile's rank window)
     {
@@ -598,9 +669,11 @@ int tlora_forward(tlora_layer* layer, const tlora_plan* plan, const void* X, voi
       const CUtensorMap ma1 = tmap_k(H_stash, R, T, tlora::kBM);
       const CUtensorMap mb1 = tmap_k(layer->BcatT.p, R, k, 256);
       if (y_dtype == TLORA_BF16)
-        launch_gemm<256, false, false, tlora::EPI_BF16, 4>(ma0, mb0, ma1, mb1, a, layer->sm_count, s);
+        launch_gemm<256, false, false, tlora::EPI_BF16, 4>(ma0, mb0, ma1, mb1, a, layer->sm_count, s,
+                                                           TLORA_L_FWD, fwd_flops);
       else
-        launch_gemm<256, false, false, tlora::EPI_F32, 4>(ma0, mb0, ma1, mb1, a, layer->sm_count, s);
+        launch_gemm<256, false, false, tlora::EPI_F32, 4>(ma0, mb0, ma1, mb1, a, layer->sm_count, s,
+                                                          TLORA_L_FWD, fwd_flops);
     }
   });
 }
@@ -609,7 +682,7 @@ int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, c
                    const void* H_stash, void* dX, float beta, void* stream) {
   return guarded([&] {
     require(layer != nullptr && plan != nullptr, TLORA_ERR_ARG, "null layer/plan");
-    require(plan->layer == layer, TLORA_ERR_PLAN, "plan was built for another layer");
+    require(plan->layer_id == layer->id, TLORA_ERR_PLAN, "plan was built for another layer");
     require(layer->base_set, TLORA_ERR_ARG, "base weight not set");
     check_align(dY, "dY");
     check_align(X, "X");
@@ -619,9 +692,11 @@ int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, c
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const auto& L = layer->L;
     const int64_t T = plan->P.T, d = L.d, k = L.k, R = L.R;
+    const double rt = (double)plan->P.tok_rank;
     __nv_bfloat16* dH = plan->dH.p;
 
-    // 1) dH = dY·Bᵀ (masked)
+    // 1) dH = dY·Bᵀ (masked; zero outside the windows, as H above)
+    TL_CUDA(cudaMemsetAsync(dH, 0, (size_t)T * R * 2, s));
     {
       GemmArgs a{};
       a.tiles = plan->tiles[TLORA_L_DH].p;
@@ -635,7 +710,8 @@ int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, c
       a.slot_col_hi = layer->col_hi.p;
       const CUtensorMap ma = tmap_k(dY, k, T, tlora::kBM);
       const CUtensorMap mb = tmap_k(layer->Bcat.p, k, R, tlora::kPlanBNLow);
-      launch_gemm<128, false, false, tlora::EPI_BF16_MASK, 6>(ma, mb, ma, mb, a, layer->sm_count, s);
+      launch_gemm<128, false, false, tlora::EPI_BF16_MASK, 6>(ma, mb, ma, mb, a, layer->sm_count, s,
+                                                              TLORA_L_DH, 2.0 * rt * k);
     }
     // 2) dX = dY·Wᵀ + dH·Aᵀ
     if (dX) {
@@ -650,7 +726,8 @@ int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, c
       const CUtensorMap mb0 = tmap_k(layer->W16.p, k, d, 256);
       const CUtensorMap ma1 = tmap_k(dH, R, T, tlora::kBM);
       const CUtensorMap mb1 = tmap_k(layer->Acat.p, R, d, 256);
-      launch_gemm<256, false, false, tlora::EPI_BF16, 4>(ma0, mb0, ma1, mb1, a, layer->sm_count, s);
+      launch_gemm<256, false, false, tlora::EPI_BF16, 4>(ma0, mb0, ma1, mb1, a, layer->sm_count, s,
+                                                         TLORA_L_DX, 2.0 * T * d * k + 2.0 * rt * d);
     }
     // 3) dBcat = Hᵀ·dY and 4) dAᵀcat = dHᵀ·X over each rank tile's token range
     for (int which = 0; which < 2; ++which) {
@@ -674,15 +751,56 @@ int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, c
       }
       const CUtensorMap ma = tmap_mn(which == 0 ? H_stash : (const void*)dH, R, T);
       const CUtensorMap mb = tmap_mn(which == 0 ? dY : X, N, T);
-      launch_gemm<128, true, true, tlora::EPI_F32, 6>(ma, mb, ma, mb, a, layer->sm_count, s);
+      launch_gemm<128, true, true, tlora::EPI_F32, 6>(ma, mb, ma, mb, a, layer->sm_count, s, launch,
+                                                      2.0 * rt * N);
       if (nsplit > 1) {
         const int32_t* cnt = which == 0 ? plan->cnt_db.p : plan->cnt_da.p;
         const int64_t work = R * N / 4;
         const int blocks = (int)std::min<int64_t>(tlora::ceil_div(work, 256), 4 * layer->sm_count);
         reduce_splits_kernel<<<blocks, 256, 0, s>>>(plan->partial.p, R * N, cnt, R, N, beta, grads);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
         TL_CUDA(cudaGetLastError());
       }
     }
+  });
+}
+
+long long tlora_launch_count(void) { return g_launches.load(); }
+
+int tlora_profile_begin(void) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto& r : g_prof) {
+      cudaEventDestroy(r.e0);
+      cudaEventDestroy(r.e1);
+    }
+    g_prof.clear();
+    g_prof_on = true;
+  });
+}
+
+int tlora_profile_end(int32_t* counts, double* total_ms, double* total_flops) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = false;
+    for (int l = 0; l < TLORA_L_COUNT; ++l) {
+      if (counts) counts[l] = 0;
+      if (total_ms) total_ms[l] = 0.0;
+      if (total_flops) total_flops[l] = 0.0;
+    }
+    for (auto& r : g_prof) {
+      TL_CUDA(cudaEventSynchronize(r.e1));
+      float ms = 0.f;
+      TL_CUDA(cudaEventElapsedTime(&ms, r.e0, r.e1));
+      if (r.launch >= 0 && r.launch < TLORA_L_COUNT) {
+        if (counts) counts[r.launch] += 1;
+        if (total_ms) total_ms[r.launch] += ms;
+        if (total_flops) total_flops[r.launch] += r.flops;
+      }
+      cudaEventDestroy(r.e0);
+      cudaEventDestroy(r.e1);
+    }
+    g_prof.clear();
   });
 }
 

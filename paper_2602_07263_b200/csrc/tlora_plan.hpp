@@ -57,11 +57,13 @@ constexpr int kPlanGradTargetTiles = 2 * 148;  // split-K target for the gradien
 constexpr int kPlanMinSplitTokens = 512;
 
 struct PlanTables {
+  RegistryLayout layout;
   int64_t T = 0;
   std::vector<PlanTile> tiles[6];  // indexed by tlora_launch
   std::vector<int32_t> split_count_db, split_count_da;  // per 128-row packed-rank tile
   int32_t splits_db = 1, splits_da = 1;
   int64_t useful_ext_cols = 0, packed_ext_cols = 0;
+  int64_t tok_rank = 0;  // sum over tokens of the owning slot's rank (algorithmic work)
   std::vector<int32_t> slot_col_lo, slot_col_hi;  // per slot: [off, off + r)
   std::vector<int64_t> slot_first, slot_last;     // per slot token range, -1 if absent
 };
@@ -111,6 +113,7 @@ inline void build_grad_tiles(const RegistryLayout& L, const PlanTables& P, int64
 
 inline PlanTables build_plan(const RegistryLayout& L, int64_t T, const int32_t* token_slot) {
   PlanTables P;
+  P.layout = L;
   P.T = T;
   const int S = (int)L.rank.size();
   for (int64_t t = 0; t < T; ++t)
@@ -127,6 +130,7 @@ inline PlanTables build_plan(const RegistryLayout& L, int64_t T, const int32_t* 
   P.slot_last.assign(S, -1);
   for (int64_t t = 0; t < T; ++t) {
     const int s = token_slot[t];
+    P.tok_rank += L.rank[s];
     if (P.slot_first[s] < 0) P.slot_first[s] = t;
     P.slot_last[s] = t;
   }

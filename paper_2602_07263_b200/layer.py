@@ -9,6 +9,7 @@ is new — the reference has none).
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -108,6 +109,7 @@ class FusedLoRALayer:
         h = C.c_void_p()
         call("tlora_layer_create", self.device, self.d, self.k, len(self.ranks), rk, C.byref(h))
         self._h = h
+        self._plans = weakref.WeakSet()
         offs = (C.c_int32 * len(self.ranks))()
         R = C.c_int32()
         call("tlora_layer_layout", self._h, offs, C.byref(R))
@@ -151,7 +153,9 @@ class FusedLoRALayer:
 
     # ---------------------------------------------------------------- compute
     def plan(self, token_slot: Sequence[int]) -> Plan:
-        return Plan(self, token_slot)
+        p = Plan(self, token_slot)
+        self._plans.add(p)
+        return p
 
     def forward(self, plan: Plan, X: torch.Tensor, Y: torch.Tensor | None = None,
                 H: torch.Tensor | None = None, y_dtype=torch.bfloat16, stream=None):
@@ -179,6 +183,8 @@ class FusedLoRALayer:
 
     def close(self):
         if getattr(self, "_h", None):
+            for p in list(getattr(self, "_plans", ())):
+                p.close()
             capi.lib().tlora_layer_destroy(self._h)
             self._h = None
 
@@ -187,6 +193,19 @@ class FusedLoRALayer:
             self.close()
         except Exception:
             pass
+
+
+def plan_tiles_host(d: int, k: int, ranks, token_slot, launch: int) -> np.ndarray:
+    """Host-only tile table (no device), identical to what Plan uploads."""
+    rk = (C.c_int32 * len(ranks))(*[int(r) for r in ranks])
+    ts = np.ascontiguousarray(np.asarray(token_slot, dtype=np.int32))
+    n = C.c_int32()
+    call("tlora_plan_tiles_host", int(d), int(k), len(ranks), rk, int(ts.shape[0]),
+         ts.ctypes.data_as(C.POINTER(C.c_int32)), int(launch), None, 0, C.byref(n))
+    buf = (capi.TileC * max(1, n.value))()
+    call("tlora_plan_tiles_host", int(d), int(k), len(ranks), rk, int(ts.shape[0]),
+         ts.ctypes.data_as(C.POINTER(C.c_int32)), int(launch), buf, n.value, C.byref(n))
+    return np.frombuffer(buf, dtype=np.int32).reshape(-1, 8)[: n.value].copy()
 
 
 def op_cost(tokens: int, d: int, k: int, tokens_per_slot, ranks, fused: bool = True):

@@ -1,0 +1,72 @@
+"""Step driver for the fused multi-LoRA layer set (the caller of the hot path).
+
+One SSM layer-set step = forward of every adapted projection, then backward of every
+projection in reverse order (synthetic upstream gradients dY), adapter gradients
+accumulated in the layers' fp32 buffers. This is the per-iteration body of the
+reference simulator's loop (proj/include/lora_fleet/sim_engine.hpp:306-315, paper
+Alg. 1 FusedKernelLaunch) executed for real.
+"""
+from __future__ import annotations
+
+import torch
+
+from .layer import FusedLoRALayer
+from .workload import INPUT_GROUP, Workload
+
+
+class LayerSetStep:
+    def __init__(self, wl: Workload, device: int = 0, seed: int | None = None,
+                 shuffle: bool = False, y_dtype=torch.bfloat16):
+        self.wl = wl
+        self.device = device
+        dev = torch.device("cuda", device)
+        self.dev = dev
+        g = torch.Generator(device=dev)
+        g.manual_seed(wl.seed if seed is None else seed)
+        T = wl.tokens
+        self.T = T
+        self.slots = wl.token_slots(shuffle=shuffle)
+        self.layers, self.plans = {}, {}
+        self.X, self.Y, self.H, self.dY, self.dX = {}, {}, {}, {}, {}
+        for name, d, k in wl.projections:
+            lay = FusedLoRALayer(d, k, wl.ranks, device=device)
+            W = torch.randn(d, k, generator=g, device=dev, dtype=torch.float32).mul_(d ** -0.5)
+            lay.set_base(W.bfloat16())
+            del W
+            for s, j in enumerate(wl.jobs):
+                A = torch.randn(d, j.rank, generator=g, device=dev).mul_(d ** -0.5).bfloat16()
+                B = torch.randn(j.rank, k, generator=g, device=dev).mul_(j.rank ** -0.5).bfloat16()
+                lay.set_adapter(s, A, B)
+            self.layers[name] = lay
+            self.plans[name] = lay.plan(self.slots)
+            grp = INPUT_GROUP.get(name, name)
+            if grp not in self.X:
+                self.X[grp] = torch.randn(T, d, generator=g, device=dev).bfloat16()
+            self.Y[name] = torch.empty(T, k, dtype=y_dtype, device=dev)
+            self.H[name] = torch.empty(T, lay.R, dtype=torch.bfloat16, device=dev)
+            self.dY[name] = torch.randn(T, k, generator=g, device=dev).bfloat16()
+            self.dX[name] = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+        torch.cuda.synchronize(dev)
+
+    def x_of(self, name):
+        return self.X[INPUT_GROUP.get(name, name)]
+
+    def forward(self, stream=None):
+        for name, _, _ in self.wl.projections:
+            self.layers[name].forward(self.plans[name], self.x_of(name), self.Y[name],
+                                      self.H[name], stream=stream)
+
+    def backward(self, stream=None, beta: float = 0.0, on_layer_done=None):
+        for name, _, _ in reversed(self.wl.projections):
+            self.layers[name].backward(self.plans[name], self.dY[name], self.x_of(name),
+                                       self.H[name], self.dX[name], beta=beta, stream=stream)
+            if on_layer_done is not None:
+                on_layer_done(name, self.layers[name])
+
+    def step(self, stream=None, on_layer_done=None):
+        self.forward(stream)
+        self.backward(stream, on_layer_done=on_layer_done)
+
+    def input_tensors(self):
+        """Every tensor a step reads from outside the layer (for the e2e host copies)."""
+        return list(self.X.values()) + list(self.dY.values())
