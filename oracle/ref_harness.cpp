@@ -314,8 +314,14 @@ int bench(int argc, char** argv) {
       projs.push_back({std::stoi(p.substr(0, c)), std::stoi(p.substr(c + 1))});
     }
   }
+  // Values do not affect the timing; a cheap counter-hash fill keeps setup of the
+  // multi-GB weight set to a few seconds (normal_distribution would dominate the run).
+  uint64_t state = 2602;
+  auto val = [&state](std::mt19937_64&) {
+    state = state * 6364136223846793005ULL + 1442695040888963407ULL;
+    return ((double)(state >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0;
+  };
   std::mt19937_64 rng(2602);
-  std::normal_distribution<double> val;
   struct Proj {
     Matrix W, Wt;
     std::vector<AdapterMatrices> ad, adT;

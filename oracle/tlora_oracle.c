@@ -234,6 +234,7 @@ int orc_aimd_step(int32_t* n, int32_t* has_prev, double* t_prev, int32_t alpha, 
 
 /* ---------------------------------------------------------------- plan oracle */
 enum { BM = 128, BK = 64, BN_BASE = 256, BN_LOW = 128, GRAD_TARGET = 2 * 148, MIN_SPLIT = 512 };
+#define L2_BUDGET (32ll << 20)
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -264,6 +265,8 @@ int64_t orc_plan_tiles(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t
   TileSink sink = {out, cap, 0};
   const int64_t n_mt = cdiv(T, BM);
   if (which <= 3) {
+    int32_t* win_lo = (int32_t*)malloc(sizeof(int32_t) * (size_t)n_mt);
+    int32_t* win_hi = (int32_t*)malloc(sizeof(int32_t) * (size_t)n_mt);
     for (int64_t m = 0; m < n_mt; ++m) {
       /* brute force: smallest / largest packed column owned by any token of the tile */
       int64_t lo = -1, hi = -1;
@@ -277,15 +280,36 @@ int64_t orc_plan_tiles(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t
         }
       }
       const int32_t c_lo = (int32_t)(lo / BK * BK), c_hi = (int32_t)(cdiv(hi, BK) * BK);
-      if (which == 0 || which == 2) {
+      win_lo[m] = c_lo;
+      win_hi[m] = c_hi;
+      if (which == 0 || which == 2)
         for (int32_t n0 = c_lo; n0 < c_hi; n0 += BN_LOW)
           emit(&sink, (int32_t)(m * BM), n0, 0, (int32_t)(which == 0 ? d : k), 0, 0, 0);
-      } else {
-        const int64_t N = which == 1 ? k : d, K = which == 1 ? d : k;
-        for (int64_t n = 0; n < cdiv(N, BN_BASE); ++n)
-          emit(&sink, (int32_t)(m * BM), (int32_t)(n * BN_BASE), 0, (int32_t)K, c_lo, c_hi, 0);
-      }
     }
+    if (which == 1 || which == 3) {
+      /* L2 panel raster: keep a <= L2_BUDGET operand panel hot, stream the other one;
+       * choose the orientation streaming fewer bytes (ties: M panels). */
+      const int64_t N = which == 1 ? k : d, K = which == 1 ? d : k;
+      const int64_t n_nt = cdiv(N, BN_BASE);
+      const int64_t a_panel = (int64_t)BM * K * 2, b_panel = (int64_t)BN_BASE * K * 2;
+      int64_t gm = L2_BUDGET / a_panel, gn = L2_BUDGET / b_panel;
+      gm = gm < 1 ? 1 : (gm > n_mt ? n_mt : gm);
+      gn = gn < 1 ? 1 : (gn > n_nt ? n_nt : gn);
+      const int64_t bytes_m = n_mt * a_panel + cdiv(n_mt, gm) * n_nt * b_panel;
+      const int64_t bytes_n = n_nt * b_panel + cdiv(n_nt, gn) * n_mt * a_panel;
+      for (int64_t g0 = 0; bytes_m <= bytes_n && g0 < n_mt; g0 += gm)
+        for (int64_t n = 0; n < n_nt; ++n)
+          for (int64_t m = g0; m < n_mt && m < g0 + gm; ++m)
+            emit(&sink, (int32_t)(m * BM), (int32_t)(n * BN_BASE), 0, (int32_t)K, win_lo[m],
+                 win_hi[m], 0);
+      for (int64_t g0 = 0; bytes_m > bytes_n && g0 < n_nt; g0 += gn)
+        for (int64_t m = 0; m < n_mt; ++m)
+          for (int64_t n = g0; n < n_nt && n < g0 + gn; ++n)
+            emit(&sink, (int32_t)(m * BM), (int32_t)(n * BN_BASE), 0, (int32_t)K, win_lo[m],
+                 win_hi[m], 0);
+    }
+    free(win_lo);
+    free(win_hi);
   } else {
     const int64_t N = which == 4 ? k : d;
     const int64_t n_rt = cdiv(R, BM), n_nt = cdiv(N, BN_LOW);

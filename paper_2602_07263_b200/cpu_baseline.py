@@ -1,5 +1,75 @@
-"""CPU baseline leg of bench.py (placeholder until oracle tools are built)."""
+"""CPU baseline leg of bench.py: the reference's CPU path timed on the host cores.
+
+kind "reference": oracle/_ref/ref_harness bench — the UNMODIFIED reference fused_forward
+(proj/include/lora_fleet/fused_lora.hpp:84-119, compiled against the Eigen-subset shim)
+for the forward and, on the transposed problem, for dX; dA/dB with the shim GEMM (the
+reference has no backward). Tokens are sharded over all host threads (the reference
+functions are pure and reentrant).
+kind "port": the C oracle (oracle/liboracle.so), when the reference harness is absent.
+Only this module (bench.py's cpu_baseline / reference arm) may execute oracle/.
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+REF = ROOT / "oracle" / "_ref" / "ref_bench"
 
 
-def measure(wl, tokens_per_job=4, seconds_budget=15.0, threads=1, repeats=1):
-    return None
+def _run_ref(wl, threads, tokens_per_job, repeats):
+    projs = ";".join(f"{d}:{k}" for _, d, k in wl.projections)
+    ranks = ",".join(str(r) for r in wl.ranks)
+    out = subprocess.run([str(REF), "bench", str(threads), str(tokens_per_job), str(repeats),
+                          ranks, projs], check=True, capture_output=True, text=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def _run_port(wl, threads, tokens_per_job, repeats):
+    import numpy as np
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    rs = np.random.RandomState(2602)
+    slots = np.repeat(np.arange(len(wl.jobs)), tokens_per_job).astype(np.int32)
+    T = len(slots)
+    P = []
+    for _, d, k in wl.projections:
+        P.append((rs.randn(d, k) / np.sqrt(d), [rs.randn(d, r) for r in wl.ranks],
+                  [rs.randn(r, k) for r in wl.ranks], rs.randn(T, d), rs.randn(T, k)))
+    t0 = time.perf_counter()
+    for _ in range(repeats):
+        for W, A, B, X, dY in P:
+            O.fused_forward(X, W, A, B, slots)
+            O.fused_backward(X, W, A, B, slots, dY)
+    return {"seconds": time.perf_counter() - t0, "tokens": T * repeats, "threads": threads}
+
+
+def measure(wl, tokens_per_job=4, seconds_budget=15.0, threads=None, repeats=1):
+    """tokens/s of fwd+bwd over every projection of `wl` on a bounded token sample.
+    With seconds_budget > 0, repeats are added until about that much CPU time is spent."""
+    threads = threads or os.cpu_count() or 1
+    kind = "reference" if REF.exists() else "port"
+    run = _run_ref if kind == "reference" else _run_port
+    try:
+        res = run(wl, threads, tokens_per_job, 1)
+        if seconds_budget > 0 and res["seconds"] < seconds_budget:
+            reps = max(1, int(seconds_budget / max(res["seconds"], 1e-3)))
+            res = run(wl, threads, tokens_per_job, reps)
+        elif repeats > 1:
+            res = run(wl, threads, tokens_per_job, repeats)
+    except Exception as e:  # pragma: no cover - reported, never silently replaced
+        return {"value": None, "unit": "tokens/s", "cores": threads, "kind": kind,
+                "sample": f"failed: {e}"}
+    value = res["tokens"] / res["seconds"]
+    sample = (f"{tokens_per_job} tokens/job x {len(wl.jobs)} jobs through all "
+              f"{len(wl.projections)} projections of {wl.name}, fwd+bwd, fp64, "
+              f"{res['tokens']} tokens in {res['seconds']:.2f} s on {threads} threads"
+              + (" (reference fused_forward for fwd and dX; shim GEMM for dA/dB)"
+                 if kind == "reference" else " (C oracle port)"))
+    return {"value": round(value, 3), "unit": "tokens/s", "cores": threads, "kind": kind,
+            "sample": sample, "tokens": res["tokens"], "dtype": "f64"}

@@ -70,6 +70,35 @@ struct PlanTables {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+constexpr int64_t kPlanL2Budget = 32ll << 20;  // bytes of operand panel kept hot in L2
+
+// L2-aware raster of an (n_mt x n_nt) output-tile grid for a GEMM with reduction depth K
+// (bf16 operands). A persistent grid runs ~148 consecutive tiles at once; ordering tiles
+// in panels (a group of M-tiles swept across all N-tiles, or a group of N-tiles swept
+// across all M-tiles) keeps one operand panel (<= kPlanL2Budget) resident in L2 while the
+// other streams. The orientation that streams fewer total bytes wins (ties: M panels).
+// Returns (m, n) tile coordinates in launch order.
+inline std::vector<std::pair<int32_t, int32_t>> raster_order(int64_t n_mt, int64_t n_nt,
+                                                             int64_t K, int64_t bm, int64_t bn) {
+  const int64_t a_panel = bm * K * 2, b_panel = bn * K * 2;  // bytes per M / N tile panel
+  const int64_t gm = std::max<int64_t>(1, std::min(n_mt, kPlanL2Budget / a_panel));
+  const int64_t gn = std::max<int64_t>(1, std::min(n_nt, kPlanL2Budget / b_panel));
+  const int64_t bytes_m = n_mt * a_panel + ceil_div(n_mt, gm) * n_nt * b_panel;
+  const int64_t bytes_n = n_nt * b_panel + ceil_div(n_nt, gn) * n_mt * a_panel;
+  std::vector<std::pair<int32_t, int32_t>> order;
+  order.reserve(n_mt * n_nt);
+  if (bytes_m <= bytes_n) {
+    for (int64_t g0 = 0; g0 < n_mt; g0 += gm)
+      for (int64_t n = 0; n < n_nt; ++n)
+        for (int64_t m = g0; m < std::min(n_mt, g0 + gm); ++m) order.push_back({(int32_t)m, (int32_t)n});
+  } else {
+    for (int64_t g0 = 0; g0 < n_nt; g0 += gn)
+      for (int64_t m = 0; m < n_mt; ++m)
+        for (int64_t n = g0; n < std::min(n_nt, g0 + gn); ++n) order.push_back({(int32_t)m, (int32_t)n});
+  }
+  return order;
+}
+
 // Gradient launches (dB: N = k, dA: N = d): rows = packed rank space, K = tokens.
 inline void build_grad_tiles(const RegistryLayout& L, const PlanTables& P, int64_t N,
                              std::vector<PlanTile>& out, std::vector<int32_t>& split_cnt,
@@ -167,10 +196,8 @@ inline PlanTables build_plan(const RegistryLayout& L, int64_t T, const int32_t* 
     const int64_t N = which == 0 ? L.k : L.d;
     const int64_t K = which == 0 ? L.d : L.k;
     auto& v = P.tiles[which == 0 ? 1 : 3];
-    for (int64_t m = 0; m < n_mt; ++m)
-      for (int64_t n = 0; n < ceil_div(N, kPlanBNBase); ++n)
-        v.push_back({(int32_t)(m * kPlanBM), (int32_t)(n * kPlanBNBase), 0, (int32_t)K, c_lo[m],
-                     c_hi[m], 0, 0});
+    for (auto [m, n] : raster_order(n_mt, ceil_div(N, kPlanBNBase), K, kPlanBM, kPlanBNBase))
+      v.push_back({m * kPlanBM, n * kPlanBNBase, 0, (int32_t)K, c_lo[m], c_hi[m], 0, 0});
   }
   build_grad_tiles(L, P, L.k, P.tiles[4], P.split_count_db, P.splits_db);
   build_grad_tiles(L, P, L.d, P.tiles[5], P.split_count_da, P.splits_da);
