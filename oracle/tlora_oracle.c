@@ -233,8 +233,8 @@ int orc_aimd_step(int32_t* n, int32_t* has_prev, double* t_prev, int32_t alpha, 
 }
 
 /* ---------------------------------------------------------------- plan oracle */
-enum { BM = 128, BK = 64, BN_BASE = 256, BN_LOW = 128, GRAD_TARGET = 2 * 148, MIN_SPLIT = 512 };
-#define L2_BUDGET (32ll << 20)
+enum { BM = 128, BM2 = 256, BK = 64, BN_BASE = 256, BN_LOW = 128, GRAD_TARGET = 2 * 148, MIN_SPLIT = 512 };
+#define L2_BUDGET (48ll << 20)
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -287,26 +287,29 @@ int64_t orc_plan_tiles(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t
           emit(&sink, (int32_t)(m * BM), n0, 0, (int32_t)(which == 0 ? d : k), 0, 0, 0);
     }
     if (which == 1 || which == 3) {
-      /* L2 panel raster: keep a <= L2_BUDGET operand panel hot, stream the other one;
+      /* fused base GEMMs: 256-token tiles (CTA pairs); window = union of the two halves.
+       * L2 panel raster: keep a <= L2_BUDGET operand panel hot, stream the other one;
        * choose the orientation streaming fewer bytes (ties: M panels). */
       const int64_t N = which == 1 ? k : d, K = which == 1 ? d : k;
-      const int64_t n_nt = cdiv(N, BN_BASE);
-      const int64_t a_panel = (int64_t)BM * K * 2, b_panel = (int64_t)BN_BASE * K * 2;
+      const int64_t n_m2 = cdiv(T, BM2), n_nt = cdiv(N, BN_BASE);
+      const int64_t a_panel = (int64_t)BM2 * K * 2, b_panel = (int64_t)BN_BASE * K * 2;
       int64_t gm = L2_BUDGET / a_panel, gn = L2_BUDGET / b_panel;
-      gm = gm < 1 ? 1 : (gm > n_mt ? n_mt : gm);
+      gm = gm < 1 ? 1 : (gm > n_m2 ? n_m2 : gm);
       gn = gn < 1 ? 1 : (gn > n_nt ? n_nt : gn);
-      const int64_t bytes_m = n_mt * a_panel + cdiv(n_mt, gm) * n_nt * b_panel;
-      const int64_t bytes_n = n_nt * b_panel + cdiv(n_nt, gn) * n_mt * a_panel;
-      for (int64_t g0 = 0; bytes_m <= bytes_n && g0 < n_mt; g0 += gm)
+      const int64_t bytes_m = n_m2 * a_panel + cdiv(n_m2, gm) * n_nt * b_panel;
+      const int64_t bytes_n = n_nt * b_panel + cdiv(n_nt, gn) * n_m2 * a_panel;
+#define WLO(m) (2 * (m) + 1 < n_mt && win_lo[2 * (m) + 1] < win_lo[2 * (m)] ? win_lo[2 * (m) + 1] : win_lo[2 * (m)])
+#define WHI(m) (2 * (m) + 1 < n_mt && win_hi[2 * (m) + 1] > win_hi[2 * (m)] ? win_hi[2 * (m) + 1] : win_hi[2 * (m)])
+      for (int64_t g0 = 0; bytes_m <= bytes_n && g0 < n_m2; g0 += gm)
         for (int64_t n = 0; n < n_nt; ++n)
-          for (int64_t m = g0; m < n_mt && m < g0 + gm; ++m)
-            emit(&sink, (int32_t)(m * BM), (int32_t)(n * BN_BASE), 0, (int32_t)K, win_lo[m],
-                 win_hi[m], 0);
+          for (int64_t m = g0; m < n_m2 && m < g0 + gm; ++m)
+            emit(&sink, (int32_t)(m * BM2), (int32_t)(n * BN_BASE), 0, (int32_t)K, WLO(m), WHI(m), 0);
       for (int64_t g0 = 0; bytes_m > bytes_n && g0 < n_nt; g0 += gn)
-        for (int64_t m = 0; m < n_mt; ++m)
+        for (int64_t m = 0; m < n_m2; ++m)
           for (int64_t n = g0; n < n_nt && n < g0 + gn; ++n)
-            emit(&sink, (int32_t)(m * BM), (int32_t)(n * BN_BASE), 0, (int32_t)K, win_lo[m],
-                 win_hi[m], 0);
+            emit(&sink, (int32_t)(m * BM2), (int32_t)(n * BN_BASE), 0, (int32_t)K, WLO(m), WHI(m), 0);
+#undef WLO
+#undef WHI
     }
     free(win_lo);
     free(win_hi);

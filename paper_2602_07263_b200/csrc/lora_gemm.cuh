@@ -66,6 +66,67 @@ struct GemmSmem {
   static constexpr int kDynamic = kTotal + 1024;  // slack for 1024-B alignment
 };
 
+// Store one 32-column chunk of an accumulator row (fp32 bits in v) per the epilogue mode.
+template <int EPI>
+__device__ __forceinline__ void epi_store32(const GemmArgs& args, int split, int row, int col0,
+                                            const uint32_t (&v)[32], int lo, int hi) {
+  using namespace ptx;
+  if (row >= args.M || col0 >= args.N) return;
+  if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_MASK) {
+    float f[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      f[i] = __uint_as_float(v[i]);
+      if constexpr (EPI == EPI_BF16_MASK) {
+        const int col = col0 + i;
+        if (col < lo || col >= hi) f[i] = 0.f;
+      }
+    }
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + (int64_t)row * args.ldo + col0;
+    if (col0 + 32 <= args.N) {
+      uint4* o4 = reinterpret_cast<uint4*>(o);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack_bf16x2(f[8 * q + 0], f[8 * q + 1]);
+        w.y = pack_bf16x2(f[8 * q + 2], f[8 * q + 3]);
+        w.z = pack_bf16x2(f[8 * q + 4], f[8 * q + 5]);
+        w.w = pack_bf16x2(f[8 * q + 6], f[8 * q + 7]);
+        o4[q] = w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < args.N) o[i] = __float2bfloat16_rn(f[i]);
+    }
+  } else {
+    float* o = reinterpret_cast<float*>(args.out) + (int64_t)split * args.split_stride +
+               (int64_t)row * args.ldo + col0;
+    if (col0 + 32 <= args.N) {
+      float4* o4 = reinterpret_cast<float4*>(o);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 w = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                               __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+        if (args.beta != 0.f) {
+          const float4 p = o4[q];
+          w.x += args.beta * p.x; w.y += args.beta * p.y;
+          w.z += args.beta * p.z; w.w += args.beta * p.w;
+        }
+        o4[q] = w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (col0 + i >= args.N) continue;
+        float w = __uint_as_float(v[i]);
+        if (args.beta != 0.f) w += args.beta * o[i];
+        o[i] = w;
+      }
+    }
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI, int STAGES>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     lora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0,
@@ -224,57 +285,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = 0u;
         }
-        const int col0 = td.n0 + c;
-        if (row >= args.M || col0 >= args.N) continue;
-        if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_MASK) {
-          float f[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            f[i] = __uint_as_float(v[i]);
-            if constexpr (EPI == EPI_BF16_MASK) {
-              const int col = col0 + i;
-              if (col < lo || col >= hi) f[i] = 0.f;
-            }
-          }
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + (int64_t)row * args.ldo + col0;
-          if (col0 + 32 <= args.N) {
-            uint4* o4 = reinterpret_cast<uint4*>(o);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 w;
-              w.x = pack_bf16x2(f[8 * q + 0], f[8 * q + 1]);
-              w.y = pack_bf16x2(f[8 * q + 2], f[8 * q + 3]);
-              w.z = pack_bf16x2(f[8 * q + 4], f[8 * q + 5]);
-              w.w = pack_bf16x2(f[8 * q + 6], f[8 * q + 7]);
-              o4[q] = w;
-            }
-          } else {
-            for (int i = 0; i < 32 && col0 + i < args.N; ++i) o[i] = __float2bfloat16_rn(f[i]);
-          }
-        } else {
-          float* o = reinterpret_cast<float*>(args.out) + (int64_t)td.split * args.split_stride +
-                     (int64_t)row * args.ldo + col0;
-          if (col0 + 32 <= args.N) {
-            float4* o4 = reinterpret_cast<float4*>(o);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              float4 w = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                     __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-              if (args.beta != 0.f) {
-                const float4 p = o4[q];
-                w.x += args.beta * p.x; w.y += args.beta * p.y;
-                w.z += args.beta * p.z; w.w += args.beta * p.w;
-              }
-              o4[q] = w;
-            }
-          } else {
-            for (int i = 0; i < 32 && col0 + i < args.N; ++i) {
-              float w = __uint_as_float(v[i]);
-              if (args.beta != 0.f) w += args.beta * o[i];
-              o[i] = w;
-            }
-          }
-        }
+        epi_store32<EPI>(args, td.split, row, td.n0 + c, v, lo, hi);
       }
       if (!empty_k) {
         tc_fence_before();

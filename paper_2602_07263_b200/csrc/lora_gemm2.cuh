@@ -1,0 +1,195 @@
+// lora_gemm2.cuh — 2-CTA (cta_group::2) variant of the fused base+LoRA GEMM.
+//
+// The fused forward  Y = X·W (+ H·Bᵀcat over the tile's packed rank window) and the fused
+// backward dX = dY·Wᵀ (+ dH·Aᵀcat) are >95% of the layer's FLOPs. They run here on CTA
+// pairs: a cluster of 2 CTAs (one TPC) owns a 256 x 256 output tile; each CTA stages half
+// of A (its 128 rows) and half of B (128 of the 256 N rows) per K block, and the leader
+// CTA issues tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 16) which reads both CTAs'
+// shared memory. Per SM this halves operand shared-memory traffic versus a 1-CTA 128x256
+// tile (64 B/clk of MMA reads + 64 B/clk of TMA writes), which is what lets the tensor
+// pipe run at rate. Each CTA's TMEM holds its 128 rows x 256 fp32 columns, double
+// buffered (512 columns), so the epilogue of tile i overlaps the MMAs of tile i+1.
+//
+// Synchronisation (barrier ownership):
+//   full[s]   leader only; expect_tx(2 x stage bytes) by the leader's producer, the TMA
+//             loads of BOTH CTAs complete on it (cp.async.bulk.tensor .cta_group::2).
+//   empty[s]  both CTAs; the leader's tcgen05.commit multicasts one arrive to each.
+//   tfull[a]  both CTAs; multicast commit after the last K block of a tile.
+//   tempty[a] leader only; 8 arrives = 4 epilogue warps x 2 CTAs (remote arrive).
+#pragma once
+#include "lora_gemm.cuh"
+
+namespace tlora {
+
+constexpr int kBM2 = 256;  // rows per CTA pair
+constexpr int kBN2 = 256;
+
+template <int STAGES>
+struct Gemm2Smem {
+  static constexpr int kABytes = 128 * kBK * 2;  // this CTA's half of A
+  static constexpr int kBBytes = 128 * kBK * 2;  // this CTA's half of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOffset = STAGES * kStageBytes;
+  static constexpr int kTotal = kBarOffset + (2 * STAGES + 4) * 8 + 16;
+  static constexpr int kDynamic = kTotal + 1024;
+};
+
+template <int EPI, int STAGES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    lora_gemm2_kernel(const __grid_constant__ CUtensorMap tmA0,
+                      const __grid_constant__ CUtensorMap tmB0,
+                      const __grid_constant__ CUtensorMap tmA1,
+                      const __grid_constant__ CUtensorMap tmB1, const GemmArgs args) {
+  using namespace ptx;
+  using L = Gemm2Smem<STAGES>;
+  constexpr uint32_t kTmemCols = 2 * kBN2;
+  constexpr uint32_t kIdesc = make_idesc_bf16(kBM2, kBN2, false, false);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const uint32_t lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x / 2;
+  const int num_clusters = gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA0);
+    tma_prefetch_desc(&tmB0);
+    tma_prefetch_desc(&tmA1);
+    tma_prefetch_desc(&tmB1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 8);
+    }
+    fence_mbar_init();
+    fence_proxy_async_smem();
+  }
+  if (warp == 2) tmem_alloc_cg2(tmem_base_slot, kTmemCols);
+  tc_fence_before();
+  cluster_sync();  // peer barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (lane == 0) {
+      const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster_id; t < args.num_tiles; t += num_clusters) {
+        const TileDesc td = args.tiles[t];
+        const int am = td.m0 + 128 * (int)rank;
+        const int bn = td.n0 + 128 * (int)rank;
+#pragma unroll 1
+        for (int seg = 0; seg < 2; ++seg) {
+          const int kb = seg == 0 ? td.kb0 : td.kb1;
+          const int ke = seg == 0 ? td.ke0 : td.ke1;
+          const CUtensorMap* ma = seg == 0 ? &tmA0 : &tmA1;
+          const CUtensorMap* mb = seg == 0 ? &tmB0 : &tmB1;
+#pragma unroll 1
+          for (int k = kb; k < ke; k += kBK) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * L::kStageBytes;
+            uint8_t* sb = sa + L::kABytes;
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * L::kStageBytes);
+            const uint32_t fb = full0 + stage * 8;
+            tma_load_2d_cg2(sa, ma, fb, k, am);
+            tma_load_2d_cg2(sb, mb, fb, k, bn);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA only) =====================
+    if (leader && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc_iter = 0;
+      for (int t = cluster_id; t < args.num_tiles; t += num_clusters) {
+        const TileDesc td = args.tiles[t];
+        const int nkb = (td.ke0 > td.kb0 ? (td.ke0 - td.kb0 + kBK - 1) / kBK : 0) +
+                        (td.ke1 > td.kb1 ? (td.ke1 - td.kb1 + kBK - 1) / kBK : 0);
+        if (nkb == 0) continue;
+        const int acc = acc_iter & 1;
+        const uint32_t acc_phase = (acc_iter >> 1) & 1;
+        ++acc_iter;
+        mbar_wait_cluster(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kBN2;
+#pragma unroll 1
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t sb = sa + L::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            mma_bf16_ss_cg2(d_tmem, make_smem_desc_kmajor(sa + kk * 32),
+                            make_smem_desc_kmajor(sb + kk * 32), kIdesc, (kb | kk) != 0 ? 1u : 0u);
+          mma_commit_cg2_mc(&empty_bar[stage], 0x3);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit_cg2_mc(&tfull_bar[acc], 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue (both CTAs: own 128 rows x 256 cols) =====================
+    const int ew = warp & 3;
+    const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
+    int acc_iter = 0;
+    for (int t = cluster_id; t < args.num_tiles; t += num_clusters) {
+      const TileDesc td = args.tiles[t];
+      const bool empty_k = !(td.ke0 > td.kb0) && !(td.ke1 > td.kb1);
+      const int row = td.m0 + 128 * (int)rank + ew * 32 + (int)lane;
+      int acc = 0;
+      if (!empty_k) {
+        acc = acc_iter & 1;
+        const uint32_t acc_phase = (acc_iter >> 1) & 1;
+        ++acc_iter;
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+      }
+      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * kBN2;
+#pragma unroll 1
+      for (int c = 0; c < kBN2; c += 32) {
+        uint32_t v[32];
+        if (!empty_k) {
+          tmem_ld_32x32b_x32(t_row + c, v);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0u;
+        }
+        epi_store32<EPI>(args, td.split, row, td.n0 + c, v, 0, 0x7fffffff);
+      }
+      if (!empty_k) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();  // no CTA frees TMEM / exits while its peer may still address it
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_cg2(tmem_base, kTmemCols);
+  }
+}
+
+}  // namespace tlora

@@ -21,6 +21,7 @@
 
 #include "../../include/tlora.h"
 #include "lora_gemm.cuh"
+#include "lora_gemm2.cuh"
 #include "tlora_plan.hpp"
 
 using tlora::GemmArgs;
@@ -158,6 +159,21 @@ void launch_gemm(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap
   constexpr int smem = tlora::GemmSmem<BN, ST>::kDynamic;
   TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = std::min(args.num_tiles, sm_count);
+  ProfScope ps(launch_kind, flops, s);
+  kern<<<grid, tlora::kGemmThreads, smem, s>>>(a0, b0, a1, b1, args);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  TL_CUDA(cudaGetLastError());
+}
+
+template <int EPI, int ST>
+void launch_gemm2(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1,
+                  const CUtensorMap& b1, const GemmArgs& args, int sm_count, cudaStream_t s,
+                  int launch_kind, double flops) {
+  if (args.num_tiles == 0) return;
+  auto kern = tlora::lora_gemm2_kernel<EPI, ST>;
+  constexpr int smem = tlora::Gemm2Smem<ST>::kDynamic;
+  TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int grid = std::min(2 * args.num_tiles, sm_count / 2 * 2);
   ProfScope ps(launch_kind, flops, s);
   kern<<<grid, tlora::kGemmThreads, smem, s>>>(a0, b0, a1, b1, args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -664,16 +680,16 @@ int tlora_forward(tlora_layer* layer, const tlora_plan* plan, const void* X, voi
       a.out = Y;
       a.ldo = k;
       a.beta = 0.f;
-      const CUtensorMap ma0 = tmap_k(X, d, T, tlora::kBM);
-      const CUtensorMap mb0 = tmap_k(layer->Wt16.p, d, k, 256);
-      const CUtensorMap ma1 = tmap_k(H_stash, R, T, tlora::kBM);
-      const CUtensorMap mb1 = tmap_k(layer->BcatT.p, R, k, 256);
+      const CUtensorMap ma0 = tmap_k(X, d, T, 128);
+      const CUtensorMap mb0 = tmap_k(layer->Wt16.p, d, k, 128);
+      const CUtensorMap ma1 = tmap_k(H_stash, R, T, 128);
+      const CUtensorMap mb1 = tmap_k(layer->BcatT.p, R, k, 128);
       if (y_dtype == TLORA_BF16)
-        launch_gemm<256, false, false, tlora::EPI_BF16, 4>(ma0, mb0, ma1, mb1, a, layer->sm_count, s,
-                                                           TLORA_L_FWD, fwd_flops);
+        launch_gemm2<tlora::EPI_BF16, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD,
+                                         fwd_flops);
       else
-        launch_gemm<256, false, false, tlora::EPI_F32, 4>(ma0, mb0, ma1, mb1, a, layer->sm_count, s,
-                                                          TLORA_L_FWD, fwd_flops);
+        launch_gemm2<tlora::EPI_F32, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD,
+                                        fwd_flops);
     }
   });
 }
@@ -722,12 +738,12 @@ int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, c
       a.N = (int)d;
       a.out = dX;
       a.ldo = d;
-      const CUtensorMap ma0 = tmap_k(dY, k, T, tlora::kBM);
-      const CUtensorMap mb0 = tmap_k(layer->W16.p, k, d, 256);
-      const CUtensorMap ma1 = tmap_k(dH, R, T, tlora::kBM);
-      const CUtensorMap mb1 = tmap_k(layer->Acat.p, R, d, 256);
-      launch_gemm<256, false, false, tlora::EPI_BF16, 4>(ma0, mb0, ma1, mb1, a, layer->sm_count, s,
-                                                         TLORA_L_DX, 2.0 * T * d * k + 2.0 * rt * d);
+      const CUtensorMap ma0 = tmap_k(dY, k, T, 128);
+      const CUtensorMap mb0 = tmap_k(layer->W16.p, k, d, 128);
+      const CUtensorMap ma1 = tmap_k(dH, R, T, 128);
+      const CUtensorMap mb1 = tmap_k(layer->Acat.p, R, d, 128);
+      launch_gemm2<tlora::EPI_BF16, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_DX,
+                                       2.0 * T * d * k + 2.0 * rt * d);
     }
     // 3) dBcat = Hᵀ·dY and 4) dAᵀcat = dHᵀ·X over each rank tile's token range
     for (int which = 0; which < 2; ++which) {

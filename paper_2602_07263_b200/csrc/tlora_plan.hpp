@@ -17,6 +17,7 @@
 // (tests/test_plan.py re-derives it from oracle/tlora_oracle.c).
 #pragma once
 #include <algorithm>
+#include <climits>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -49,7 +50,8 @@ struct RegistryLayout {
   }
 };
 
-constexpr int kPlanBM = 128;      // MMA M tile (tokens or packed-rank rows)
+constexpr int kPlanBM = 128;      // MMA M tile (tokens or packed-rank rows), 1-CTA launches
+constexpr int kPlanBMBase = 256;  // M tile of the fused base GEMMs (2-CTA pair)
 constexpr int kPlanBK = 64;       // K block
 constexpr int kPlanBNBase = 256;  // N tile of the fused base GEMMs (fwd, dX)
 constexpr int kPlanBNLow = 128;   // N tile of the low-rank launches (shrink, dH, dA, dB)
@@ -70,7 +72,7 @@ struct PlanTables {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-constexpr int64_t kPlanL2Budget = 32ll << 20;  // bytes of operand panel kept hot in L2
+constexpr int64_t kPlanL2Budget = 48ll << 20;  // bytes of operand panel kept hot in L2
 
 // L2-aware raster of an (n_mt x n_nt) output-tile grid for a GEMM with reduction depth K
 // (bf16 operands). A persistent grid runs ~148 consecutive tiles at once; ordering tiles
@@ -178,9 +180,20 @@ inline PlanTables build_plan(const RegistryLayout& L, int64_t T, const int32_t* 
     }
     c_lo[m] = L.offset[smin] / kPlanBK * kPlanBK;
     c_hi[m] = (int32_t)(ceil_div(L.offset[smax] + L.rank[smax], kPlanBK) * kPlanBK);
+  }
+  // packing efficiency of the fused GEMM's K-extension, per 256-token tile
+  for (int64_t m2 = 0; m2 < ceil_div(T, kPlanBMBase); ++m2) {
+    std::vector<char> present(S, 0);
+    int32_t lo = INT32_MAX, hi = 0;
+    for (int64_t t = m2 * kPlanBMBase; t < std::min(T, (m2 + 1) * kPlanBMBase); ++t) {
+      const int s = token_slot[t];
+      present[s] = 1;
+      lo = std::min(lo, L.offset[s] / kPlanBK * kPlanBK);
+      hi = std::max(hi, (int32_t)(ceil_div(L.offset[s] + L.rank[s], kPlanBK) * kPlanBK));
+    }
     for (int s = 0; s < S; ++s)
       if (present[s]) P.useful_ext_cols += L.rank[s];
-    P.packed_ext_cols += c_hi[m] - c_lo[m];
+    P.packed_ext_cols += hi - lo;
   }
 
   // shrink / dH: per M-tile, N-tiles over that tile's packed rank window
@@ -191,13 +204,24 @@ inline PlanTables build_plan(const RegistryLayout& L, int64_t T, const int32_t* 
       for (int32_t n0 = c_lo[m]; n0 < c_hi[m]; n0 += kPlanBNLow)
         v.push_back({(int32_t)(m * kPlanBM), n0, 0, (int32_t)K, 0, 0, 0, 0});
   }
-  // fused base GEMMs: fwd (N = k, K = d) and dX (N = d, K = k), K-extension = window
+  // fused base GEMMs on 256-token tiles (CTA pairs): fwd (N = k, K = d) and dX (N = d,
+  // K = k); the K-extension window of a 256-tile is the union of its two 128-halves'.
+  const int64_t n_mt2 = ceil_div(T, kPlanBMBase);
+  std::vector<int32_t> w_lo(n_mt2), w_hi(n_mt2);
+  for (int64_t m = 0; m < n_mt2; ++m) {
+    w_lo[m] = c_lo[2 * m];
+    w_hi[m] = c_hi[2 * m];
+    if (2 * m + 1 < n_mt) {
+      w_lo[m] = std::min(w_lo[m], c_lo[2 * m + 1]);
+      w_hi[m] = std::max(w_hi[m], c_hi[2 * m + 1]);
+    }
+  }
   for (int which = 0; which < 2; ++which) {
     const int64_t N = which == 0 ? L.k : L.d;
     const int64_t K = which == 0 ? L.d : L.k;
     auto& v = P.tiles[which == 0 ? 1 : 3];
-    for (auto [m, n] : raster_order(n_mt, ceil_div(N, kPlanBNBase), K, kPlanBM, kPlanBNBase))
-      v.push_back({m * kPlanBM, n * kPlanBNBase, 0, (int32_t)K, c_lo[m], c_hi[m], 0, 0});
+    for (auto [m, n] : raster_order(n_mt2, ceil_div(N, kPlanBNBase), K, kPlanBMBase, kPlanBNBase))
+      v.push_back({m * kPlanBMBase, n * kPlanBNBase, 0, (int32_t)K, w_lo[m], w_hi[m], 0, 0});
   }
   build_grad_tiles(L, P, L.k, P.tiles[4], P.split_count_db, P.splits_db);
   build_grad_tiles(L, P, L.d, P.tiles[5], P.split_count_da, P.splits_da);

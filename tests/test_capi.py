@@ -111,7 +111,7 @@ def test_plan_covers_every_owned_column():
         fwd = plan_tiles_host(d, k, ranks, slots, capi.L_FWD)
         win = {int(t[0]): (int(t[4]), int(t[5])) for t in fwd}
         for m0, (lo, hi) in win.items():
-            owned = slots[m0:m0 + 128]
+            owned = slots[m0:m0 + 256]  # fused GEMMs run on 256-token CTA-pair tiles
             need_lo = min(off[s] for s in owned)
             need_hi = max(off[s] + ranks[s] for s in owned)
             assert lo <= need_lo and hi >= need_hi
