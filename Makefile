@@ -11,7 +11,15 @@ CSRC     := $(PKG)/csrc
 LIB      := $(PKG)/libtlora.so
 ORACLE   := oracle/liboracle.so
 
-all: $(LIB) $(ORACLE)
+CPPTEST  := tests/cpp/_build/test_dropin
+
+all: $(LIB) $(ORACLE) $(CPPTEST)
+
+# reference tests restated against the C++ drop-in headers (links libtlora.so)
+$(CPPTEST): tests/cpp/test_dropin.cpp include/lora_fleet/*.hpp include/tlora.h $(LIB)
+	mkdir -p tests/cpp/_build
+	$(CXX) -std=c++20 -O2 -Iinclude -DLORA_FLEET_WITH_TEST_ORACLE -o $@ tests/cpp/test_dropin.cpp \
+	  -L$(PKG) -ltlora -Wl,-rpath,'$$ORIGIN/../../../$(PKG)'
 
 $(LIB): $(CSRC)/tlora_capi.cu $(CSRC)/lora_gemm.cuh $(CSRC)/sm100_ptx.cuh $(CSRC)/tlora_plan.hpp include/tlora.h
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/tlora_capi.cu 2> build_ptxas.log || (cat build_ptxas.log; false)
@@ -23,6 +31,6 @@ ref:
 	$(MAKE) -C oracle ref
 
 clean:
-	rm -f $(LIB) $(ORACLE) build_ptxas.log
+	rm -f $(LIB) $(ORACLE) $(CPPTEST) build_ptxas.log
 
 .PHONY: all clean ref

@@ -1,0 +1,323 @@
+// fused_lora.hpp — drop-in for the reference's fused multi-LoRA operator API.
+//
+// Same types, function names, argument meaning, ordering and error behaviour as
+// proj/include/lora_fleet/fused_lora.hpp (reference), but the arithmetic runs in the
+// sm_100a kernels of libtlora.so through the C-ABI in include/tlora.h:
+//   fused_forward            fused_lora.hpp:84-119  -> tlora_forward   (+ new fused_backward)
+//   unfused_cost             fused_lora.hpp:139-163 -> tlora_op_cost
+//   trainable_param_count    fused_lora.hpp:166-170
+//   adapter_flops_per_token  fused_lora.hpp:173-176
+//   materialized_oracle      fused_lora.hpp:124-135 — the reference's TEST oracle; only
+//                            compiled with -DLORA_FLEET_WITH_TEST_ORACLE (tests), never
+//                            on the product path.
+// Shape and registry errors are thrown as std::runtime_error with the reference's
+// messages (fused_lora.hpp:66-76) before anything touches the device. There is no CPU
+// fallback: without an sm_100 GPU the compute calls throw.
+//
+// Numerics: operands are rounded to bf16, accumulation is fp32, Y is returned from an
+// fp32 epilogue (see DESIGN.md §Numerics for the tolerances the tests state).
+#pragma once
+#include <cstdint>
+#include <cstdlib>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../tlora.h"
+#include "lora_fleet/matrix.hpp"
+#include "lora_fleet/workload.hpp"
+
+namespace lora_fleet {
+
+struct AdapterMatrices {
+  std::string job_id;
+  Matrix A;  // d x r, down-projection
+  Matrix B;  // r x k, up-projection
+};
+
+struct TokenBatch {
+  Matrix rows;                           // total_tokens x d
+  std::vector<std::string> segment_map;  // owning job_id per row, any interleaving
+};
+
+struct OpCost {
+  double flops = 0.0;
+  double bytes_moved = 0.0;
+  long long kernel_launches = 0;
+
+  OpCost& operator+=(const OpCost& o) {
+    flops += o.flops;
+    bytes_moved += o.bytes_moved;
+    kernel_launches += o.kernel_launches;
+    return *this;
+  }
+};
+
+// Gradients of L = <dY, Y> (new; the reference has no backward).
+struct FusedGradients {
+  Matrix dX;                            // total_tokens x d
+  std::map<std::string, Matrix> dA;     // job_id -> d x r
+  std::map<std::string, Matrix> dB;     // job_id -> r x k
+};
+
+namespace detail {
+
+// std::map by job_id; a duplicate id keeps the LAST entry (fused_lora.hpp:48-53).
+inline std::map<std::string, const AdapterMatrices*> index_adapters(
+    const std::vector<AdapterMatrices>& adapters) {
+  std::map<std::string, const AdapterMatrices*> by_id;
+  for (const auto& a : adapters) by_id[a.job_id] = &a;
+  return by_id;
+}
+
+// Ascending rows of `batch` owned by job_id (fused_lora.hpp:56-61).
+inline std::vector<Index> segment_rows(const TokenBatch& batch, const std::string& job_id) {
+  std::vector<Index> idx;
+  for (Index t = 0; t < batch.rows.rows(); ++t)
+    if (batch.segment_map[static_cast<size_t>(t)] == job_id) idx.push_back(t);
+  return idx;
+}
+
+// Validation with the reference's messages (fused_lora.hpp:63-78). Only adapters that
+// some token references are shape-checked, as in the reference.
+inline void check_shapes(const TokenBatch& batch, const Matrix& base_weight,
+                         const std::map<std::string, const AdapterMatrices*>& by_id) {
+  const auto d = batch.rows.cols();
+  if (base_weight.rows() != d)
+    throw std::runtime_error("fused_lora: base weight rows != token dim d");
+  if (static_cast<Index>(batch.segment_map.size()) != batch.rows.rows())
+    throw std::runtime_error("fused_lora: segment_map length != token count");
+  for (const auto& id : batch.segment_map) {
+    auto it = by_id.find(id);
+    if (it == by_id.end())
+      throw std::runtime_error("fused_lora: segment '" + id + "' has no adapter");
+    const auto& a = *it->second;
+    if (a.A.rows() != d || a.A.cols() != a.B.rows() || a.B.cols() != base_weight.cols())
+      throw std::runtime_error("fused_lora: shape mismatch in segment '" + id + "'");
+  }
+}
+
+inline void tl_check(int code) {
+  if (code != TLORA_OK) throw std::runtime_error(std::string("tlora: ") + tlora_last_error());
+}
+
+inline int device_index() {
+  const char* e = std::getenv("TLORA_DEVICE");
+  return e ? std::atoi(e) : 0;
+}
+
+inline Index round8(Index n) { return (n + 7) / 8 * 8; }
+
+// Row-major, zero-padded copy of an m x n Matrix into rows x cols (f64).
+inline std::vector<double> padded(const Matrix& m, Index rows, Index cols) {
+  std::vector<double> v(static_cast<size_t>(rows * cols), 0.0);
+  for (Index i = 0; i < m.rows(); ++i)
+    for (Index j = 0; j < m.cols(); ++j) v[static_cast<size_t>(i * cols + j)] = m(i, j);
+  return v;
+}
+
+// RAII device buffer through the C-ABI.
+struct DeviceBuffer {
+  int dev = 0;
+  void* p = nullptr;
+  DeviceBuffer(int d, size_t bytes) : dev(d) { tl_check(tlora_buffer_alloc(d, bytes, &p)); }
+  ~DeviceBuffer() { tlora_buffer_free(dev, p); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+};
+
+// One fused layer built from the reference-style inputs: registry (slots in std::map
+// order), padded bf16 device copies, and the plan of this batch.
+class DeviceLayer {
+ public:
+  DeviceLayer(const TokenBatch& batch, const Matrix& W,
+              const std::map<std::string, const AdapterMatrices*>& by_id)
+      : dev_(device_index()),
+        T_(batch.rows.rows()),
+        d_(batch.rows.cols()),
+        k_(W.cols()),
+        dp_(round8(d_)),
+        kp_(round8(k_)) {
+    std::vector<int32_t> ranks;
+    std::map<std::string, int32_t> slot_of;
+    for (const auto& [id, a] : by_id) {
+      slot_of[id] = static_cast<int32_t>(ranks.size());
+      ranks.push_back(static_cast<int32_t>(a->A.cols()));
+      ids_.push_back(id);
+    }
+    tl_check(tlora_layer_create(dev_, dp_, kp_, static_cast<int32_t>(ranks.size()), ranks.data(),
+                                &layer_));
+    const auto wp = padded(W, dp_, kp_);
+    tl_check(tlora_layer_set_base(layer_, wp.data(), TLORA_F64, TLORA_HOST, nullptr));
+    for (const auto& [id, a] : by_id) {
+      const auto ap = padded(a->A, dp_, a->A.cols());
+      const auto bp = padded(a->B, a->B.rows(), kp_);
+      tl_check(tlora_layer_set_adapter(layer_, slot_of[id], ap.data(), bp.data(), TLORA_F64,
+                                       TLORA_HOST, nullptr));
+    }
+    tl_check(tlora_layer_layout(layer_, nullptr, &R_));
+    std::vector<int32_t> slots(static_cast<size_t>(T_));
+    for (Index t = 0; t < T_; ++t) slots[static_cast<size_t>(t)] = slot_of[batch.segment_map[t]];
+    tl_check(tlora_plan_create(layer_, T_, slots.data(), &plan_));
+    X_ = std::make_unique<DeviceBuffer>(dev_, static_cast<size_t>(T_ * dp_ * 2));
+    H_ = std::make_unique<DeviceBuffer>(dev_, static_cast<size_t>(T_ * R_ * 2));
+    const auto xp = padded(batch.rows, T_, dp_);
+    tl_check(tlora_copy_to_device(X_->p, TLORA_BF16, xp.data(), TLORA_F64, T_ * dp_, nullptr));
+  }
+  ~DeviceLayer() {
+    tlora_plan_destroy(plan_);
+    tlora_layer_destroy(layer_);
+  }
+
+  Matrix forward() {
+    DeviceBuffer Y(dev_, static_cast<size_t>(T_ * kp_ * 4));
+    tl_check(tlora_forward(layer_, plan_, X_->p, Y.p, TLORA_F32, H_->p, nullptr));
+    std::vector<double> y(static_cast<size_t>(T_ * kp_));
+    tl_check(tlora_copy_to_host(y.data(), TLORA_F64, Y.p, TLORA_F32, T_ * kp_, nullptr));
+    Matrix out(T_, k_);
+    for (Index t = 0; t < T_; ++t)
+      for (Index j = 0; j < k_; ++j) out(t, j) = y[static_cast<size_t>(t * kp_ + j)];
+    return out;
+  }
+
+  FusedGradients backward(const Matrix& dY) {
+    DeviceBuffer g(dev_, static_cast<size_t>(T_ * kp_ * 2));
+    DeviceBuffer dX(dev_, static_cast<size_t>(T_ * dp_ * 2));
+    const auto gp = padded(dY, T_, kp_);
+    tl_check(tlora_copy_to_device(g.p, TLORA_BF16, gp.data(), TLORA_F64, T_ * kp_, nullptr));
+    tl_check(tlora_backward(layer_, plan_, g.p, X_->p, H_->p, dX.p, 0.0f, nullptr));
+    FusedGradients out;
+    std::vector<double> dx(static_cast<size_t>(T_ * dp_));
+    tl_check(tlora_copy_to_host(dx.data(), TLORA_F64, dX.p, TLORA_BF16, T_ * dp_, nullptr));
+    out.dX = Matrix(T_, d_);
+    for (Index t = 0; t < T_; ++t)
+      for (Index j = 0; j < d_; ++j) out.dX(t, j) = dx[static_cast<size_t>(t * dp_ + j)];
+    for (size_t s = 0; s < ids_.size(); ++s) {
+      const auto& id = ids_[s];
+      const Index r = rank_of(s);
+      std::vector<float> da(static_cast<size_t>(dp_ * r)), db(static_cast<size_t>(r * kp_));
+      tl_check(tlora_layer_read_grad(layer_, static_cast<int32_t>(s), da.data(), db.data(),
+                                     TLORA_HOST, nullptr));
+      Matrix A(d_, r), B(r, k_);
+      for (Index i = 0; i < d_; ++i)
+        for (Index j = 0; j < r; ++j) A(i, j) = da[static_cast<size_t>(i * r + j)];
+      for (Index i = 0; i < r; ++i)
+        for (Index j = 0; j < k_; ++j) B(i, j) = db[static_cast<size_t>(i * kp_ + j)];
+      out.dA[id] = std::move(A);
+      out.dB[id] = std::move(B);
+    }
+    return out;
+  }
+
+  void set_ranks(std::vector<Index> r) { ranks_ = std::move(r); }
+
+ private:
+  Index rank_of(size_t s) const { return ranks_.at(s); }
+
+  int dev_;
+  Index T_, d_, k_, dp_, kp_;
+  int32_t R_ = 0;
+  tlora_layer* layer_ = nullptr;
+  tlora_plan* plan_ = nullptr;
+  std::vector<std::string> ids_;
+  std::vector<Index> ranks_;
+  std::unique_ptr<DeviceBuffer> X_, H_;
+};
+
+inline std::unique_ptr<DeviceLayer> make_device_layer(
+    const TokenBatch& batch, const Matrix& W,
+    const std::map<std::string, const AdapterMatrices*>& by_id) {
+  auto L = std::make_unique<DeviceLayer>(batch, W, by_id);
+  std::vector<Index> ranks;
+  for (const auto& [id, a] : by_id) ranks.push_back(a->A.cols());
+  L->set_ranks(std::move(ranks));
+  return L;
+}
+
+}  // namespace detail
+
+// Y[t] = X[t]·W + X[t]·A_i·B_i for t's owning job i (fused_lora.hpp:82-119): one shared
+// base GEMM with the low-rank expand fused as a K-extension, on the GPU. The returned
+// OpCost is the reference's analytic model, bit-identical (tlora_op_cost).
+inline std::pair<Matrix, OpCost> fused_forward(const TokenBatch& batch, const Matrix& base_weight,
+                                               const std::vector<AdapterMatrices>& adapters) {
+  auto by_id = detail::index_adapters(adapters);
+  detail::check_shapes(batch, base_weight, by_id);
+  std::vector<int64_t> tokens;
+  std::vector<int32_t> ranks;
+  for (const auto& [id, a] : by_id) {
+    tokens.push_back(static_cast<int64_t>(detail::segment_rows(batch, id).size()));
+    ranks.push_back(static_cast<int32_t>(a->A.cols()));
+  }
+  OpCost cost;
+  detail::tl_check(tlora_op_cost(batch.rows.rows(), batch.rows.cols(), base_weight.cols(),
+                                 static_cast<int32_t>(ranks.size()), tokens.data(), ranks.data(),
+                                 1, &cost.flops, &cost.bytes_moved, &cost.kernel_launches));
+  if (batch.rows.rows() == 0) return {Matrix(0, base_weight.cols()), cost};
+  auto L = detail::make_device_layer(batch, base_weight, by_id);
+  return {L->forward(), cost};
+}
+
+// Backward of fused_forward for upstream gradient dY (new; SPEC.md:146 has none).
+inline FusedGradients fused_backward(const TokenBatch& batch, const Matrix& base_weight,
+                                     const std::vector<AdapterMatrices>& adapters,
+                                     const Matrix& dY) {
+  auto by_id = detail::index_adapters(adapters);
+  detail::check_shapes(batch, base_weight, by_id);
+  if (dY.rows() != batch.rows.rows() || dY.cols() != base_weight.cols())
+    throw std::runtime_error("fused_lora: upstream gradient shape != token count x k");
+  auto L = detail::make_device_layer(batch, base_weight, by_id);
+  L->forward();
+  return L->backward(dY);
+}
+
+// Unfused accounting (fused_lora.hpp:137-163), via the bit-identical C-ABI restatement.
+inline OpCost unfused_cost(const TokenBatch& batch, const Matrix& base_weight,
+                           const std::vector<AdapterMatrices>& adapters) {
+  auto by_id = detail::index_adapters(adapters);
+  detail::check_shapes(batch, base_weight, by_id);
+  std::vector<int64_t> tokens;
+  std::vector<int32_t> ranks;
+  for (const auto& [id, a] : by_id) {
+    tokens.push_back(static_cast<int64_t>(detail::segment_rows(batch, id).size()));
+    ranks.push_back(static_cast<int32_t>(a->A.cols()));
+  }
+  OpCost cost;
+  detail::tl_check(tlora_op_cost(batch.rows.rows(), batch.rows.cols(), base_weight.cols(),
+                                 static_cast<int32_t>(ranks.size()), tokens.data(), ranks.data(),
+                                 0, &cost.flops, &cost.bytes_moved, &cost.kernel_launches));
+  return cost;
+}
+
+// r·(d + k) trainable parameters per adapted layer (fused_lora.hpp:165-170).
+inline long long trainable_param_count(const JobSpec& job) {
+  job.validate();
+  return static_cast<long long>(job.rank) * (job.model.hidden_dim + job.model.proj_dim) *
+         job.model.num_layers;
+}
+
+// Forward adapter FLOPs per token per adapted layer (fused_lora.hpp:172-176).
+inline double adapter_flops_per_token(const JobSpec& job) {
+  return 2.0 * static_cast<double>(job.rank) *
+         static_cast<double>(job.model.hidden_dim + job.model.proj_dim);
+}
+
+#ifdef LORA_FLEET_WITH_TEST_ORACLE
+// TEST ORACLE ONLY (fused_lora.hpp:121-135): materialises W_i = W + A_i·B_i on the host.
+inline Matrix materialized_oracle(const TokenBatch& batch, const Matrix& base_weight,
+                                  const std::vector<AdapterMatrices>& adapters) {
+  auto by_id = detail::index_adapters(adapters);
+  detail::check_shapes(batch, base_weight, by_id);
+  Matrix out(batch.rows.rows(), base_weight.cols());
+  for (const auto& [id, adapter] : by_id) {
+    Matrix w_i = base_weight + adapter->A * adapter->B;
+    for (auto t : detail::segment_rows(batch, id)) out.row(t) = batch.rows.row(t) * w_i;
+  }
+  return out;
+}
+#endif
+
+}  // namespace lora_fleet

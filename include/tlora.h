@@ -83,6 +83,20 @@ int tlora_abi_version(void);
 /* Fails with TLORA_ERR_NO_DEVICE unless device `device` is an sm_100 GPU. */
 int tlora_device_check(int device, int* sm_count);
 
+/* ---- device buffers (so non-CUDA hosts — C++, cgo, JNI, ctypes — need no cudart) --- */
+int tlora_buffer_alloc(int device, size_t bytes, void** out);
+int tlora_buffer_free(int device, void* ptr);
+/* count elements host -> device, converting src_dtype -> dst_dtype (f64/f32/bf16 in,
+ * f32/bf16 out; bf16 rounding is round-to-nearest-even). Synchronous w.r.t. the host
+ * buffer: it may be reused when the call returns. */
+int tlora_copy_to_device(void* dst, int dst_dtype, const void* src_host, int src_dtype,
+                         int64_t count, void* stream);
+/* count elements device -> host with conversion (f32/bf16 in, f64/f32/bf16 out).
+ * Returns after the data has landed in dst_host. */
+int tlora_copy_to_host(void* dst_host, int dst_dtype, const void* src, int src_dtype,
+                       int64_t count, void* stream);
+int tlora_stream_sync(void* stream);
+
 /* ---- layer: one adapted projection (frozen base W + adapter registry) --------- */
 /* ranks[num_slots]: registry layout in reference adapter order (std::map by job_id,
  * fused_lora.hpp:48-53). Slot s owns packed rank columns [off_s, off_s + ranks[s]). */

@@ -45,6 +45,13 @@ SIGNATURES = {
     "tlora_last_error": (C.c_char_p, []),
     "tlora_abi_version": (C.c_int, []),
     "tlora_device_check": (C.c_int, [C.c_int, C.POINTER(C.c_int)]),
+    "tlora_buffer_alloc": (C.c_int, [C.c_int, C.c_size_t, C.POINTER(C.c_void_p)]),
+    "tlora_buffer_free": (C.c_int, [C.c_int, C.c_void_p]),
+    "tlora_copy_to_device": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int64,
+                                       C.c_void_p]),
+    "tlora_copy_to_host": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int64,
+                                     C.c_void_p]),
+    "tlora_stream_sync": (C.c_int, [C.c_void_p]),
     "tlora_layer_create": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int32,
                                      C.POINTER(C.c_int32), C.POINTER(C.c_void_p)]),
     "tlora_layer_destroy": (C.c_int, [C.c_void_p]),

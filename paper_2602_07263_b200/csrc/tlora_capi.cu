@@ -229,6 +229,20 @@ __global__ void pack_adapter_kernel(const void* A, const void* B, int dtype, int
   }
 }
 
+// Elementwise dtype conversion (device), used by the host-buffer copy entry points.
+__global__ void convert_kernel(const void* src, int sdt, void* dst, int ddt, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v;
+    if (sdt == TLORA_F64) v = reinterpret_cast<const double*>(src)[i];
+    else if (sdt == TLORA_F32) v = reinterpret_cast<const float*>(src)[i];
+    else v = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[i]);
+    if (ddt == TLORA_F64) reinterpret_cast<double*>(dst)[i] = v;
+    else if (ddt == TLORA_F32) reinterpret_cast<float*>(dst)[i] = (float)v;
+    else reinterpret_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn((float)v);
+  }
+}
+
 // dAT rows [off, off+r) (r x d) -> dA (d x r); dB rows -> dB (r x k).
 __global__ void read_grad_kernel(const float* dAT, const float* dBc, int64_t d, int64_t k, int r,
                                  int off, float* dA, float* dB) {
@@ -381,6 +395,80 @@ int tlora_device_check(int device, int* sm_count) {
     const int sms = device_sm_count(device);
     if (sm_count) *sm_count = sms;
   });
+}
+
+int tlora_buffer_alloc(int device, size_t bytes, void** out) {
+  return guarded([&] {
+    require(out != nullptr, TLORA_ERR_ARG, "out is null");
+    *out = nullptr;
+    int n = 0;
+    TL_CUDA(cudaGetDeviceCount(&n));
+    require(device >= 0 && device < n, TLORA_ERR_NO_DEVICE, "no CUDA device " + std::to_string(device));
+    DeviceGuard g(device);
+    if (bytes) TL_CUDA(cudaMalloc(out, bytes));
+  });
+}
+
+int tlora_buffer_free(int device, void* ptr) {
+  return guarded([&] {
+    if (!ptr) return;
+    DeviceGuard g(device);
+    TL_CUDA(cudaFree(ptr));
+  });
+}
+
+int tlora_copy_to_device(void* dst, int dst_dtype, const void* src_host, int src_dtype,
+                         int64_t count, void* stream) {
+  return guarded([&] {
+    require(count >= 0, TLORA_ERR_ARG, "negative count");
+    if (count == 0) return;
+    require(dst && src_host, TLORA_ERR_ARG, "null pointer");
+    require(dst_dtype == TLORA_F32 || dst_dtype == TLORA_BF16, TLORA_ERR_ARG,
+            "device dtype must be f32 or bf16");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t sb = dtype_size(src_dtype);
+    if (src_dtype == dst_dtype) {
+      TL_CUDA(cudaMemcpyAsync(dst, src_host, count * sb, cudaMemcpyHostToDevice, s));
+      TL_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    DevBuf<char> tmp;
+    tmp.alloc(count * sb);
+    TL_CUDA(cudaMemcpyAsync(tmp.p, src_host, count * sb, cudaMemcpyHostToDevice, s));
+    convert_kernel<<<(unsigned)std::min<int64_t>(tlora::ceil_div(count, 256), 4096), 256, 0, s>>>(
+        tmp.p, src_dtype, dst, dst_dtype, count);
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tlora_copy_to_host(void* dst_host, int dst_dtype, const void* src, int src_dtype,
+                       int64_t count, void* stream) {
+  return guarded([&] {
+    require(count >= 0, TLORA_ERR_ARG, "negative count");
+    if (count == 0) return;
+    require(dst_host && src, TLORA_ERR_ARG, "null pointer");
+    require(src_dtype == TLORA_F32 || src_dtype == TLORA_BF16, TLORA_ERR_ARG,
+            "device dtype must be f32 or bf16");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t db = dtype_size(dst_dtype);
+    if (src_dtype == dst_dtype) {
+      TL_CUDA(cudaMemcpyAsync(dst_host, src, count * db, cudaMemcpyDeviceToHost, s));
+      TL_CUDA(cudaStreamSynchronize(s));
+      return;
+    }
+    DevBuf<char> tmp;
+    tmp.alloc(count * db);
+    convert_kernel<<<(unsigned)std::min<int64_t>(tlora::ceil_div(count, 256), 4096), 256, 0, s>>>(
+        src, src_dtype, tmp.p, dst_dtype, count);
+    TL_CUDA(cudaGetLastError());
+    TL_CUDA(cudaMemcpyAsync(dst_host, tmp.p, count * db, cudaMemcpyDeviceToHost, s));
+    TL_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tlora_stream_sync(void* stream) {
+  return guarded([&] { TL_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream))); });
 }
 
 int tlora_layer_create(int device, int64_t d, int64_t k, int32_t num_slots, const int32_t* ranks,
