@@ -248,7 +248,7 @@ def run_ours(args, rank, world, local_rank):
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak else None,
                 "frac_of_burst": round(achieved / float(peaks["bf16_tflops"]), 4),
-                "traffic": traffic, "kernel": "lora_gemm_kernel<256,K,K> (fwd + dX)",
+                "traffic": traffic, "kernel": "lora_gemm2_kernel (2-CTA fused base+LoRA GEMM: fwd + dX)",
                 "peak_source": peaks["source"] + " sustained bf16", "per_launch": per_launch}
 
     cpu = None
@@ -286,6 +286,79 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk,
     }
     return out
+
+
+def run_tp(args, rank, world, local_rank):
+    """Tensor-parallel layer set: one layer of the configured model split over
+    the TP group, per-nano-batch all-gather / reduce-scatter on a comm stream overlapped
+    with the GEMMs; N chosen online by AIMD during warm-up, then frozen for timing.
+    Strong scaling: the global token batch is fixed, value = global tokens / step time."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_07263_b200 import capi
+    from paper_2602_07263_b200.tp import TPLayerSetStep
+    from paper_2602_07263_b200.workload import config
+
+    torch.cuda.set_device(local_rank)
+    wl = config(args.config)
+    st = TPLayerSetStep(wl, rank, world, local_rank, nano=args.nano)
+    stream = torch.cuda.current_stream()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    trajectory = []
+
+    def timed_step(n):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st.step(n)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    for _ in range(args.warmup):
+        timed_step(st.n)
+    if args.aimd_steps > 0:
+        best = (float("inf"), st.n)
+        for _ in range(args.aimd_steps):
+            n = st.n
+            ms = timed_step(n)
+            trajectory.append([n, round(ms, 3)])
+            best = min(best, (ms, n))
+            st.adapt(ms / 1e3)  # identical on all ranks (times are max-reduced)
+        st.n = best[1]
+    dist.barrier()
+    torch.cuda.synchronize()
+    lib = capi.lib()
+    n0 = lib.tlora_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        st.step(st.n)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = t.item() / args.steps
+    flops = wl.flops_fwd_bwd() / wl.layers
+    value = wl.tokens / (ms_per_step / 1e3)
+    return {
+        "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded normal activations/grads, random-init W and adapters)",
+        "config": {"workload": f"{wl.name}: {wl.notes} (one layer of the stack per step)",
+                   "tokens_global": wl.tokens, "parallelism": f"tp{world}",
+                   "nano_batches": st.n, "aimd_trajectory_n_ms": trajectory,
+                   "algorithmic_tflop_per_step": round(flops / 1e12, 3),
+                   "achieved_tflops_aggregate": round(flops / (ms_per_step / 1e3) / 1e12, 1),
+                   "achieved_tflops_per_gpu": round(flops / world / (ms_per_step / 1e3) / 1e12, 1)},
+        "gpu_launches": int(lib.tlora_launch_count() - n0),
+        "clocks": clk,
+    }
 
 
 def run_reference(args, rank, world):
@@ -338,6 +411,10 @@ def main():
     ap.add_argument("--cpu-tokens-per-job", type=int, default=4)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-tokens-per-job", type=int, default=2)
+    ap.add_argument("--tp", action="store_true",
+                    help="tensor-parallel layer set over the torchrun group (default config C4)")
+    ap.add_argument("--nano", type=int, default=4, help="initial nano-batch count (TP mode)")
+    ap.add_argument("--aimd-steps", type=int, default=8, help="AIMD exploration steps (TP mode)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -351,15 +428,22 @@ def main():
             print(json.dumps(out), flush=True)
         return
 
-    if world > 1:
+    if args.tp and args.config == "C2" and "--config" not in sys.argv:
+        args.config = "C4"
+    if world > 1 or args.tp:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    out = run_ours(args, rank, world, local_rank)
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29555")
+            os.environ.setdefault("RANK", str(rank))
+            os.environ.setdefault("WORLD_SIZE", str(world))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_tp(args, rank, world, local_rank) if args.tp else run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if world > 1 or args.tp:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()

@@ -147,6 +147,26 @@ int tlora_forward(tlora_layer* layer, const tlora_plan* plan, const void* X, voi
 int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, const void* X,
                    const void* H_stash, void* dX, float beta, void* stream);
 
+/* Per-launch entry points of the same computation, for drivers that interleave
+ * collectives between the launches (tensor-parallel nano-batch pipeline). tlora_forward
+ * = shrink + gemm; tlora_backward = dh + dx + grad_b(H, dY) + grad_a(X, dH). H / dH are
+ * T x R bf16, masked to each token's own packed-rank columns (zero elsewhere), so partial
+ * H / dH summed across ranks stay valid operands. Calls on one plan are serialised on
+ * one stream (the split-K workspace belongs to the plan). */
+int tlora_forward_shrink(tlora_layer* layer, const tlora_plan* plan, const void* X, void* H,
+                         void* stream);
+int tlora_forward_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X, const void* H,
+                       void* Y, int y_dtype, void* stream);
+int tlora_backward_dh(tlora_layer* layer, const tlora_plan* plan, const void* dY, void* dH,
+                      void* stream);
+/* dX = dY·Wᵀ + dH·Aᵀ + beta·dX (beta = 1 sums the dX of projections sharing an input) */
+int tlora_backward_dx(tlora_layer* layer, const tlora_plan* plan, const void* dY, const void* dH,
+                      void* dX, float beta, void* stream);
+int tlora_backward_grad_b(tlora_layer* layer, const tlora_plan* plan, const void* H,
+                          const void* dY, float beta, void* stream);
+int tlora_backward_grad_a(tlora_layer* layer, const tlora_plan* plan, const void* X,
+                          const void* dH, float beta, void* stream);
+
 /* ---- live launch profiling (CUDA events on each launch's own stream) ------------- */
 /* Between begin and end every GEMM launch is bracketed by CUDA events. end() waits for
  * them and returns, per tlora_launch kind, the launch count, summed device ms and the

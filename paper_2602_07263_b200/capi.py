@@ -76,6 +76,17 @@ SIGNATURES = {
                                 C.c_void_p, C.c_void_p]),
     "tlora_backward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_float, C.c_void_p]),
+    "tlora_forward_shrink": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p]),
+    "tlora_forward_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_int, C.c_void_p]),
+    "tlora_backward_dh": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tlora_backward_dx": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_float, C.c_void_p]),
+    "tlora_backward_grad_b": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_float, C.c_void_p]),
+    "tlora_backward_grad_a": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_float, C.c_void_p]),
     "tlora_profile_begin": (C.c_int, []),
     "tlora_launch_count": (C.c_longlong, []),
     "tlora_profile_end": (C.c_int, [C.POINTER(C.c_int32), C.POINTER(C.c_double),

@@ -48,7 +48,7 @@ struct GemmArgs {
   void* out;
   int64_t ldo;       // elements
   int64_t split_stride;  // elements between split-K partial planes (EPI_F32)
-  float beta;        // EPI_F32: out = acc + beta * out
+  float beta;        // EPI_F32 / EPI_BF16: out = acc + beta * out
   // EPI_BF16_MASK: column window per row = [col_lo[slot], col_hi[slot])
   const int32_t* row_slot;
   const int32_t* slot_col_lo;
@@ -85,6 +85,19 @@ __device__ __forceinline__ void epi_store32(const GemmArgs& args, int split, int
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + (int64_t)row * args.ldo + col0;
     if (col0 + 32 <= args.N) {
       uint4* o4 = reinterpret_cast<uint4*>(o);
+      if (args.beta != 0.f) {  // out = acc + beta * out (in fp32, one bf16 rounding)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 p = o4[q];
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&p);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 pf = __bfloat1622float2(h[e]);
+            f[8 * q + 2 * e] += args.beta * pf.x;
+            f[8 * q + 2 * e + 1] += args.beta * pf.y;
+          }
+        }
+      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         uint4 w;
@@ -97,7 +110,9 @@ __device__ __forceinline__ void epi_store32(const GemmArgs& args, int split, int
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (col0 + i < args.N) o[i] = __float2bfloat16_rn(f[i]);
+        if (col0 + i < args.N)
+          o[i] = __float2bfloat16_rn(args.beta != 0.f ? f[i] + args.beta * __bfloat162float(o[i])
+                                                      : f[i]);
     }
   } else {
     float* o = reinterpret_cast<float*>(args.out) + (int64_t)split * args.split_stride +

@@ -720,12 +720,155 @@ int tlora_plan_tiles_host(int64_t d, int64_t k, int32_t num_slots, const int32_t
   });
 }
 
+}  // extern "C"
+
+// ==================================================================== launch bodies
+namespace {
+
+void check_bound(const tlora_layer* layer, const tlora_plan* plan) {
+  require(layer != nullptr && plan != nullptr, TLORA_ERR_ARG, "null layer/plan");
+  require(plan->layer_id == layer->id, TLORA_ERR_PLAN, "plan was built for another layer");
+  require(layer->base_set, TLORA_ERR_ARG, "base weight not set");
+}
+
+// H = X·Aᵀcatᵀ masked to each token's own packed columns. Shrink tiles write only their
+// token tile's rank window; the gradient launches read H over whole job token ranges, so
+// every other column must be an exact zero (memset first).
+void run_shrink(tlora_layer* layer, const tlora_plan* plan, const void* X, void* H, cudaStream_t s) {
+  const auto& L = layer->L;
+  const int64_t T = plan->P.T, d = L.d, R = L.R;
+  TL_CUDA(cudaMemsetAsync(H, 0, (size_t)T * R * 2, s));
+  GemmArgs a{};
+  a.tiles = plan->tiles[TLORA_L_SHRINK].p;
+  a.num_tiles = (int)plan->P.tiles[TLORA_L_SHRINK].size();
+  a.M = (int)T;
+  a.N = (int)R;
+  a.out = H;
+  a.ldo = R;
+  a.row_slot = plan->token_slot.p;
+  a.slot_col_lo = layer->col_lo.p;
+  a.slot_col_hi = layer->col_hi.p;
+  const CUtensorMap ma = tmap_k(X, d, T, tlora::kBM);
+  const CUtensorMap mb = tmap_k(layer->AT.p, d, R, tlora::kPlanBNLow);
+  launch_gemm<128, false, false, tlora::EPI_BF16_MASK, 6>(ma, mb, ma, mb, a, layer->sm_count, s,
+                                                          TLORA_L_SHRINK,
+                                                          2.0 * (double)plan->P.tok_rank * d);
+}
+
+// Y = X·W + H·Bᵀcatᵀ: 2-CTA fused GEMM, K-extension over each tile's packed-rank window.
+void run_fwd_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X, const void* H, void* Y,
+                  int y_dtype, cudaStream_t s) {
+  const auto& L = layer->L;
+  const int64_t T = plan->P.T, d = L.d, k = L.k, R = L.R;
+  const double flops = 2.0 * T * d * k + 2.0 * (double)plan->P.tok_rank * k;
+  GemmArgs a{};
+  a.tiles = plan->tiles[TLORA_L_FWD].p;
+  a.num_tiles = (int)plan->P.tiles[TLORA_L_FWD].size();
+  a.M = (int)T;
+  a.N = (int)k;
+  a.out = Y;
+  a.ldo = k;
+  a.beta = 0.f;
+  const CUtensorMap ma0 = tmap_k(X, d, T, 128);
+  const CUtensorMap mb0 = tmap_k(layer->Wt16.p, d, k, 128);
+  const CUtensorMap ma1 = tmap_k(H, R, T, 128);
+  const CUtensorMap mb1 = tmap_k(layer->BcatT.p, R, k, 128);
+  if (y_dtype == TLORA_BF16)
+    launch_gemm2<tlora::EPI_BF16, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD, flops);
+  else
+    launch_gemm2<tlora::EPI_F32, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD, flops);
+}
+
+// dH = dY·Bᵀ (masked; zero outside the windows, as H)
+void run_dh(tlora_layer* layer, const tlora_plan* plan, const void* dY, void* dH, cudaStream_t s) {
+  const auto& L = layer->L;
+  const int64_t T = plan->P.T, k = L.k, R = L.R;
+  TL_CUDA(cudaMemsetAsync(dH, 0, (size_t)T * R * 2, s));
+  GemmArgs a{};
+  a.tiles = plan->tiles[TLORA_L_DH].p;
+  a.num_tiles = (int)plan->P.tiles[TLORA_L_DH].size();
+  a.M = (int)T;
+  a.N = (int)R;
+  a.out = dH;
+  a.ldo = R;
+  a.row_slot = plan->token_slot.p;
+  a.slot_col_lo = layer->col_lo.p;
+  a.slot_col_hi = layer->col_hi.p;
+  const CUtensorMap ma = tmap_k(dY, k, T, tlora::kBM);
+  const CUtensorMap mb = tmap_k(layer->Bcat.p, k, R, tlora::kPlanBNLow);
+  launch_gemm<128, false, false, tlora::EPI_BF16_MASK, 6>(ma, mb, ma, mb, a, layer->sm_count, s,
+                                                          TLORA_L_DH,
+                                                          2.0 * (double)plan->P.tok_rank * k);
+}
+
+// dX = dY·Wᵀ + dH·Aᵀ (2-CTA fused GEMM)
+void run_dx(tlora_layer* layer, const tlora_plan* plan, const void* dY, const void* dH, void* dX,
+            float beta, cudaStream_t s) {
+  const auto& L = layer->L;
+  const int64_t T = plan->P.T, d = L.d, k = L.k, R = L.R;
+  GemmArgs a{};
+  a.tiles = plan->tiles[TLORA_L_DX].p;
+  a.num_tiles = (int)plan->P.tiles[TLORA_L_DX].size();
+  a.M = (int)T;
+  a.N = (int)d;
+  a.out = dX;
+  a.ldo = d;
+  a.beta = beta;
+  const CUtensorMap ma0 = tmap_k(dY, k, T, 128);
+  const CUtensorMap mb0 = tmap_k(layer->W16.p, k, d, 128);
+  const CUtensorMap ma1 = tmap_k(dH, R, T, 128);
+  const CUtensorMap mb1 = tmap_k(layer->Acat.p, R, d, 128);
+  launch_gemm2<tlora::EPI_BF16, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_DX,
+                                   2.0 * T * d * k + 2.0 * (double)plan->P.tok_rank * d);
+}
+
+// which = 0: dBcat = Hᵀ·dY (lowrank = H, full = dY, N = k)
+// which = 1: dAᵀcat = dHᵀ·X (lowrank = dH, full = X, N = d)
+// over each rank tile's token range; grads = beta·grads + result (split-K reduced in order)
+void run_grad(tlora_layer* layer, const tlora_plan* plan, int which, const void* lowrank,
+              const void* full, float beta, cudaStream_t s) {
+  const auto& L = layer->L;
+  const int64_t T = plan->P.T, R = L.R;
+  const int launch = which == 0 ? TLORA_L_DB : TLORA_L_DA;
+  const int64_t N = which == 0 ? L.k : L.d;
+  const int nsplit = which == 0 ? plan->P.splits_db : plan->P.splits_da;
+  float* grads = which == 0 ? layer->dB.p : layer->dAT.p;
+  GemmArgs a{};
+  a.tiles = plan->tiles[launch].p;
+  a.num_tiles = (int)plan->P.tiles[launch].size();
+  a.M = (int)R;
+  a.N = (int)N;
+  a.ldo = N;
+  if (nsplit > 1) {
+    a.out = plan->partial.p;
+    a.split_stride = R * N;
+    a.beta = 0.f;
+  } else {
+    a.out = grads;
+    a.beta = beta;
+  }
+  const CUtensorMap ma = tmap_mn(lowrank, R, T);
+  const CUtensorMap mb = tmap_mn(full, N, T);
+  launch_gemm<128, true, true, tlora::EPI_F32, 6>(ma, mb, ma, mb, a, layer->sm_count, s, launch,
+                                                  2.0 * (double)plan->P.tok_rank * N);
+  if (nsplit > 1) {
+    const int32_t* cnt = which == 0 ? plan->cnt_db.p : plan->cnt_da.p;
+    const int64_t work = R * N / 4;
+    const int blocks = (int)std::min<int64_t>(tlora::ceil_div(work, 256), 4 * layer->sm_count);
+    reduce_splits_kernel<<<blocks, 256, 0, s>>>(plan->partial.p, R * N, cnt, R, N, beta, grads);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    TL_CUDA(cudaGetLastError());
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
 int tlora_forward(tlora_layer* layer, const tlora_plan* plan, const void* X, void* Y, int y_dtype,
                   void* H_stash, void* stream) {
   return guarded([&] {
-    require(layer != nullptr && plan != nullptr, TLORA_ERR_ARG, "null layer/plan");
-    require(plan->layer_id == layer->id, TLORA_ERR_PLAN, "plan was built for another layer");
-    require(layer->base_set, TLORA_ERR_ARG, "base weight not set");
+    check_bound(layer, plan);
     check_align(X, "X");
     check_align(Y, "Y");
     check_align(H_stash, "H_stash");
@@ -733,139 +876,96 @@ int tlora_forward(tlora_layer* layer, const tlora_plan* plan, const void* X, voi
             "Y dtype must be bf16 or f32");
     DeviceGuard g(layer->device);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const auto& L = layer->L;
-    const int64_t T = plan->P.T, d = L.d, k = L.k, R = L.R;
-    const double rt = (double)plan->P.tok_rank;
-    const double fwd_flops = 2.0 * T * d * k + 2.0 * rt * k;
+    run_shrink(layer, plan, X, H_stash, s);
+    run_fwd_gemm(layer, plan, X, H_stash, Y, y_dtype, s);
+  });
+}
 
-    // 1) shrink: H = X·Aᵀcatᵀ masked to each token's own packed columns. Shrink tiles
-    //    write only their token tile's rank window; the gradient launches read H over
-    //    whole job token ranges, so every other column must be an exact zero.
-    TL_CUDA(cudaMemsetAsync(H_stash, 0, (size_t)T * R * 2, s));
-    {
-      GemmArgs a{};
-      a.tiles = plan->tiles[TLORA_L_SHRINK].p;
-      a.num_tiles = (int)plan->P.tiles[TLORA_L_SHRINK].size();
-      a.M = (int)T;
-      a.N = (int)R;
-      a.out = H_stash;
-      a.ldo = R;
-      a.row_slot = plan->token_slot.p;
-      a.slot_col_lo = layer->col_lo.p;
-      a.slot_col_hi = layer->col_hi.p;
-      const CUtensorMap ma = tmap_k(X, d, T, tlora::kBM);
-      const CUtensorMap mb = tmap_k(layer->AT.p, d, R, tlora::kPlanBNLow);
-      launch_gemm<128, false, false, tlora::EPI_BF16_MASK, 6>(ma, mb, ma, mb, a, layer->sm_count, s,
-                                                              TLORA_L_SHRINK, 2.0 * rt * d);
-    }
-    // 2) fused base + expand: Y = X·W + H·Bᵀcatᵀ (K-extension over the tile's rank window)
-    {
-      GemmArgs a{};
-      a.tiles = plan->tiles[TLORA_L_FWD].p;
-      a.num_tiles = (int)plan->P.tiles[TLORA_L_FWD].size();
-      a.M = (int)T;
-      a.N = (int)k;
-      a.out = Y;
-      a.ldo = k;
-      a.beta = 0.f;
-      const CUtensorMap ma0 = tmap_k(X, d, T, 128);
-      const CUtensorMap mb0 = tmap_k(layer->Wt16.p, d, k, 128);
-      const CUtensorMap ma1 = tmap_k(H_stash, R, T, 128);
-      const CUtensorMap mb1 = tmap_k(layer->BcatT.p, R, k, 128);
-      if (y_dtype == TLORA_BF16)
-        launch_gemm2<tlora::EPI_BF16, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD,
-                                         fwd_flops);
-      else
-        launch_gemm2<tlora::EPI_F32, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD,
-                                        fwd_flops);
-    }
+int tlora_forward_shrink(tlora_layer* layer, const tlora_plan* plan, const void* X, void* H,
+                         void* stream) {
+  return guarded([&] {
+    check_bound(layer, plan);
+    check_align(X, "X");
+    check_align(H, "H");
+    DeviceGuard g(layer->device);
+    run_shrink(layer, plan, X, H, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int tlora_forward_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X, const void* H,
+                       void* Y, int y_dtype, void* stream) {
+  return guarded([&] {
+    check_bound(layer, plan);
+    check_align(X, "X");
+    check_align(H, "H");
+    check_align(Y, "Y");
+    require(y_dtype == TLORA_BF16 || y_dtype == TLORA_F32, TLORA_ERR_ARG,
+            "Y dtype must be bf16 or f32");
+    DeviceGuard g(layer->device);
+    run_fwd_gemm(layer, plan, X, H, Y, y_dtype, reinterpret_cast<cudaStream_t>(stream));
   });
 }
 
 int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, const void* X,
                    const void* H_stash, void* dX, float beta, void* stream) {
   return guarded([&] {
-    require(layer != nullptr && plan != nullptr, TLORA_ERR_ARG, "null layer/plan");
-    require(plan->layer_id == layer->id, TLORA_ERR_PLAN, "plan was built for another layer");
-    require(layer->base_set, TLORA_ERR_ARG, "base weight not set");
+    check_bound(layer, plan);
     check_align(dY, "dY");
     check_align(X, "X");
     check_align(H_stash, "H_stash");
     if (dX) check_align(dX, "dX");
     DeviceGuard g(layer->device);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const auto& L = layer->L;
-    const int64_t T = plan->P.T, d = L.d, k = L.k, R = L.R;
-    const double rt = (double)plan->P.tok_rank;
     __nv_bfloat16* dH = plan->dH.p;
+    run_dh(layer, plan, dY, dH, s);
+    if (dX) run_dx(layer, plan, dY, dH, dX, 0.f, s);
+    run_grad(layer, plan, 0, H_stash, dY, beta, s);
+    run_grad(layer, plan, 1, dH, X, beta, s);
+  });
+}
 
-    // 1) dH = dY·Bᵀ (masked; zero outside the windows, as H above)
-    TL_CUDA(cudaMemsetAsync(dH, 0, (size_t)T * R * 2, s));
-    {
-      GemmArgs a{};
-      a.tiles = plan->tiles[TLORA_L_DH].p;
-      a.num_tiles = (int)plan->P.tiles[TLORA_L_DH].size();
-      a.M = (int)T;
-      a.N = (int)R;
-      a.out = dH;
-      a.ldo = R;
-      a.row_slot = plan->token_slot.p;
-      a.slot_col_lo = layer->col_lo.p;
-      a.slot_col_hi = layer->col_hi.p;
-      const CUtensorMap ma = tmap_k(dY, k, T, tlora::kBM);
-      const CUtensorMap mb = tmap_k(layer->Bcat.p, k, R, tlora::kPlanBNLow);
-      launch_gemm<128, false, false, tlora::EPI_BF16_MASK, 6>(ma, mb, ma, mb, a, layer->sm_count, s,
-                                                              TLORA_L_DH, 2.0 * rt * k);
-    }
-    // 2) dX = dY·Wᵀ + dH·Aᵀ
-    if (dX) {
-      GemmArgs a{};
-      a.tiles = plan->tiles[TLORA_L_DX].p;
-      a.num_tiles = (int)plan->P.tiles[TLORA_L_DX].size();
-      a.M = (int)T;
-      a.N = (int)d;
-      a.out = dX;
-      a.ldo = d;
-      const CUtensorMap ma0 = tmap_k(dY, k, T, 128);
-      const CUtensorMap mb0 = tmap_k(layer->W16.p, k, d, 128);
-      const CUtensorMap ma1 = tmap_k(dH, R, T, 128);
-      const CUtensorMap mb1 = tmap_k(layer->Acat.p, R, d, 128);
-      launch_gemm2<tlora::EPI_BF16, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_DX,
-                                       2.0 * T * d * k + 2.0 * rt * d);
-    }
-    // 3) dBcat = Hᵀ·dY and 4) dAᵀcat = dHᵀ·X over each rank tile's token range
-    for (int which = 0; which < 2; ++which) {
-      const int launch = which == 0 ? TLORA_L_DB : TLORA_L_DA;
-      const int64_t N = which == 0 ? k : d;
-      const int nsplit = which == 0 ? plan->P.splits_db : plan->P.splits_da;
-      float* grads = which == 0 ? layer->dB.p : layer->dAT.p;
-      GemmArgs a{};
-      a.tiles = plan->tiles[launch].p;
-      a.num_tiles = (int)plan->P.tiles[launch].size();
-      a.M = (int)R;
-      a.N = (int)N;
-      a.ldo = N;
-      if (nsplit > 1) {
-        a.out = plan->partial.p;
-        a.split_stride = R * N;
-        a.beta = 0.f;
-      } else {
-        a.out = grads;
-        a.beta = beta;
-      }
-      const CUtensorMap ma = tmap_mn(which == 0 ? H_stash : (const void*)dH, R, T);
-      const CUtensorMap mb = tmap_mn(which == 0 ? dY : X, N, T);
-      launch_gemm<128, true, true, tlora::EPI_F32, 6>(ma, mb, ma, mb, a, layer->sm_count, s, launch,
-                                                      2.0 * rt * N);
-      if (nsplit > 1) {
-        const int32_t* cnt = which == 0 ? plan->cnt_db.p : plan->cnt_da.p;
-        const int64_t work = R * N / 4;
-        const int blocks = (int)std::min<int64_t>(tlora::ceil_div(work, 256), 4 * layer->sm_count);
-        reduce_splits_kernel<<<blocks, 256, 0, s>>>(plan->partial.p, R * N, cnt, R, N, beta, grads);
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        TL_CUDA(cudaGetLastError());
-      }
-    }
+int tlora_backward_dh(tlora_layer* layer, const tlora_plan* plan, const void* dY, void* dH,
+                      void* stream) {
+  return guarded([&] {
+    check_bound(layer, plan);
+    check_align(dY, "dY");
+    check_align(dH, "dH");
+    DeviceGuard g(layer->device);
+    run_dh(layer, plan, dY, dH, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int tlora_backward_dx(tlora_layer* layer, const tlora_plan* plan, const void* dY, const void* dH,
+                      void* dX, float beta, void* stream) {
+  return guarded([&] {
+    check_bound(layer, plan);
+    check_align(dY, "dY");
+    check_align(dH, "dH");
+    check_align(dX, "dX");
+    DeviceGuard g(layer->device);
+    run_dx(layer, plan, dY, dH, dX, beta, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int tlora_backward_grad_b(tlora_layer* layer, const tlora_plan* plan, const void* H,
+                          const void* dY, float beta, void* stream) {
+  return guarded([&] {
+    check_bound(layer, plan);
+    check_align(H, "H");
+    check_align(dY, "dY");
+    DeviceGuard g(layer->device);
+    run_grad(layer, plan, 0, H, dY, beta, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int tlora_backward_grad_a(tlora_layer* layer, const tlora_plan* plan, const void* X,
+                          const void* dH, float beta, void* stream) {
+  return guarded([&] {
+    check_bound(layer, plan);
+    check_align(X, "X");
+    check_align(dH, "dH");
+    DeviceGuard g(layer->device);
+    run_grad(layer, plan, 1, dH, X, beta, reinterpret_cast<cudaStream_t>(stream));
   });
 }
 

@@ -181,6 +181,29 @@ class FusedLoRALayer:
              C.c_float(beta), _stream_ptr(stream))
         return dX
 
+    # ---- per-launch entry points (tensor-parallel / nano-batch drivers)
+    def shrink(self, plan: Plan, X, H, stream=None):
+        call("tlora_forward_shrink", self._h, plan._h, _ptr(X), _ptr(H), _stream_ptr(stream))
+
+    def fused_gemm(self, plan: Plan, X, H, Y, stream=None):
+        call("tlora_forward_gemm", self._h, plan._h, _ptr(X), _ptr(H), _ptr(Y), _DT[Y.dtype],
+             _stream_ptr(stream))
+
+    def dh(self, plan: Plan, dY, dH, stream=None):
+        call("tlora_backward_dh", self._h, plan._h, _ptr(dY), _ptr(dH), _stream_ptr(stream))
+
+    def dx(self, plan: Plan, dY, dH, dX, beta=0.0, stream=None):
+        call("tlora_backward_dx", self._h, plan._h, _ptr(dY), _ptr(dH), _ptr(dX), C.c_float(beta),
+             _stream_ptr(stream))
+
+    def grad_b(self, plan: Plan, H, dY, beta=0.0, stream=None):
+        call("tlora_backward_grad_b", self._h, plan._h, _ptr(H), _ptr(dY), C.c_float(beta),
+             _stream_ptr(stream))
+
+    def grad_a(self, plan: Plan, X, dH, beta=0.0, stream=None):
+        call("tlora_backward_grad_a", self._h, plan._h, _ptr(X), _ptr(dH), C.c_float(beta),
+             _stream_ptr(stream))
+
     def close(self):
         if getattr(self, "_h", None):
             for p in list(getattr(self, "_plans", ())):

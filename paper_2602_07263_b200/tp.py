@@ -1,0 +1,336 @@
+"""Tensor-parallel fused multi-LoRA layer set with rank-aware nano-batches.
+
+One process per GPU; the P ranks of the group split W (Megatron style, sequence-parallel
+activations between projection groups):
+
+  column-parallel  q, k, v, gate, up   W[:, k/P], B_j[:, k/P] local, A_j replicated
+      fwd: shrink on this rank's token shard -> all-gather [X | H] -> fused GEMM (local N)
+      bwd: dH_p = dY_p·B_pᵀ and dX_p = dY_p·W_pᵀ + dH_p·Aᵀ are partial sums over ranks;
+           reduce-scatter [dX | dH] (dX of projections sharing an input summed in place
+           first), dA_j from the token shard (all-reduced over TP once per step),
+           dB_j local from the gathered H.
+  row-parallel     o, down             W[d/P, :], A_j[d/P, :] local, B_j replicated
+      fwd: partial H_p = X_p·A_p and Y_p = X_p·W_p + H_p·B; reduce-scatter Y
+      bwd: all-gather dY; dH = dY·Bᵀ exact; dX local; dA_j local; dB_j partial
+           (all-reduced over TP once per step).
+
+The combined batch (Σ_j B_j samples) is cut into N nano-batches with the reference's
+balanced `partition` (nano_pipeline.hpp:51-60); samples keep job order, so every nano-batch
+is job-contiguous (the fast case of the tile packer). A compute stream runs the tlora
+launches and a comm stream runs the NCCL collectives: the all-gather of nano n+1 and the
+reduce-scatter of nano n-1 overlap the GEMMs of nano n. N is adapted online by the
+reference's AIMD rule (nano_pipeline.hpp:99-112) from CUDA-event step times — the real
+version of the simulator loop sim_engine.hpp:306-315.
+
+Inputs of the four projection groups are independent synthetic activations (attention,
+norms and activations are outside the path); the collective pattern is the real one.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .layer import AimdState, FusedLoRALayer, aimd_step, partition
+from .workload import INPUT_GROUP, Workload
+
+COLUMN = ("q", "k", "v", "gate", "up")
+ROW = ("o", "down")
+
+
+# ------------------------------------------------------------------ pure host-side plan
+@dataclass
+class NanoBatch:
+    index: int
+    t0: int          # first global token of this nano-batch (nano order)
+    tokens: int      # T_n
+    slots: np.ndarray  # owning slot per token, job-contiguous
+
+    def shard(self, rank: int, world: int):
+        """(first row within the nano, rows) of this rank's sequence-parallel shard."""
+        assert self.tokens % world == 0
+        n = self.tokens // world
+        return rank * n, n
+
+
+def nano_batches(wl: Workload, n: int) -> list[NanoBatch]:
+    """partition(Σ_j B_j, n) samples into nano-batches, job order kept (rank-aware in the
+    sense that each nano-batch holds whole samples of consecutive jobs, so its tile plan
+    packs at most a few ranks per M-tile)."""
+    samples = [(s, j.seq_len) for s, j in enumerate(wl.jobs) for _ in range(j.batch)]
+    n_eff, counts = partition(len(samples), n)
+    out, i, t0 = [], 0, 0
+    for idx, c in enumerate(counts):
+        chunk = samples[i:i + c]
+        slots = np.concatenate([np.full(seq, s, np.int32) for s, seq in chunk])
+        out.append(NanoBatch(idx, t0, int(slots.shape[0]), slots))
+        i += c
+        t0 += int(slots.shape[0])
+    return out
+
+
+def shard_columns(full: torch.Tensor, rank: int, world: int) -> torch.Tensor:
+    k = full.shape[1]
+    assert k % world == 0
+    w = k // world
+    return full[:, rank * w:(rank + 1) * w].contiguous()
+
+
+def shard_rows(full: torch.Tensor, rank: int, world: int) -> torch.Tensor:
+    d = full.shape[0]
+    assert d % world == 0
+    w = d // world
+    return full[rank * w:(rank + 1) * w].contiguous()
+
+
+# ------------------------------------------------------------------ the driver
+class TPLayerSetStep:
+    def __init__(self, wl: Workload, rank: int, world: int, device: int, group=None,
+                 nano: int = 4, seed: int | None = None):
+        self.wl, self.rank, self.world, self.group = wl, rank, world, group
+        self.dev = torch.device("cuda", device)
+        self.T = wl.tokens
+        self.n = nano
+        self.compute = torch.cuda.current_stream(self.dev)
+        self.comm = torch.cuda.Stream(self.dev)
+        seed = wl.seed if seed is None else seed
+        self.layers, self.R = {}, {}
+        self.full_weights = {}
+        P, T = world, self.T
+        bf = torch.bfloat16
+        for pi, (name, d, k) in enumerate(wl.projections):
+            # identical full weights on every rank (same seed), then this rank's slice
+            g = torch.Generator(device=self.dev).manual_seed(seed * 1000 + pi)
+            W = (torch.randn(d, k, generator=g, device=self.dev) * d ** -0.5).bfloat16()
+            As = [(torch.randn(d, j.rank, generator=g, device=self.dev) * d ** -0.5).bfloat16()
+                  for j in wl.jobs]
+            Bs = [(torch.randn(j.rank, k, generator=g, device=self.dev) * j.rank ** -0.5).bfloat16()
+                  for j in wl.jobs]
+            if name in COLUMN:
+                lay = FusedLoRALayer(d, k // P, wl.ranks, device=device)
+                lay.set_base(shard_columns(W, rank, P))
+                for s in range(len(wl.jobs)):
+                    lay.set_adapter(s, As[s], shard_columns(Bs[s], rank, P))
+            else:
+                lay = FusedLoRALayer(d // P, k, wl.ranks, device=device)
+                lay.set_base(shard_rows(W, rank, P))
+                for s in range(len(wl.jobs)):
+                    lay.set_adapter(s, shard_rows(As[s], rank, P), Bs[s])
+            self.layers[name] = lay
+            self.R[name] = lay.R
+            self.full_weights[name] = (W, As, Bs)
+        # step-sized buffers; nano-batch n is a row range of each (no realloc when N moves)
+        gen = torch.Generator(device=self.dev).manual_seed(seed * 7919 + rank)
+        rnd = lambda *shape: torch.randn(*shape, generator=gen, device=self.dev).to(bf)  # noqa: E731
+        dims = {name: (d, k) for name, d, k in wl.projections}
+        self.groups = sorted({INPUT_GROUP[p] for p in COLUMN if p in dims})
+        gdim = {INPUT_GROUP[p]: dims[p][0] for p in COLUMN if p in dims}
+        self.X_shard = {g: rnd(T // P, gdim[g]) for g in self.groups}
+        self.X_full = {g: torch.empty(T, gdim[g], dtype=bf, device=self.dev) for g in self.groups}
+        self.dX_part = {g: torch.empty(T, gdim[g], dtype=bf, device=self.dev) for g in self.groups}
+        self.dX_shard = {g: torch.empty(T // P, gdim[g], dtype=bf, device=self.dev)
+                         for g in self.groups}
+        self.H_shard, self.H_full, self.Y, self.dY, self.dH_part, self.dH_shard = {}, {}, {}, {}, {}, {}
+        self.X_loc, self.H_row, self.Y_part, self.Y_shard, self.dY_shard, self.dY_full = ({}, {}, {},
+                                                                                         {}, {}, {})
+        self.dH_row, self.dX_loc = {}, {}
+        for name in COLUMN:
+            if name not in dims:
+                continue
+            d, k = dims[name]
+            R = self.R[name]
+            self.H_shard[name] = torch.empty(T // P, R, dtype=bf, device=self.dev)
+            self.H_full[name] = torch.empty(T, R, dtype=bf, device=self.dev)
+            self.Y[name] = torch.empty(T, k // P, dtype=bf, device=self.dev)
+            self.dY[name] = rnd(T, k // P)
+            self.dH_part[name] = torch.empty(T, R, dtype=bf, device=self.dev)
+            self.dH_shard[name] = torch.empty(T // P, R, dtype=bf, device=self.dev)
+        for name in ROW:
+            if name not in dims:
+                continue
+            d, k = dims[name]
+            R = self.R[name]
+            self.X_loc[name] = rnd(T, d // P)
+            self.H_row[name] = torch.empty(T, R, dtype=bf, device=self.dev)
+            self.Y_part[name] = torch.empty(T, k, dtype=bf, device=self.dev)
+            self.Y_shard[name] = torch.empty(T // P, k, dtype=bf, device=self.dev)
+            self.dY_shard[name] = rnd(T // P, k)
+            self.dY_full[name] = torch.empty(T, k, dtype=bf, device=self.dev)
+            self.dH_row[name] = torch.empty(T, R, dtype=bf, device=self.dev)
+            self.dX_loc[name] = torch.empty(T, d // P, dtype=bf, device=self.dev)
+        self._plans = {}
+        self.aimd = AimdState(n=nano)
+        torch.cuda.synchronize(self.dev)
+
+    # -------------------------------------------------------------- plans per N
+    def plans(self, n: int):
+        if n not in self._plans:
+            nb = nano_batches(self.wl, n)
+            per = []
+            for b in nb:
+                r0, rows = b.shard(self.rank, self.world)
+                shard_slots = b.slots[r0:r0 + rows]
+                per.append({name: (lay.plan(b.slots),
+                                   lay.plan(shard_slots) if name in COLUMN else None)
+                            for name, lay in self.layers.items()})
+            self._plans[n] = (nb, per)
+        return self._plans[n]
+
+    # -------------------------------------------------------------- helpers
+    def _rows(self, t, b: NanoBatch):
+        return t[b.t0:b.t0 + b.tokens]
+
+    def _srows(self, t, b: NanoBatch):
+        return t[b.t0 // self.world:(b.t0 + b.tokens) // self.world]
+
+    def _ag(self, out, inp):
+        dist.all_gather_into_tensor(out, inp, group=self.group)
+
+    def _rs(self, out, inp):
+        dist.reduce_scatter_tensor(out, inp, group=self.group)
+
+    # -------------------------------------------------------------- forward
+    def forward(self, n: int | None = None):
+        n = self.n if n is None else n
+        nb, plans = self.plans(n)
+        C, M = self.compute, self.comm
+        cols = [p for p in COLUMN if p in self.layers]
+        rows = [p for p in ROW if p in self.layers]
+
+        def shrink(i):
+            b = nb[i]
+            for p in cols:
+                self.layers[p].shrink(plans[i][p][1], self._srows(self.X_shard[INPUT_GROUP[p]], b),
+                                      self._srows(self.H_shard[p], b), stream=C)
+            ev = torch.cuda.Event()
+            ev.record(C)
+            return ev
+
+        def gather(i, ev):
+            b = nb[i]
+            M.wait_event(ev)
+            with torch.cuda.stream(M):
+                for g in self.groups:
+                    self._ag(self._rows(self.X_full[g], b), self._srows(self.X_shard[g], b))
+                for p in cols:
+                    self._ag(self._rows(self.H_full[p], b), self._srows(self.H_shard[p], b))
+            ev2 = torch.cuda.Event()
+            ev2.record(M)
+            return ev2
+
+        ev_g = gather(0, shrink(0))
+        for i in range(len(nb)):
+            ev_next = gather(i + 1, shrink(i + 1)) if i + 1 < len(nb) else None
+            b = nb[i]
+            C.wait_event(ev_g)
+            for p in cols:
+                self.layers[p].fused_gemm(plans[i][p][0], self._rows(self.X_full[INPUT_GROUP[p]], b),
+                                          self._rows(self.H_full[p], b), self._rows(self.Y[p], b),
+                                          stream=C)
+            for p in rows:
+                lay, pl = self.layers[p], plans[i][p][0]
+                lay.shrink(pl, self._rows(self.X_loc[p], b), self._rows(self.H_row[p], b), stream=C)
+                lay.fused_gemm(pl, self._rows(self.X_loc[p], b), self._rows(self.H_row[p], b),
+                               self._rows(self.Y_part[p], b), stream=C)
+            ev_y = torch.cuda.Event()
+            ev_y.record(C)
+            M.wait_event(ev_y)
+            with torch.cuda.stream(M):
+                for p in rows:
+                    self._rs(self._srows(self.Y_shard[p], b), self._rows(self.Y_part[p], b))
+            ev_g = ev_next
+        C.wait_stream(M)
+
+    # -------------------------------------------------------------- backward
+    def backward(self, n: int | None = None):
+        n = self.n if n is None else n
+        nb, plans = self.plans(n)
+        C, M = self.compute, self.comm
+        cols = [p for p in COLUMN if p in self.layers]
+        rows = [p for p in ROW if p in self.layers]
+        start = torch.cuda.Event()
+        start.record(C)
+
+        def gather_dy(i):
+            b = nb[i]
+            M.wait_event(start)
+            with torch.cuda.stream(M):
+                for p in rows:
+                    self._ag(self._rows(self.dY_full[p], b), self._srows(self.dY_shard[p], b))
+            ev = torch.cuda.Event()
+            ev.record(M)
+            return ev
+
+        def grad_a_cols(i, ev):
+            b = nb[i]
+            C.wait_event(ev)
+            for p in cols:
+                self.layers[p].grad_a(plans[i][p][1], self._srows(self.X_shard[INPUT_GROUP[p]], b),
+                                      self._srows(self.dH_shard[p], b), beta=1.0 if i else 0.0,
+                                      stream=C)
+
+        ev_dy = gather_dy(0)
+        pending = None
+        for i in range(len(nb)):
+            ev_dy_next = gather_dy(i + 1) if i + 1 < len(nb) else None
+            b = nb[i]
+            beta = 1.0 if i else 0.0
+            C.wait_event(ev_dy)
+            for p in rows:  # row-parallel: dH exact, dX local, dA local, dB partial
+                lay, pl = self.layers[p], plans[i][p][0]
+                dYf = self._rows(self.dY_full[p], b)
+                lay.dh(pl, dYf, self._rows(self.dH_row[p], b), stream=C)
+                lay.dx(pl, dYf, self._rows(self.dH_row[p], b), self._rows(self.dX_loc[p], b), stream=C)
+                lay.grad_b(pl, self._rows(self.H_row[p], b), dYf, beta=beta, stream=C)
+                lay.grad_a(pl, self._rows(self.X_loc[p], b), self._rows(self.dH_row[p], b),
+                           beta=beta, stream=C)
+            first = {}
+            for p in reversed(cols):  # column-parallel: partial dH / dX, local dB
+                lay, pl = self.layers[p], plans[i][p][0]
+                g = INPUT_GROUP[p]
+                dYl = self._rows(self.dY[p], b)
+                lay.dh(pl, dYl, self._rows(self.dH_part[p], b), stream=C)
+                lay.dx(pl, dYl, self._rows(self.dH_part[p], b), self._rows(self.dX_part[g], b),
+                       beta=1.0 if g in first else 0.0, stream=C)
+                first[g] = True
+                lay.grad_b(pl, self._rows(self.H_full[p], b), dYl, beta=beta, stream=C)
+            ev_c = torch.cuda.Event()
+            ev_c.record(C)
+            M.wait_event(ev_c)
+            with torch.cuda.stream(M):
+                for g in self.groups:
+                    self._rs(self._srows(self.dX_shard[g], b), self._rows(self.dX_part[g], b))
+                for p in cols:
+                    self._rs(self._srows(self.dH_shard[p], b), self._rows(self.dH_part[p], b))
+            ev_r = torch.cuda.Event()
+            ev_r.record(M)
+            if pending is not None:
+                grad_a_cols(*pending)
+            pending = (i, ev_r)
+            ev_dy = ev_dy_next
+        grad_a_cols(*pending)
+        # replicated adapter halves: sum the TP partials once per step
+        ev = torch.cuda.Event()
+        ev.record(C)
+        M.wait_event(ev)
+        with torch.cuda.stream(M):
+            for p in cols:
+                dist.all_reduce(self.layers[p].packed_grads()[0], group=self.group)  # dAᵀ
+            for p in rows:
+                dist.all_reduce(self.layers[p].packed_grads()[1], group=self.group)  # dB
+        C.wait_stream(M)
+
+    def step(self, n: int | None = None):
+        self.forward(n)
+        self.backward(n)
+
+    def adapt(self, step_seconds: float):
+        """AIMD update of N from a measured step time (nano_pipeline.hpp:99-112), clamped
+        to the combined batch as the simulator does (sim_engine.hpp:314)."""
+        self.aimd = aimd_step(self.aimd, step_seconds)
+        total = sum(j.batch for j in self.wl.jobs)
+        self.aimd.n = max(1, min(self.aimd.n, total))
+        self.n = self.aimd.n
+        return self.n
