@@ -233,7 +233,8 @@ int orc_aimd_step(int32_t* n, int32_t* has_prev, double* t_prev, int32_t alpha, 
 }
 
 /* ---------------------------------------------------------------- plan oracle */
-enum { BM = 128, BM2 = 256, BK = 64, BN_BASE = 256, BN_LOW = 128, GRAD_TARGET = 2 * 148, MIN_SPLIT = 512 };
+enum { BM = 128, BM2 = 256, BK = 64, BN_BASE = 256, BN_LOW = 128, GRAD_MAX_N = 256,
+       GRAD_TARGET = 2 * 148 };
 #define L2_BUDGET (48ll << 20)
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -314,36 +315,98 @@ int64_t orc_plan_tiles(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t
     free(win_lo);
     free(win_hi);
   } else {
-    const int64_t N = which == 4 ? k : d;
-    const int64_t n_rt = cdiv(R, BM), n_nt = cdiv(N, BN_LOW);
-    int64_t target = cdiv(GRAD_TARGET, n_rt * n_nt);
-    if (target < 1) target = 1;
-    for (int64_t rt = 0; rt < n_rt; ++rt) {
-      int64_t tlo = -1, thi = -1;
-      for (int64_t t = 0; t < T; ++t) {
-        const int64_t c0 = off[slot[t]], c1 = c0 + ranks[slot[t]];
-        if (c1 <= rt * BM || c0 >= (rt + 1) * BM) continue;
-        if (tlo < 0) tlo = t;
-        thi = t + 1;
-      }
-      if (tlo < 0) {
-        for (int64_t nt = 0; nt < n_nt; ++nt)
-          emit(&sink, (int32_t)(rt * BM), (int32_t)(nt * BN_LOW), 0, 0, 0, 0, 0);
-        continue;
-      }
-      const int64_t len = thi - tlo;
-      int64_t nsplit = len / MIN_SPLIT < target ? len / MIN_SPLIT : target;
-      if (nsplit < 1) nsplit = 1;
-      const int64_t chunk = cdiv(cdiv(len, nsplit), BK) * BK;
-      for (int64_t s = 0; s < nsplit; ++s) {
-        const int64_t kb = tlo + s * chunk;
-        const int64_t ke = thi < kb + chunk ? thi : kb + chunk;
-        if (kb >= ke) break;
-        for (int64_t nt = 0; nt < n_nt; ++nt)
-          emit(&sink, (int32_t)(rt * BM), (int32_t)(nt * BN_LOW), (int32_t)kb, (int32_t)ke, 0, 0,
-               (int32_t)s);
+    /* per-job transposed gradient tiles (dB: M-dim = k, dA: M-dim = d), brute force:
+     * token range of a job = [first token, last token] found by scanning. */
+    const int64_t Md = which == 4 ? k : d;
+    const int64_t n_mt = cdiv(Md, BM);
+    int64_t total = 0;
+    int64_t* first = (int64_t*)malloc(sizeof(int64_t) * S);
+    int64_t* last = (int64_t*)malloc(sizeof(int64_t) * S);
+    for (int32_t s = 0; s < S; ++s) {
+      first[s] = -1;
+      last[s] = -1;
+      for (int64_t t = 0; t < T; ++t)
+        if (slot[t] == s) {
+          if (first[s] < 0) first[s] = t;
+          last[s] = t;
+        }
+      if (first[s] < 0) continue;
+      for (int64_t q = 0; q < ranks[s]; q += GRAD_MAX_N) {
+        const int64_t nc = ranks[s] - q < GRAD_MAX_N ? ranks[s] - q : GRAD_MAX_N;
+        total += (last[s] + 1 - first[s]) * (BM + cdiv(nc, 64) * 64) * n_mt;
       }
     }
+    int64_t w_star = total / GRAD_TARGET;
+    if (w_star < 1) w_star = 1;
+    /* collect (work, order, tile) then sort by work desc, order asc (== stable sort) */
+    int64_t cap_t = 16, nt = 0;
+    int64_t* keyw = (int64_t*)malloc(sizeof(int64_t) * cap_t);
+    int32_t* tl = (int32_t*)malloc(sizeof(int32_t) * 8 * cap_t);
+#define PUSH(W_, m0_, n0_, kb_, ke_, sp_, nc_)                                   \
+  do {                                                                           \
+    if (nt == cap_t) {                                                           \
+      cap_t *= 2;                                                                \
+      keyw = (int64_t*)realloc(keyw, sizeof(int64_t) * cap_t);                   \
+      tl = (int32_t*)realloc(tl, sizeof(int32_t) * 8 * cap_t);                   \
+    }                                                                            \
+    keyw[nt] = (W_);                                                             \
+    int32_t* t_ = tl + 8 * nt;                                                   \
+    t_[0] = (m0_); t_[1] = (n0_); t_[2] = (kb_); t_[3] = (ke_);                  \
+    t_[4] = 0; t_[5] = 0; t_[6] = (sp_); t_[7] = (nc_);                          \
+    ++nt;                                                                        \
+  } while (0)
+    for (int32_t s = 0; s < S; ++s) {
+      for (int64_t q = 0; q < ranks[s]; q += GRAD_MAX_N) {
+        const int32_t c0 = off[s] + (int32_t)q;
+        const int32_t nc = (int32_t)(ranks[s] - q < GRAD_MAX_N ? ranks[s] - q : GRAD_MAX_N);
+        if (first[s] < 0) {
+          for (int64_t mt = 0; mt < n_mt; ++mt) PUSH(0, (int32_t)(mt * BM), c0, 0, 0, 0, nc);
+          continue;
+        }
+        const int64_t tlo = first[s], thi = last[s] + 1, len = thi - tlo;
+        const int64_t per_tile = len * (BM + cdiv(nc, 64) * 64);
+        int64_t c = cdiv(per_tile, w_star);
+        const int64_t cmax = len / 256 < 1 ? 1 : len / 256;
+        if (c > cmax) c = cmax;
+        if (c < 1) c = 1;
+        const int64_t chunk = cdiv(cdiv(len, c), BK) * BK;
+        for (int64_t sp = 0; sp < c; ++sp) {
+          const int64_t kb = tlo + sp * chunk;
+          const int64_t ke = thi < kb + chunk ? thi : kb + chunk;
+          if (kb >= ke) break;
+          for (int64_t mt = 0; mt < n_mt; ++mt)
+            PUSH((ke - kb) * (BM + cdiv(nc, 64) * 64), (int32_t)(mt * BM), c0, (int32_t)kb,
+                 (int32_t)ke, (int32_t)sp, nc);
+        }
+      }
+    }
+#undef PUSH
+    /* insertion-free stable order: repeatedly emit in (work desc, index asc) order */
+    int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (nt > 0 ? nt : 1));
+    for (int64_t i = 0; i < nt; ++i) idx[i] = i;
+    /* merge sort by (keyw desc, idx asc) */
+    int64_t* tmp = (int64_t*)malloc(sizeof(int64_t) * (nt > 0 ? nt : 1));
+    for (int64_t width = 1; width < nt; width *= 2) {
+      for (int64_t lo = 0; lo < nt; lo += 2 * width) {
+        int64_t mid = lo + width < nt ? lo + width : nt, hi = lo + 2 * width < nt ? lo + 2 * width : nt;
+        int64_t i = lo, j = mid, o = lo;
+        while (i < mid && j < hi) tmp[o++] = keyw[idx[j]] > keyw[idx[i]] ? idx[j++] : idx[i++];
+        while (i < mid) tmp[o++] = idx[i++];
+        while (j < hi) tmp[o++] = idx[j++];
+      }
+      memcpy(idx, tmp, sizeof(int64_t) * nt);
+    }
+    for (int64_t i = 0; i < nt; ++i) {
+      const int32_t* t_ = tl + 8 * idx[i];
+      if (sink.n < sink.cap) memcpy(sink.out + 8 * sink.n, t_, 8 * sizeof(int32_t));
+      sink.n++;
+    }
+    free(idx);
+    free(tmp);
+    free(keyw);
+    free(tl);
+    free(first);
+    free(last);
   }
   free(off);
   return sink.n;

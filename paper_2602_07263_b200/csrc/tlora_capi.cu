@@ -22,6 +22,7 @@
 #include "../../include/tlora.h"
 #include "lora_gemm.cuh"
 #include "lora_gemm2.cuh"
+#include "lora_grad.cuh"
 #include "tlora_plan.hpp"
 
 using tlora::GemmArgs;
@@ -165,12 +166,12 @@ void launch_gemm(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap
   TL_CUDA(cudaGetLastError());
 }
 
-template <int EPI, int ST>
+template <int EPI, int ST, bool AMN = false, bool BMN = false>
 void launch_gemm2(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1,
                   const CUtensorMap& b1, const GemmArgs& args, int sm_count, cudaStream_t s,
                   int launch_kind, double flops) {
   if (args.num_tiles == 0) return;
-  auto kern = tlora::lora_gemm2_kernel<EPI, ST>;
+  auto kern = tlora::lora_gemm2_kernel<EPI, ST, AMN, BMN>;
   constexpr int smem = tlora::Gemm2Smem<ST>::kDynamic;
   TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = std::min(2 * args.num_tiles, sm_count / 2 * 2);
@@ -267,7 +268,7 @@ __global__ void reduce_splits_kernel(const float* __restrict__ partial, int64_t 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R * n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / n4;
-    const int c = cnt[row / tlora::kBM];
+    const int c = cnt[row];
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < c; ++s) {
       const float4 p = reinterpret_cast<const float4*>(partial + s * plane)[i];
@@ -847,10 +848,21 @@ void run_grad(tlora_layer* layer, const tlora_plan* plan, int which, const void*
     a.out = grads;
     a.beta = beta;
   }
-  const CUtensorMap ma = tmap_mn(lowrank, R, T);
-  const CUtensorMap mb = tmap_mn(full, N, T);
-  launch_gemm<128, true, true, tlora::EPI_F32, 6>(ma, mb, ma, mb, a, layer->sm_count, s, launch,
-                                                  2.0 * (double)plan->P.tok_rank * N);
+  a.M = (int)N;  // transposed form: M = layer dimension, output rows = packed rank columns
+  const CUtensorMap ma = tmap_mn(full, N, T);
+  const CUtensorMap mb = tmap_mn(lowrank, R, T);
+  {
+    auto kern = tlora::lora_grad_kernel<4>;
+    constexpr int smem = tlora::GradSmem<4>::kDynamic;
+    TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int grid = std::min(a.num_tiles, layer->sm_count);
+    ProfScope ps(launch, 2.0 * (double)plan->P.tok_rank * N, s);
+    if (a.num_tiles > 0) {
+      kern<<<grid, tlora::kGemmThreads, smem, s>>>(ma, mb, a);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      TL_CUDA(cudaGetLastError());
+    }
+  }
   if (nsplit > 1) {
     const int32_t* cnt = which == 0 ? plan->cnt_db.p : plan->cnt_da.p;
     const int64_t work = R * N / 4;

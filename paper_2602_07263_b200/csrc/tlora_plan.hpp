@@ -55,14 +55,15 @@ constexpr int kPlanBMBase = 256;  // M tile of the fused base GEMMs (2-CTA pair)
 constexpr int kPlanBK = 64;       // K block
 constexpr int kPlanBNBase = 256;  // N tile of the fused base GEMMs (fwd, dX)
 constexpr int kPlanBNLow = 128;   // N tile of the low-rank launches (shrink, dH, dA, dB)
-constexpr int kPlanGradTargetTiles = 2 * 148;  // split-K target for the gradient launches
+constexpr int kPlanGradMaxN = 256;            // rank columns per gradient tile
+constexpr int kPlanGradTargetTiles = 2 * 148;  // split-K target: ~2 waves of CTAs
 constexpr int kPlanMinSplitTokens = 512;
 
 struct PlanTables {
   RegistryLayout layout;
   int64_t T = 0;
   std::vector<PlanTile> tiles[6];  // indexed by tlora_launch
-  std::vector<int32_t> split_count_db, split_count_da;  // per 128-row packed-rank tile
+  std::vector<int32_t> split_count_db, split_count_da;  // per packed rank row (R entries)
   int32_t splits_db = 1, splits_da = 1;
   int64_t useful_ext_cols = 0, packed_ext_cols = 0;
   int64_t tok_rank = 0;  // sum over tokens of the owning slot's rank (algorithmic work)
@@ -101,45 +102,61 @@ inline std::vector<std::pair<int32_t, int32_t>> raster_order(int64_t n_mt, int64
   return order;
 }
 
-// Gradient launches (dB: N = k, dA: N = d): rows = packed rank space, K = tokens.
-inline void build_grad_tiles(const RegistryLayout& L, const PlanTables& P, int64_t N,
+// Gradient launches, per job in transposed form (lora_grad.cuh):
+//   dB: M-dim = k, dA: M-dim = d; N = the job's own rank columns (<= 256 per tile);
+//   K = the job's token range [first, last] (only its own tokens when job-contiguous).
+// Long token ranges are split so that the largest tile is about total/kPlanGradTargetTiles
+// of the work; each split except a range's last ends on a 64-token boundary (TMA boxes of
+// split s never overlap split s+1). split_cnt has one entry per packed rank row. Tiles are
+// ordered largest-work first (stable), so the static round-robin over CTAs is balanced.
+inline void build_grad_tiles(const RegistryLayout& L, const PlanTables& P, int64_t Mdim,
                              std::vector<PlanTile>& out, std::vector<int32_t>& split_cnt,
                              int32_t& max_split) {
-  const int64_t n_rt = ceil_div(L.R, kPlanBM);
-  const int64_t n_nt = ceil_div(N, kPlanBNLow);
-  const int64_t target_split = std::max<int64_t>(1, ceil_div(kPlanGradTargetTiles, n_rt * n_nt));
+  const int64_t n_mt = ceil_div(Mdim, kPlanBM);
+  auto round64 = [](int64_t x) { return ceil_div(x, 64) * 64; };
+  split_cnt.assign(L.R, 0);
   max_split = 1;
-  split_cnt.assign(n_rt, 1);
-  for (int64_t rt = 0; rt < n_rt; ++rt) {
-    const int64_t r0 = rt * kPlanBM, r1 = r0 + kPlanBM;
-    int64_t tlo = -1, thi = -1;
-    for (size_t s = 0; s < L.rank.size(); ++s) {
-      const int64_t c0 = L.offset[s], c1 = c0 + L.rank[s];
-      if (c1 <= r0 || c0 >= r1 || P.slot_first[s] < 0) continue;
-      tlo = tlo < 0 ? P.slot_first[s] : std::min(tlo, P.slot_first[s]);
-      thi = std::max(thi, P.slot_last[s] + 1);
-    }
-    if (tlo < 0) {  // no token touches these rank rows: empty-K tiles write zeros
-      for (int64_t nt = 0; nt < n_nt; ++nt)
-        out.push_back({(int32_t)r0, (int32_t)(nt * kPlanBNLow), 0, 0, 0, 0, 0, 0});
-      continue;
-    }
-    const int64_t len = thi - tlo;
-    const int64_t nsplit =
-        std::max<int64_t>(1, std::min(target_split, len / kPlanMinSplitTokens));
-    const int64_t chunk = ceil_div(ceil_div(len, nsplit), kPlanBK) * kPlanBK;
-    int32_t used = 0;
-    for (int64_t s = 0; s < nsplit; ++s) {
-      const int64_t kb = tlo + s * chunk, ke = std::min(thi, kb + chunk);
-      if (kb >= ke) break;
-      for (int64_t nt = 0; nt < n_nt; ++nt)
-        out.push_back({(int32_t)r0, (int32_t)(nt * kPlanBNLow), (int32_t)kb, (int32_t)ke, 0, 0,
-                       (int32_t)s, 0});
-      ++used;
-    }
-    split_cnt[rt] = used;
-    max_split = std::max(max_split, used);
+  int64_t total = 0;
+  for (size_t s = 0; s < L.rank.size(); ++s) {
+    if (P.slot_first[s] < 0) continue;
+    const int64_t len = P.slot_last[s] + 1 - P.slot_first[s];
+    for (int64_t q = 0; q < L.rank[s]; q += kPlanGradMaxN)
+      total += len * (kPlanBM + round64(std::min<int64_t>(kPlanGradMaxN, L.rank[s] - q))) * n_mt;
   }
+  const int64_t w_star = std::max<int64_t>(1, total / kPlanGradTargetTiles);
+  std::vector<std::pair<int64_t, PlanTile>> tiles;
+  for (size_t s = 0; s < L.rank.size(); ++s) {
+    for (int64_t q = 0; q < L.rank[s]; q += kPlanGradMaxN) {
+      const int32_t c0 = L.offset[s] + (int32_t)q;
+      const int32_t nc = (int32_t)std::min<int64_t>(kPlanGradMaxN, L.rank[s] - q);
+      if (P.slot_first[s] < 0) {  // job absent from this batch: zero (beta-scaled) grads
+        for (int64_t mt = 0; mt < n_mt; ++mt)
+          tiles.push_back({0, {(int32_t)(mt * kPlanBM), c0, 0, 0, 0, 0, 0, nc}});
+        for (int32_t r = c0; r < c0 + nc; ++r) split_cnt[r] = 1;
+        continue;
+      }
+      const int64_t tlo = P.slot_first[s], thi = P.slot_last[s] + 1, len = thi - tlo;
+      const int64_t per_tile = len * (kPlanBM + round64(nc));
+      const int64_t c = std::max<int64_t>(
+          1, std::min(ceil_div(per_tile, w_star), std::max<int64_t>(1, len / 256)));
+      const int64_t chunk = ceil_div(ceil_div(len, c), kPlanBK) * kPlanBK;
+      int32_t used = 0;
+      for (int64_t sp = 0; sp < c; ++sp) {
+        const int64_t kb = tlo + sp * chunk, ke = std::min(thi, kb + chunk);
+        if (kb >= ke) break;
+        for (int64_t mt = 0; mt < n_mt; ++mt)
+          tiles.push_back({(ke - kb) * (kPlanBM + round64(nc)),
+                           {(int32_t)(mt * kPlanBM), c0, (int32_t)kb, (int32_t)ke, 0, 0,
+                            (int32_t)sp, nc}});
+        ++used;
+      }
+      for (int32_t r = c0; r < c0 + nc; ++r) split_cnt[r] = used;
+      max_split = std::max(max_split, used);
+    }
+  }
+  std::stable_sort(tiles.begin(), tiles.end(),
+                   [](const auto& x, const auto& y) { return x.first > y.first; });
+  for (auto& t : tiles) out.push_back(t.second);
 }
 
 inline PlanTables build_plan(const RegistryLayout& L, int64_t T, const int32_t* token_slot) {
