@@ -233,7 +233,7 @@ int orc_aimd_step(int32_t* n, int32_t* has_prev, double* t_prev, int32_t alpha, 
 }
 
 /* ---------------------------------------------------------------- plan oracle */
-enum { BM = 128, BM2 = 256, BK = 64, BN_BASE = 256, BN_LOW = 128, GRAD_MAX_N = 256,
+enum { BM = 128, BM2 = 256, BK = 64, BN_BASE = 256, BN_LOW = 128, GRAD_MAX_N = 128,
        GRAD_TARGET = 2 * 148 };
 #define L2_BUDGET (48ll << 20)
 

@@ -222,6 +222,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               for (int c = 0; c < BN / 64; ++c)
                 tma_load_2d(sb + c * (64 * kBK * 2), mb, &full_bar[stage], td.n0 + 64 * c, k);
             }
+#ifndef TLORA_PREFETCH_LOWRANK
+#define TLORA_PREFETCH_LOWRANK 0
+#endif
+            if constexpr (TLORA_PREFETCH_LOWRANK && !A_MN && !B_MN) {  // L2 prefetch ahead
+              const int kp = k + STAGES * kBK;
+              if (kp < ke) {
+                tma_prefetch_2d(ma, kp, td.m0);
+                tma_prefetch_2d(mb, kp, td.n0);
+              }
+            }
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
         }

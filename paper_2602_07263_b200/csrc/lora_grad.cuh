@@ -4,7 +4,7 @@
 //   dA_j  [d x r_j] = X_jᵀ  [d x T_j] · dH_j [T_j x r_j]      (dA_jᵀ is what is stored)
 //
 // M = the layer dimension (k or d, 128-row tiles), N = the job's own rank columns
-// (64-column MMA granules, runtime N <= 256), K = the job's token range only. A packed
+// (64-column MMA granules, runtime N <= 128), K = the job's token range only. A packed
 // formulation (M = packed rank space, K = tokens of every job in the tile) multiplies the
 // masked zeros of H/dH; here no MMA work is spent on other jobs' rows, and dY / X are read
 // once per M-tile row band: the launch is HBM-bound at ~the minimal bytes.
@@ -23,7 +23,7 @@ namespace tlora {
 template <int STAGES>
 struct GradSmem {
   static constexpr int kABytes = 128 * kBK * 2;  // 2 MN chunks
-  static constexpr int kBBytes = 256 * kBK * 2;  // up to 4 MN chunks
+  static constexpr int kBBytes = 128 * kBK * 2;  // up to 2 MN chunks (N <= 128)
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOffset = STAGES * kStageBytes;
   static constexpr int kTotal = kBarOffset + (2 * STAGES + 4) * 8 + 16;
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                      const GemmArgs args) {
   using namespace ptx;
   using L = GradSmem<STAGES>;
-  constexpr uint32_t kTmemCols = 512;
+  constexpr uint32_t kTmemCols = 256;
   constexpr uint32_t kChunk = 64 * kBK * 2;
 
   extern __shared__ uint8_t smem_raw[];
@@ -90,6 +90,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tma_load_2d(sa + kChunk, &tmA, &full_bar[stage], td.m0 + 64, k);
           for (int c = 0; c < nch; ++c)
             tma_load_2d(sb + c * kChunk, &tmB, &full_bar[stage], td.n0 + 64 * c, k);
+          // L2 prefetch one smem ring ahead (HBM latency > what the ring covers)
+#ifndef TLORA_PREFETCH_GRAD
+#define TLORA_PREFETCH_GRAD 0
+#endif
+          const int kp = k + STAGES * kBK;
+          if (TLORA_PREFETCH_GRAD && kp < td.ke0) {
+            tma_prefetch_2d(&tmA, td.m0, kp);
+            tma_prefetch_2d(&tmA, td.m0 + 64, kp);
+            for (int c = 0; c < nch; ++c) tma_prefetch_2d(&tmB, td.n0 + 64 * c, kp);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -109,7 +119,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         ++acc_iter;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * 256;
+        const uint32_t d_tmem = tmem_base + acc * 128;
 #pragma unroll 1
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
@@ -142,7 +152,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
       }
-      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * 256;
+      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * 128;
       float* out = reinterpret_cast<float*>(args.out) + (int64_t)td.split * args.split_stride;
 #pragma unroll 1
       for (int c0 = 0; c0 < td.pad; c0 += 32) {

@@ -852,8 +852,11 @@ void run_grad(tlora_layer* layer, const tlora_plan* plan, int which, const void*
   const CUtensorMap ma = tmap_mn(full, N, T);
   const CUtensorMap mb = tmap_mn(lowrank, R, T);
   {
-    auto kern = tlora::lora_grad_kernel<4>;
-    constexpr int smem = tlora::GradSmem<4>::kDynamic;
+#ifndef TLORA_GRAD_STAGES
+#define TLORA_GRAD_STAGES 6
+#endif
+    auto kern = tlora::lora_grad_kernel<TLORA_GRAD_STAGES>;
+    constexpr int smem = tlora::GradSmem<TLORA_GRAD_STAGES>::kDynamic;
     TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int grid = std::min(a.num_tiles, layer->sm_count);
     ProfScope ps(launch, 2.0 * (double)plan->P.tok_rank * N, s);

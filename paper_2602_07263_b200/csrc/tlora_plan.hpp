@@ -55,7 +55,7 @@ constexpr int kPlanBMBase = 256;  // M tile of the fused base GEMMs (2-CTA pair)
 constexpr int kPlanBK = 64;       // K block
 constexpr int kPlanBNBase = 256;  // N tile of the fused base GEMMs (fwd, dX)
 constexpr int kPlanBNLow = 128;   // N tile of the low-rank launches (shrink, dH, dA, dB)
-constexpr int kPlanGradMaxN = 256;            // rank columns per gradient tile
+constexpr int kPlanGradMaxN = 128;            // rank columns per gradient tile
 constexpr int kPlanGradTargetTiles = 2 * 148;  // split-K target: ~2 waves of CTAs
 constexpr int kPlanMinSplitTokens = 512;
 
