@@ -364,38 +364,35 @@ def run_tp(args, rank, world, local_rank):
 
 
 def run_reference(args, rank, world):
+    """Reference arm: the reference's own CPU implementation of the path (oracle/_ref/
+    ref_bench: unmodified fused_forward for fwd and dX, shim GEMM for dA/dB) on all host
+    threads; rank 0 only. One harness process: untimed setup, W warm-up repetitions, then
+    K timed repetitions (each = one bounded sample step of the workload)."""
     from paper_2602_07263_b200.workload import config
     wl = config(args.config)
     if rank != 0:
         return None
     from paper_2602_07263_b200 import cpu_baseline
     threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        cpu_baseline.measure(wl, tokens_per_job=args.ref_tokens_per_job, seconds_budget=0.0,
-                             threads=threads, repeats=1)
-    t0 = time.perf_counter()
-    res = None
-    tokens = 0
-    for _ in range(args.steps):
-        res = cpu_baseline.measure(wl, tokens_per_job=args.ref_tokens_per_job, seconds_budget=0.0,
-                                   threads=threads, repeats=1)
-        if res is None:
-            break
-        tokens += res["tokens"]
-    dt = time.perf_counter() - t0
-    if res is None:
-        return {"impl": "reference", "unavailable": "reference CPU build missing (run make ref)"}
-    value = tokens / dt
+    res = cpu_baseline.measure(wl, tokens_per_job=args.ref_tokens_per_job, seconds_budget=0.0,
+                               threads=threads, repeats=args.steps)
+    if res is None or res.get("value") is None:
+        why = (res or {}).get("sample", "reference CPU build missing (make ref)")
+        return {"impl": "reference", "unavailable": why}
+    per = res.get("per_repeat_s") or []
+    ms_per_step = 1e3 * (sum(per) / len(per)) if per else None
+    value = res["value"]
     return {
-        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tokens/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": world, "steps": len(per) or args.steps, "warmup": max(args.warmup, 1),
+        "ms_per_step": round(ms_per_step, 3) if ms_per_step else None, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": res["dtype"],
-        "data": "synthetic (seeded normal)",
-        "config": {"workload": f"{wl.name}: {wl.notes}", "sample": res["sample"]},
-        "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": res["cores"],
+        "data": "synthetic (seeded)",
+        "config": {"workload": f"{wl.name}: {wl.notes}", "sample": res["sample"],
+                   "tokens_per_step": res.get("tokens_per_repeat")},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": res["cores"],
                          "kind": res["kind"], "sample": res["sample"]},
-        "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -410,9 +407,9 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--shuffle", action="store_true", help="interleave jobs' tokens")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-tokens-per-job", type=int, default=4)
+    ap.add_argument("--cpu-tokens-per-job", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-tokens-per-job", type=int, default=2)
+    ap.add_argument("--ref-tokens-per-job", type=int, default=8)
     ap.add_argument("--tp", action="store_true",
                     help="tensor-parallel layer set over the torchrun group (default config C4)")
     ap.add_argument("--nano", type=int, default=4, help="initial nano-batch count (TP mode)")

@@ -275,7 +275,9 @@ int golden(const std::string& dir) {
 }
 
 // ------------------------------------------------------------------------- bench mode
-// ref_harness bench <threads> <tokens_per_job> <repeats> <ranks csv> <d:k;d:k;...>
+// ref_harness bench <threads> <tokens_per_job> <repeats> <ranks csv> <d:k;d:k;...> [min_s]
+// Setup (weights, inputs) is untimed; one warm-up repetition, then `repeats` timed
+// repetitions (or more, until min_s seconds have elapsed); per-repetition times printed.
 // One "step" = for every projection: reference fused_forward (fwd), reference
 // fused_forward on the transposed problem (dX = dY·(W + A_j B_j)ᵀ, exact), and the
 // adapter gradients dB_j = (X_j A_j)ᵀ dY_j, dA_j = X_jᵀ (dY_j B_jᵀ) with the shim GEMM
@@ -398,14 +400,22 @@ int bench(int argc, char** argv) {
     for (auto& t : ts) t.join();
     for (double v : sinks) checksum += v;
   };
+  const double min_s = argc > 7 ? std::atof(argv[7]) : 0.0;
   run_once();  // warm-up
-  const auto t0 = std::chrono::steady_clock::now();
-  for (int r = 0; r < repeats; ++r) run_once();
-  const double secs =
-      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::vector<double> per;
+  double secs = 0.0;
+  while ((int)per.size() < repeats || secs < min_s) {
+    const auto t0 = std::chrono::steady_clock::now();
+    run_once();
+    per.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    secs += per.back();
+    if (per.size() >= 100000) break;
+  }
   std::printf("{\"seconds\": %.6f, \"tokens\": %d, \"repeats\": %d, \"threads\": %d, "
-              "\"checksum\": %.6e}\n",
-              secs, tcount * repeats, repeats, threads, checksum);
+              "\"checksum\": %.6e, \"per_repeat\": [",
+              secs, tcount * (int)per.size(), (int)per.size(), threads, checksum);
+  for (size_t i = 0; i < per.size(); ++i) std::printf("%s%.6f", i ? ", " : "", per[i]);
+  std::printf("]}\n");
   return 0;
 }
 

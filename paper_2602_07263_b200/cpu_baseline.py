@@ -21,15 +21,16 @@ ROOT = Path(__file__).resolve().parents[1]
 REF = ROOT / "oracle" / "_ref" / "ref_bench"
 
 
-def _run_ref(wl, threads, tokens_per_job, repeats):
+def _run_ref(wl, threads, tokens_per_job, repeats, min_seconds=0.0):
     projs = ";".join(f"{d}:{k}" for _, d, k in wl.projections)
     ranks = ",".join(str(r) for r in wl.ranks)
     out = subprocess.run([str(REF), "bench", str(threads), str(tokens_per_job), str(repeats),
-                          ranks, projs], check=True, capture_output=True, text=True).stdout
+                          ranks, projs, str(min_seconds)], check=True, capture_output=True,
+                         text=True).stdout
     return json.loads(out.strip().splitlines()[-1])
 
 
-def _run_port(wl, threads, tokens_per_job, repeats):
+def _run_port(wl, threads, tokens_per_job, repeats, min_seconds=0.0):
     import numpy as np
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as O
@@ -41,12 +42,15 @@ def _run_port(wl, threads, tokens_per_job, repeats):
     for _, d, k in wl.projections:
         P.append((rs.randn(d, k) / np.sqrt(d), [rs.randn(d, r) for r in wl.ranks],
                   [rs.randn(r, k) for r in wl.ranks], rs.randn(T, d), rs.randn(T, k)))
-    t0 = time.perf_counter()
-    for _ in range(repeats):
+    per = []
+    while len(per) < repeats or sum(per) < min_seconds:
+        t0 = time.perf_counter()
         for W, A, B, X, dY in P:
             O.fused_forward(X, W, A, B, slots)
             O.fused_backward(X, W, A, B, slots, dY)
-    return {"seconds": time.perf_counter() - t0, "tokens": T * repeats, "threads": threads}
+        per.append(time.perf_counter() - t0)
+    return {"seconds": sum(per), "tokens": T * len(per), "threads": threads, "per_repeat": per,
+            "repeats": len(per)}
 
 
 def measure(wl, tokens_per_job=4, seconds_budget=15.0, threads=None, repeats=1):
@@ -56,20 +60,18 @@ def measure(wl, tokens_per_job=4, seconds_budget=15.0, threads=None, repeats=1):
     kind = "reference" if REF.exists() else "port"
     run = _run_ref if kind == "reference" else _run_port
     try:
-        res = run(wl, threads, tokens_per_job, 1)
-        if seconds_budget > 0 and res["seconds"] < seconds_budget:
-            reps = max(1, int(seconds_budget / max(res["seconds"], 1e-3)))
-            res = run(wl, threads, tokens_per_job, reps)
-        elif repeats > 1:
-            res = run(wl, threads, tokens_per_job, repeats)
+        res = run(wl, threads, tokens_per_job, max(1, repeats), seconds_budget)
     except Exception as e:  # pragma: no cover - reported, never silently replaced
         return {"value": None, "unit": "tokens/s", "cores": threads, "kind": kind,
                 "sample": f"failed: {e}"}
     value = res["tokens"] / res["seconds"]
     sample = (f"{tokens_per_job} tokens/job x {len(wl.jobs)} jobs through all "
               f"{len(wl.projections)} projections of {wl.name}, fwd+bwd, fp64, "
-              f"{res['tokens']} tokens in {res['seconds']:.2f} s on {threads} threads"
+              f"{res['tokens']} tokens in {res['seconds']:.2f} s ({res.get('repeats', 1)} timed "
+              f"repetitions after 1 warm-up, setup untimed) on {threads} threads"
               + (" (reference fused_forward for fwd and dX; shim GEMM for dA/dB)"
                  if kind == "reference" else " (C oracle port)"))
     return {"value": round(value, 3), "unit": "tokens/s", "cores": threads, "kind": kind,
-            "sample": sample, "tokens": res["tokens"], "dtype": "f64"}
+            "sample": sample, "tokens": res["tokens"], "dtype": "f64",
+            "per_repeat_s": res.get("per_repeat"), "tokens_per_repeat":
+                res["tokens"] // max(1, res.get("repeats", 1))}
