@@ -70,3 +70,14 @@ class LayerSetStep:
     def input_tensors(self):
         """Every tensor a step reads from outside the layer (for the e2e host copies)."""
         return list(self.X.values()) + list(self.dY.values())
+
+    # ---- double-buffered inputs (e2e: H2D of step i+1 overlaps compute of step i)
+    def make_input_sets(self, n: int = 2):
+        self._sets = [(self.X, self.dY)]
+        for _ in range(n - 1):
+            self._sets.append(({g: t.clone() for g, t in self.X.items()},
+                               {p: t.clone() for p, t in self.dY.items()}))
+        return [list(X.values()) + list(dY.values()) for X, dY in self._sets]
+
+    def use_inputs(self, i: int):
+        self.X, self.dY = self._sets[i]
