@@ -3,8 +3,9 @@
 
 Contract (see task / DESIGN.md §Measurement):
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
-One step = fwd+bwd of every adapted projection of the configured layer set over the
-whole multi-job token batch (BASELINE.json configs[1] = C2 by default). Rank 0 prints
+One step = one LoRA training step of the configured layer set over the whole multi-job
+token batch (BASELINE.json configs[1] = C2 by default): fwd + bwd of every adapted
+projection and the fused per-job AdamW update of every adapter. Rank 0 prints
 ONE JSON line. Under torchrun each rank runs one GPU (weak scaling: data-parallel
 replicas, adapter-gradient all-reduce over NCCL — the path's only exchange step).
 """
@@ -127,6 +128,7 @@ def run_ours(args, rank, world, local_rank):
     capi.call("tlora_device_check", local_rank, None)
     wl = config(args.config)
     step = LayerSetStep(wl, device=local_rank, seed=wl.seed + rank, shuffle=args.shuffle)
+    step.enable_optimizer()
     stream = torch.cuda.current_stream()
 
     comm_stream = torch.cuda.Stream() if world > 1 else None
@@ -144,12 +146,15 @@ def run_ours(args, rank, world, local_rank):
             pending.append(dist.all_reduce(dB, async_op=True))
 
     def one_step():
-        step.step(stream=stream, on_layer_done=allreduce_grads if world > 1 else None)
+        # training step: fwd + bwd (+ DP all-reduce) + fused multi-job AdamW of all adapters
+        step.forward(stream)
+        step.backward(stream, on_layer_done=allreduce_grads if world > 1 else None)
         if world > 1:
             for w in pending:
                 w.wait()
             pending.clear()
             stream.wait_stream(comm_stream)
+        step.optimizer_step(stream, grad_scale=1.0 / world)
 
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -225,6 +230,7 @@ def run_ours(args, rank, world, local_rank):
                     w.wait()
                 pending.clear()
                 stream.wait_stream(comm_stream)
+            step.optimizer_step(stream, grad_scale=1.0 / world)
             done[i].record(stream)
             with torch.cuda.stream(copy):
                 if i + 1 < nsteps:
@@ -334,6 +340,7 @@ def run_tp(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     wl = config(args.config)
     st = TPLayerSetStep(wl, rank, world, local_rank, nano=args.nano)
+    st.enable_optimizer()
     stream = torch.cuda.current_stream()
     clocks = ClockSampler(local_rank)
     clocks.start()

@@ -118,6 +118,19 @@ int tlora_layer_grad_ptrs(tlora_layer* layer, float** dAT, float** dB);
 int tlora_layer_read_grad(tlora_layer* layer, int32_t slot, float* dA, float* dB, int where,
                           void* stream);
 
+/* ---- fused multi-job AdamW over the packed adapters (optimizer step) -- */
+/* Per-slot learning rate and (decoupled) weight decay (num_slots entries; weight_decay
+ * may be NULL = 0); shared beta1/beta2/eps. Resets the moments and step counters. The
+ * fp32 masters are the values given to tlora_layer_set_adapter. */
+int tlora_layer_set_optimizer(tlora_layer* layer, const float* lr, const float* weight_decay,
+                              float beta1, float beta2, float eps);
+/* One AdamW step of every slot on grads * grad_scale (e.g. 1/world for a DP mean); writes
+ * the fp32 masters/moments and refreshes the bf16 operand layouts the kernels read. */
+int tlora_layer_optimizer_step(tlora_layer* layer, float grad_scale, void* stream);
+/* Copy one slot's fp32 master adapter out: A is d x r, B is r x k. */
+int tlora_layer_read_adapter(tlora_layer* layer, int32_t slot, float* A, float* B, int where,
+                             void* stream);
+
 /* ---- plan: the rank-aware tile-packing / indexing plan of one (nano-)batch ------ */
 /* token_slot[T] (host): owning slot of each token row, any interleaving allowed
  * (fused_lora.hpp:28-31). Errors: slot out of range -> TLORA_ERR_REGISTRY. */

@@ -63,6 +63,12 @@ SIGNATURES = {
     "tlora_layer_grad_ptrs": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "tlora_layer_read_grad": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int,
                                         C.c_void_p]),
+    "tlora_layer_set_optimizer": (C.c_int, [C.c_void_p, C.POINTER(C.c_float),
+                                            C.POINTER(C.c_float), C.c_float, C.c_float,
+                                            C.c_float]),
+    "tlora_layer_optimizer_step": (C.c_int, [C.c_void_p, C.c_float, C.c_void_p]),
+    "tlora_layer_read_adapter": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int,
+                                           C.c_void_p]),
     "tlora_plan_create": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int32),
                                     C.POINTER(C.c_void_p)]),
     "tlora_plan_destroy": (C.c_int, [C.c_void_p]),

@@ -7,7 +7,8 @@
 //   * fused forward  Y  = X·W  (+ segment 1: H·Bᵀcat over the tile's packed rank range)
 //   * shrink         H  = X·Acat, masked to each token's own job columns
 //   * backward       dX = dY·Wᵀ (+ segment 1: dH·Aᵀcat), dH = dY·Bᵀcat (masked)
-//   * adapter grads  dBcat = Hᵀ·dY, dAᵀcat = dHᵀ·X  (MN-major operands, token-range K)
+//   (the 2-CTA variant for the base GEMMs is lora_gemm2.cuh; the per-job adapter-gradient
+//    GEMM with MN-major operands is lora_grad.cuh)
 // Reference semantics: proj/include/lora_fleet/fused_lora.hpp:84-119 (forward); the
 // backward is new (the reference has none).
 //

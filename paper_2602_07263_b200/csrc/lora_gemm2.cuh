@@ -34,7 +34,7 @@ struct Gemm2Smem {
   static constexpr int kDynamic = kTotal + 1024;
 };
 
-template <int EPI, int STAGES, bool A_MN = false, bool B_MN = false>
+template <int EPI, int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     lora_gemm2_kernel(const __grid_constant__ CUtensorMap tmA0,
                       const __grid_constant__ CUtensorMap tmB0,
@@ -43,8 +43,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   using namespace ptx;
   using L = Gemm2Smem<STAGES>;
   constexpr uint32_t kTmemCols = 2 * kBN2;
-  constexpr uint32_t kIdesc = make_idesc_bf16(kBM2, kBN2, A_MN, B_MN);
-  constexpr uint32_t kChunk = 64 * kBK * 2;  // one 64(MN) x 64(K) MN-major TMA box
+  constexpr uint32_t kIdesc = make_idesc_bf16(kBM2, kBN2, false, false);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -107,18 +106,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             uint8_t* sb = sa + L::kABytes;
             if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * L::kStageBytes);
             const uint32_t fb = full0 + stage * 8;
-            if constexpr (!A_MN) {
-              tma_load_2d_cg2(sa, ma, fb, k, am);
-            } else {
-              tma_load_2d_cg2(sa, ma, fb, am, k);
-              tma_load_2d_cg2(sa + kChunk, ma, fb, am + 64, k);
-            }
-            if constexpr (!B_MN) {
-              tma_load_2d_cg2(sb, mb, fb, k, bn);
-            } else {
-              tma_load_2d_cg2(sb, mb, fb, bn, k);
-              tma_load_2d_cg2(sb + kChunk, mb, fb, bn + 64, k);
-            }
+            tma_load_2d_cg2(sa, ma, fb, k, am);
+            tma_load_2d_cg2(sb, mb, fb, k, bn);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
         }
@@ -148,13 +137,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
           const uint32_t sb = sa + L::kABytes;
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk) {
-            const uint64_t ad = A_MN ? make_smem_desc_mnmajor(sa + kk * 16 * 128, kChunk)
-                                     : make_smem_desc_kmajor(sa + kk * 32);
-            const uint64_t bd = B_MN ? make_smem_desc_mnmajor(sb + kk * 16 * 128, kChunk)
-                                     : make_smem_desc_kmajor(sb + kk * 32);
-            mma_bf16_ss_cg2(d_tmem, ad, bd, kIdesc, (kb | kk) != 0 ? 1u : 0u);
-          }
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            mma_bf16_ss_cg2(d_tmem, make_smem_desc_kmajor(sa + kk * 32),
+                            make_smem_desc_kmajor(sb + kk * 32), kIdesc, (kb | kk) != 0 ? 1u : 0u);
           mma_commit_cg2_mc(&empty_bar[stage], 0x3);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }

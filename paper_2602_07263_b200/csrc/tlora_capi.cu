@@ -166,12 +166,12 @@ void launch_gemm(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap
   TL_CUDA(cudaGetLastError());
 }
 
-template <int EPI, int ST, bool AMN = false, bool BMN = false>
+template <int EPI, int ST>
 void launch_gemm2(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1,
                   const CUtensorMap& b1, const GemmArgs& args, int sm_count, cudaStream_t s,
                   int launch_kind, double flops) {
   if (args.num_tiles == 0) return;
-  auto kern = tlora::lora_gemm2_kernel<EPI, ST, AMN, BMN>;
+  auto kern = tlora::lora_gemm2_kernel<EPI, ST>;
   constexpr int smem = tlora::Gemm2Smem<ST>::kDynamic;
   TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = std::min(2 * args.num_tiles, sm_count / 2 * 2);
@@ -212,21 +212,69 @@ __global__ void pack_base_kernel(const void* W, int dtype, int64_t d, int64_t k,
 // Adapter of one slot (A: d x r, B: r x k) -> the four packed bf16 layouts.
 __global__ void pack_adapter_kernel(const void* A, const void* B, int dtype, int64_t d, int64_t k,
                                     int r, int off, int R, __nv_bfloat16* AT, __nv_bfloat16* Acat,
-                                    __nv_bfloat16* BcatT, __nv_bfloat16* Bcat) {
+                                    __nv_bfloat16* BcatT, __nv_bfloat16* Bcat, float* ATm,
+                                    float* Bm) {
   const int64_t nA = d * r, nB = (int64_t)r * k;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nA + nB;
        i += (int64_t)gridDim.x * blockDim.x) {
     if (i < nA) {
       const int64_t row = i / r, j = i % r;  // A[row, j]
-      const __nv_bfloat16 v = __float2bfloat16_rn(load_as_float<float>(A, i, dtype));
+      const float f = load_as_float<float>(A, i, dtype);
+      const __nv_bfloat16 v = __float2bfloat16_rn(f);
       AT[(off + j) * d + row] = v;
       Acat[row * R + off + j] = v;
+      ATm[(off + j) * d + row] = f;
     } else {
       const int64_t q = i - nA, j = q / k, col = q % k;  // B[j, col]
-      const __nv_bfloat16 v = __float2bfloat16_rn(load_as_float<float>(B, q, dtype));
+      const float f = load_as_float<float>(B, q, dtype);
+      const __nv_bfloat16 v = __float2bfloat16_rn(f);
       Bcat[(off + j) * k + col] = v;
       BcatT[col * R + off + j] = v;
+      Bm[(off + j) * k + col] = f;
     }
+  }
+}
+
+// Fused multi-job AdamW over one packed adapter matrix P (R x N, fp32 master) with its
+// gradient G and moments; per-row job hyperparameters via row_slot -> hp[slot]. Writes the
+// bf16 operand copies in both layouts the kernels read: P16 (R x N) and P16t (N x R,
+// through a shared-memory transpose). Padding-gap rows stay exactly zero. HBM-bound:
+// 16 B read + 12 B written (fp32) + 4 B (bf16 x2) per parameter.
+__global__ void adamw_packed_kernel(const float* __restrict__ G, float* __restrict__ P,
+                                    float* __restrict__ Mo, float* __restrict__ Vo,
+                                    __nv_bfloat16* __restrict__ P16,
+                                    __nv_bfloat16* __restrict__ P16t,
+                                    const int32_t* __restrict__ row_slot,
+                                    const float4* __restrict__ hp, float b1, float b2, float eps,
+                                    float grad_scale, int64_t R, int64_t N) {
+  __shared__ float tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    float val = 0.f;
+    if (r < R && c < N) {
+      const int s = row_slot[r];
+      if (s >= 0) {
+        const int64_t idx = r * N + c;
+        const float4 h = hp[s];  // lr, wd, 1/(1-b1^t), 1/(1-b2^t)
+        const float g = G[idx] * grad_scale;
+        float p = P[idx];
+        const float m = b1 * Mo[idx] + (1.f - b1) * g;
+        const float v = b2 * Vo[idx] + (1.f - b2) * g * g;
+        p -= h.x * (m * h.z / (sqrtf(v * h.w) + eps) + h.y * p);
+        P[idx] = p;
+        Mo[idx] = m;
+        Vo[idx] = v;
+        val = p;
+      }
+      P16[r * N + c] = __float2bfloat16_rn(val);
+    }
+    tile[i][threadIdx.x] = val;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < R && c < N) P16t[c * R + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
   }
 }
 
@@ -346,6 +394,14 @@ struct tlora_layer {
   DevBuf<float> dAT, dB;
   DevBuf<int32_t> col_lo, col_hi;
   bool base_set = false;
+  // fused multi-job AdamW state (fp32 masters of the packed adapters + moments)
+  DevBuf<float> ATm, Bm, mA, vA, mB, vB;
+  DevBuf<int32_t> row_slot;  // packed rank row -> slot, -1 in padding gaps
+  DevBuf<float4> hparams;    // per slot {lr, weight_decay, 1/(1-b1^t), 1/(1-b2^t)}
+  std::vector<float> lr, wd;
+  std::vector<long long> steps;
+  float beta1 = 0.9f, beta2 = 0.999f, eps = 1e-8f;
+  bool opt_set = false;
 };
 
 struct tlora_plan {
@@ -506,6 +562,17 @@ int tlora_layer_create(int device, int64_t d, int64_t k, int32_t num_slots, cons
     layer->Bcat.alloc(R * k);
     layer->dAT.alloc(R * d);
     layer->dB.alloc(R * k);
+    layer->ATm.alloc(R * d);
+    layer->Bm.alloc(R * k);
+    TL_CUDA(cudaMemset(layer->ATm.p, 0, R * d * 4));
+    TL_CUDA(cudaMemset(layer->Bm.p, 0, R * k * 4));
+    {
+      std::vector<int32_t> rs(R, -1);
+      for (int s2 = 0; s2 < num_slots; ++s2)
+        for (int i = 0; i < rv[s2]; ++i) rs[layer->L.offset[s2] + i] = s2;
+      layer->row_slot.alloc(R);
+      TL_CUDA(cudaMemcpy(layer->row_slot.p, rs.data(), R * 4, cudaMemcpyHostToDevice));
+    }
     TL_CUDA(cudaMemset(layer->AT.p, 0, R * d * 2));
     TL_CUDA(cudaMemset(layer->Acat.p, 0, R * d * 2));
     TL_CUDA(cudaMemset(layer->BcatT.p, 0, R * k * 2));
@@ -564,7 +631,8 @@ int tlora_layer_set_adapter(tlora_layer* layer, int32_t slot, const void* A, con
     const void* b = stage_input(B, (size_t)r * k, dtype, where, tb, s);
     pack_adapter_kernel<<<256, 256, 0, s>>>(a, b, dtype, d, k, r, layer->L.offset[slot],
                                             layer->L.R, layer->AT.p, layer->Acat.p,
-                                            layer->BcatT.p, layer->Bcat.p);
+                                            layer->BcatT.p, layer->Bcat.p, layer->ATm.p,
+                                            layer->Bm.p);
     TL_CUDA(cudaGetLastError());
     if (ta.p || tb.p) TL_CUDA(cudaStreamSynchronize(s));
     layer->loaded[slot] = 1;
@@ -623,6 +691,101 @@ int tlora_layer_read_grad(tlora_layer* layer, int32_t slot, float* dA, float* dB
     if (where == TLORA_HOST) {
       TL_CUDA(cudaMemcpyAsync(dA, oa, d * r * 4, cudaMemcpyDeviceToHost, s));
       TL_CUDA(cudaMemcpyAsync(dB, ob, (size_t)r * k * 4, cudaMemcpyDeviceToHost, s));
+      TL_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+int tlora_layer_set_optimizer(tlora_layer* layer, const float* lr, const float* weight_decay,
+                              float beta1, float beta2, float eps) {
+  return guarded([&] {
+    require(layer != nullptr && lr != nullptr, TLORA_ERR_ARG, "null argument");
+    require(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && eps > 0.f,
+            TLORA_ERR_ARG, "invalid AdamW hyperparameters");
+    DeviceGuard g(layer->device);
+    const int S = (int)layer->L.rank.size();
+    const int64_t R = layer->L.R, d = layer->L.d, k = layer->L.k;
+    layer->lr.assign(lr, lr + S);
+    layer->wd.assign(S, 0.f);
+    if (weight_decay) layer->wd.assign(weight_decay, weight_decay + S);
+    layer->beta1 = beta1;
+    layer->beta2 = beta2;
+    layer->eps = eps;
+    if (!layer->opt_set) {
+      layer->mA.alloc(R * d);
+      layer->vA.alloc(R * d);
+      layer->mB.alloc(R * k);
+      layer->vB.alloc(R * k);
+      layer->hparams.alloc(S);
+      layer->steps.assign(S, 0);
+    }
+    TL_CUDA(cudaMemset(layer->mA.p, 0, R * d * 4));
+    TL_CUDA(cudaMemset(layer->vA.p, 0, R * d * 4));
+    TL_CUDA(cudaMemset(layer->mB.p, 0, R * k * 4));
+    TL_CUDA(cudaMemset(layer->vB.p, 0, R * k * 4));
+    layer->steps.assign(S, 0);
+    layer->opt_set = true;
+  });
+}
+
+int tlora_layer_optimizer_step(tlora_layer* layer, float grad_scale, void* stream) {
+  return guarded([&] {
+    require(layer != nullptr, TLORA_ERR_ARG, "layer is null");
+    require(layer->opt_set, TLORA_ERR_ARG, "optimizer not configured (tlora_layer_set_optimizer)");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int S = (int)layer->L.rank.size();
+    const int64_t R = layer->L.R, d = layer->L.d, k = layer->L.k;
+    std::vector<float4> hp(S);
+    for (int i = 0; i < S; ++i) {
+      const long long t = ++layer->steps[i];
+      hp[i] = make_float4(layer->lr[i], layer->wd[i],
+                          (float)(1.0 / (1.0 - std::pow((double)layer->beta1, (double)t))),
+                          (float)(1.0 / (1.0 - std::pow((double)layer->beta2, (double)t))));
+    }
+    TL_CUDA(cudaMemcpyAsync(layer->hparams.p, hp.data(), S * sizeof(float4), cudaMemcpyHostToDevice, s));
+    const dim3 block(32, 8);
+    adamw_packed_kernel<<<dim3((unsigned)tlora::ceil_div(d, 32), (unsigned)tlora::ceil_div(R, 32)),
+                          block, 0, s>>>(layer->dAT.p, layer->ATm.p, layer->mA.p, layer->vA.p,
+                                         layer->AT.p, layer->Acat.p, layer->row_slot.p,
+                                         layer->hparams.p, layer->beta1, layer->beta2, layer->eps,
+                                         grad_scale, R, d);
+    TL_CUDA(cudaGetLastError());
+    adamw_packed_kernel<<<dim3((unsigned)tlora::ceil_div(k, 32), (unsigned)tlora::ceil_div(R, 32)),
+                          block, 0, s>>>(layer->dB.p, layer->Bm.p, layer->mB.p, layer->vB.p,
+                                         layer->Bcat.p, layer->BcatT.p, layer->row_slot.p,
+                                         layer->hparams.p, layer->beta1, layer->beta2, layer->eps,
+                                         grad_scale, R, k);
+    TL_CUDA(cudaGetLastError());
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+  });
+}
+
+int tlora_layer_read_adapter(tlora_layer* layer, int32_t slot, float* A, float* B, int where,
+                             void* stream) {
+  return guarded([&] {
+    require(layer != nullptr, TLORA_ERR_ARG, "layer is null");
+    require(slot >= 0 && slot < (int)layer->L.rank.size(), TLORA_ERR_REGISTRY,
+            "slot " + std::to_string(slot) + " is not in the registry");
+    require(A != nullptr && B != nullptr, TLORA_ERR_ARG, "output pointer is null");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t d = layer->L.d, k = layer->L.k;
+    const int r = layer->L.rank[slot];
+    DevBuf<float> tmp;
+    float* oa = A;
+    float* ob = B;
+    if (where == TLORA_HOST) {
+      tmp.alloc(d * r + (int64_t)r * k);
+      oa = tmp.p;
+      ob = tmp.p + d * r;
+    }
+    read_grad_kernel<<<256, 256, 0, s>>>(layer->ATm.p, layer->Bm.p, d, k, r, layer->L.offset[slot],
+                                         oa, ob);
+    TL_CUDA(cudaGetLastError());
+    if (where == TLORA_HOST) {
+      TL_CUDA(cudaMemcpyAsync(A, oa, d * r * 4, cudaMemcpyDeviceToHost, s));
+      TL_CUDA(cudaMemcpyAsync(B, ob, (size_t)r * k * 4, cudaMemcpyDeviceToHost, s));
       TL_CUDA(cudaStreamSynchronize(s));
     }
   });

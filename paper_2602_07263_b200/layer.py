@@ -151,6 +151,28 @@ class FusedLoRALayer:
              _stream_ptr(stream))
         return dA, dB
 
+    # ---------------------------------------------------------------- optimizer
+    def set_optimizer(self, lr, weight_decay=None, beta1=0.9, beta2=0.999, eps=1e-8):
+        """Fused multi-job AdamW; lr / weight_decay: scalar or one value per slot."""
+        S = len(self.ranks)
+        lr = [float(lr)] * S if np.isscalar(lr) else [float(x) for x in lr]
+        wd = [0.0] * S if weight_decay is None else (
+            [float(weight_decay)] * S if np.isscalar(weight_decay) else [float(x) for x in weight_decay])
+        call("tlora_layer_set_optimizer", self._h, (C.c_float * S)(*lr), (C.c_float * S)(*wd),
+             float(beta1), float(beta2), float(eps))
+
+    def optimizer_step(self, grad_scale=1.0, stream=None):
+        call("tlora_layer_optimizer_step", self._h, C.c_float(grad_scale), _stream_ptr(stream))
+
+    def read_adapter(self, slot: int, stream=None):
+        r = self.ranks[slot]
+        dev = torch.device("cuda", self.device)
+        A = torch.empty(self.d, r, dtype=torch.float32, device=dev)
+        B = torch.empty(r, self.k, dtype=torch.float32, device=dev)
+        call("tlora_layer_read_adapter", self._h, int(slot), _ptr(A), _ptr(B), capi.DEVICE,
+             _stream_ptr(stream))
+        return A, B
+
     # ---------------------------------------------------------------- compute
     def plan(self, token_slot: Sequence[int]) -> Plan:
         p = Plan(self, token_slot)

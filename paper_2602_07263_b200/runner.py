@@ -63,9 +63,23 @@ class LayerSetStep:
             if on_layer_done is not None:
                 on_layer_done(name, self.layers[name])
 
+    def enable_optimizer(self, base_lr: float = 1e-4, weight_decay: float = 0.01):
+        """Per-job AdamW hyperparameters (each job is an independent fine-tuning run)."""
+        lrs = [base_lr * (1.0 + 0.25 * (s % 4)) for s in range(len(self.wl.jobs))]
+        for lay in self.layers.values():
+            lay.set_optimizer(lrs, weight_decay)
+        self.optim = True
+
+    def optimizer_step(self, stream=None, grad_scale: float = 1.0):
+        for lay in self.layers.values():
+            lay.optimizer_step(grad_scale, stream=stream)
+
     def step(self, stream=None, on_layer_done=None):
+        """One training step: forward, backward, fused AdamW update of every adapter."""
         self.forward(stream)
         self.backward(stream, on_layer_done=on_layer_done)
+        if getattr(self, "optim", False):
+            self.optimizer_step(stream)
 
     def input_tensors(self):
         """Every tensor a step reads from outside the layer (for the e2e host copies)."""

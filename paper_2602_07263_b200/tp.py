@@ -322,9 +322,20 @@ class TPLayerSetStep:
                 dist.all_reduce(self.layers[p].packed_grads()[1], group=self.group)  # dB
         C.wait_stream(M)
 
+    def enable_optimizer(self, base_lr: float = 1e-4, weight_decay: float = 0.01):
+        lrs = [base_lr * (1.0 + 0.25 * (s % 4)) for s in range(len(self.wl.jobs))]
+        for lay in self.layers.values():
+            lay.set_optimizer(lrs, weight_decay)
+        self.optim = True
+
     def step(self, n: int | None = None):
+        """Training step: fwd + bwd (TP collectives) + fused AdamW of every adapter shard
+        (replicated halves were all-reduced, so every rank applies identical updates)."""
         self.forward(n)
         self.backward(n)
+        if getattr(self, "optim", False):
+            for lay in self.layers.values():
+                lay.optimizer_step(1.0, stream=self.compute)
 
     def adapt(self, step_seconds: float):
         """AIMD update of N from a measured step time (nano_pipeline.hpp:99-112), clamped

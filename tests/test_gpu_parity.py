@@ -272,3 +272,50 @@ def test_c2_full_size_properties(proj):
         Yr[idx] += h @ Bs[s].float()
     err = (Y1 - Yr).abs().max().item() / max(1.0, Yr.abs().max().item())
     assert err <= 3e-3, err  # same H near-tie bound as the oracle comparison
+
+
+def test_fused_adamw_matches_restatement():
+    """Two AdamW steps of the fused multi-job optimizer vs a float64 numpy restatement
+    (per-job lr / weight decay, bias-corrected moments), then a forward with the refreshed
+    bf16 operand layouts vs the oracle on the updated adapters."""
+    X, W, A, B, slots, dY = _random_problem(600, 128, 136, [8, 24, 64], seed=9)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    lay = FusedLoRALayer(128, 136, [8, 24, 64])
+    lay.set_base(t(W).bfloat16())
+    for s in range(3):
+        lay.set_adapter(s, t(A[s]).float(), t(B[s]).float())
+    lr, wd, b1, b2, eps = [1e-2, 2e-2, 5e-3], [0.0, 0.1, 0.01], 0.9, 0.99, 1e-8
+    lay.set_optimizer(lr, wd, b1, b2, eps)
+    plan = lay.plan(slots)
+    Xd, dYd = t(X).bfloat16(), t(dY).bfloat16()
+    P = {s: [A[s].astype(np.float32).astype(np.float64), B[s].astype(np.float32).astype(np.float64)]
+         for s in range(3)}
+    M = {s: [np.zeros_like(P[s][0]), np.zeros_like(P[s][1])] for s in range(3)}
+    V = {s: [np.zeros_like(P[s][0]), np.zeros_like(P[s][1])] for s in range(3)}
+    scale = 0.5
+    for step in (1, 2):
+        Y, H = lay.forward(plan, Xd)
+        lay.backward(plan, dYd, Xd, H)
+        torch.cuda.synchronize()
+        grads = {s: [g.double().cpu().numpy() for g in lay.read_grad(s)] for s in range(3)}
+        lay.optimizer_step(grad_scale=scale)
+        torch.cuda.synchronize()
+        for s in range(3):
+            for i in range(2):
+                g = grads[s][i] * scale
+                M[s][i] = b1 * M[s][i] + (1 - b1) * g
+                V[s][i] = b2 * V[s][i] + (1 - b2) * g * g
+                mh, vh = M[s][i] / (1 - b1 ** step), V[s][i] / (1 - b2 ** step)
+                P[s][i] = P[s][i] - lr[s] * (mh / (np.sqrt(vh) + eps) + wd[s] * P[s][i])
+            got = [x.double().cpu().numpy() for x in lay.read_adapter(s)]
+            for i in range(2):
+                err = np.abs(got[i] - P[s][i]).max() / max(1e-6, np.abs(P[s][i]).max())
+                assert err < 1e-5, (step, s, i, err)
+    # the kernels now read the refreshed bf16 copies of the updated adapters
+    Y, _ = lay.forward(plan, Xd, y_dtype=torch.float32)
+    Ab = [bf(lay.read_adapter(s)[0].double().cpu().numpy()) for s in range(3)]
+    Bb = [bf(lay.read_adapter(s)[1].double().cpu().numpy()) for s in range(3)]
+    Ye = O.fused_forward(X, W, Ab, Bb, slots, round_bf16=True)
+    assert maxrel(Y.double().cpu().numpy(), Ye) <= 3e-3
+    lay.close()
