@@ -133,7 +133,8 @@ int tlora_layer_read_adapter(tlora_layer* layer, int32_t slot, float* A, float* 
 
 /* ---- plan: the rank-aware tile-packing / indexing plan of one (nano-)batch ------ */
 /* token_slot[T] (host): owning slot of each token row, any interleaving allowed
- * (fused_lora.hpp:28-31). Errors: slot out of range -> TLORA_ERR_REGISTRY. */
+ * (fused_lora.hpp:28-31). Errors: slot out of range -> TLORA_ERR_REGISTRY. A plan may be
+ * used with any layer of the same registry layout (d, k, ranks) on the same device. */
 int tlora_plan_create(tlora_layer* layer, int64_t tokens, const int32_t* token_slot,
                       tlora_plan** out);
 int tlora_plan_destroy(tlora_plan* plan);

@@ -404,6 +404,32 @@ struct tlora_layer {
   bool opt_set = false;
 };
 
+namespace {
+// Per-(device, stream) scratch for the split-K partial planes and tlora_backward's dH.
+// Launches on one stream are ordered, so one buffer per stream is race-free; growing
+// reallocates (cudaFree synchronises) — it happens only while shapes are first seen.
+struct Workspace {
+  DevBuf<char> partial, dh;
+};
+std::mutex g_ws_mu;
+std::map<std::pair<int, cudaStream_t>, std::unique_ptr<Workspace>> g_ws;
+
+template <class T>
+T* ws_get(int device, cudaStream_t s, bool dh, size_t count) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto& w = g_ws[{device, s}];
+  if (!w) w = std::make_unique<Workspace>();
+  DevBuf<char>& b = dh ? w->dh : w->partial;
+  const size_t bytes = count * sizeof(T);
+  if (b.n < bytes) {
+    TL_CUDA(cudaStreamSynchronize(s));
+    b.alloc(bytes);
+    if (dh) TL_CUDA(cudaMemset(b.p, 0, bytes));
+  }
+  return reinterpret_cast<T*>(b.p);
+}
+}  // namespace
+
 struct tlora_plan {
   tlora_layer* layer = nullptr;  // only dereferenced after checking layer_id (see bound())
   uint64_t layer_id = 0;
@@ -411,8 +437,6 @@ struct tlora_plan {
   tlora::PlanTables P;
   DevBuf<TileDesc> tiles[TLORA_L_COUNT];
   DevBuf<int32_t> token_slot, cnt_db, cnt_da;
-  DevBuf<__nv_bfloat16> dH;
-  DevBuf<float> partial;
 };
 
 namespace {
@@ -824,10 +848,7 @@ int tlora_plan_create(tlora_layer* layer, int64_t tokens, const int32_t* token_s
     TL_CUDA(cudaMemcpy(plan->cnt_da.p, plan->P.split_count_da.data(),
                        plan->P.split_count_da.size() * 4, cudaMemcpyHostToDevice));
     const int64_t R = layer->L.R;
-    plan->dH.alloc(tokens * R);
-    const int64_t nsplit = std::max(plan->P.splits_db, plan->P.splits_da);
-    if (nsplit > 1)
-      plan->partial.alloc(nsplit * R * std::max(layer->L.d, layer->L.k));
+
     *out = plan.release();
   });
 }
@@ -891,7 +912,13 @@ namespace {
 
 void check_bound(const tlora_layer* layer, const tlora_plan* plan) {
   require(layer != nullptr && plan != nullptr, TLORA_ERR_ARG, "null layer/plan");
-  require(plan->layer_id == layer->id, TLORA_ERR_PLAN, "plan was built for another layer");
+  // a plan serves every layer with the same registry layout (d, k, ranks) on its device,
+  // e.g. one plan per projection shape for a whole layer stack
+  const auto& a = plan->P.layout;
+  const auto& b = layer->L;
+  require(plan->layer_id == layer->id ||
+              (plan->device == layer->device && a.d == b.d && a.k == b.k && a.rank == b.rank),
+          TLORA_ERR_PLAN, "plan was built for a layer with a different registry layout");
   require(layer->base_set, TLORA_ERR_ARG, "base weight not set");
 }
 
@@ -1004,7 +1031,7 @@ void run_grad(tlora_layer* layer, const tlora_plan* plan, int which, const void*
   a.N = (int)N;
   a.ldo = N;
   if (nsplit > 1) {
-    a.out = plan->partial.p;
+    a.out = ws_get<float>(layer->device, s, false, (size_t)nsplit * R * N);
     a.split_stride = R * N;
     a.beta = 0.f;
   } else {
@@ -1033,7 +1060,8 @@ void run_grad(tlora_layer* layer, const tlora_plan* plan, int which, const void*
     const int32_t* cnt = which == 0 ? plan->cnt_db.p : plan->cnt_da.p;
     const int64_t work = R * N / 4;
     const int blocks = (int)std::min<int64_t>(tlora::ceil_div(work, 256), 4 * layer->sm_count);
-    reduce_splits_kernel<<<blocks, 256, 0, s>>>(plan->partial.p, R * N, cnt, R, N, beta, grads);
+    reduce_splits_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(a.out), R * N, cnt, R,
+                                                N, beta, grads);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     TL_CUDA(cudaGetLastError());
   }
@@ -1094,7 +1122,8 @@ int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, c
     if (dX) check_align(dX, "dX");
     DeviceGuard g(layer->device);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    __nv_bfloat16* dH = plan->dH.p;
+    __nv_bfloat16* dH =
+        ws_get<__nv_bfloat16>(layer->device, s, true, (size_t)plan->P.T * layer->L.R);
     run_dh(layer, plan, dY, dH, s);
     if (dX) run_dx(layer, plan, dY, dH, dX, 0.f, s);
     run_grad(layer, plan, 0, H_stash, dY, beta, s);

@@ -15,6 +15,16 @@ from .workload import INPUT_GROUP, Workload
 
 
 class LayerSetStep:
+    """Forward/backward/optimizer driver for `wl.layers` stacked layer sets.
+
+    Every (layer, projection) has its own frozen W, adapters, optimizer state and H stash
+    (the backward of layer L consumes the H its forward produced). One tile plan per
+    projection shape serves all layers (same registry layout). Activation buffers (X, Y,
+    dY, dX) are shared across layers: the layer is the unit of work here and attention /
+    norms / activations between projections are out of scope, so synthetic inputs stand in
+    for them.
+    """
+
     def __init__(self, wl: Workload, device: int = 0, seed: int | None = None,
                  shuffle: bool = False, y_dtype=torch.bfloat16):
         self.wl = wl
@@ -28,7 +38,10 @@ class LayerSetStep:
         self.slots = wl.token_slots(shuffle=shuffle)
         self.layers, self.plans = {}, {}
         self.X, self.Y, self.H, self.dY, self.dX = {}, {}, {}, {}, {}
-        for name, d, k in wl.projections:
+        self.keys = [(L, name) for L in range(wl.layers) for name, _, _ in wl.projections]
+        dims = {name: (d, k) for name, d, k in wl.projections}
+        for L, name in self.keys:
+            d, k = dims[name]
             lay = FusedLoRALayer(d, k, wl.ranks, device=device)
             W = torch.randn(d, k, generator=g, device=dev, dtype=torch.float32).mul_(d ** -0.5)
             lay.set_base(W.bfloat16())
@@ -37,31 +50,34 @@ class LayerSetStep:
                 A = torch.randn(d, j.rank, generator=g, device=dev).mul_(d ** -0.5).bfloat16()
                 B = torch.randn(j.rank, k, generator=g, device=dev).mul_(j.rank ** -0.5).bfloat16()
                 lay.set_adapter(s, A, B)
-            self.layers[name] = lay
-            self.plans[name] = lay.plan(self.slots)
+            self.layers[(L, name)] = lay
+            if name not in self.plans:
+                self.plans[name] = lay.plan(self.slots)
             grp = INPUT_GROUP.get(name, name)
             if grp not in self.X:
                 self.X[grp] = torch.randn(T, d, generator=g, device=dev).bfloat16()
-            self.Y[name] = torch.empty(T, k, dtype=y_dtype, device=dev)
-            self.H[name] = torch.empty(T, lay.R, dtype=torch.bfloat16, device=dev)
-            self.dY[name] = torch.randn(T, k, generator=g, device=dev).bfloat16()
-            self.dX[name] = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+            if name not in self.Y:
+                self.Y[name] = torch.empty(T, k, dtype=y_dtype, device=dev)
+                self.dY[name] = torch.randn(T, k, generator=g, device=dev).bfloat16()
+                self.dX[name] = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+            self.H[(L, name)] = torch.zeros(T, lay.R, dtype=torch.bfloat16, device=dev)
         torch.cuda.synchronize(dev)
 
     def x_of(self, name):
         return self.X[INPUT_GROUP.get(name, name)]
 
     def forward(self, stream=None):
-        for name, _, _ in self.wl.projections:
-            self.layers[name].forward(self.plans[name], self.x_of(name), self.Y[name],
-                                      self.H[name], stream=stream)
+        for L, name in self.keys:
+            self.layers[(L, name)].forward(self.plans[name], self.x_of(name), self.Y[name],
+                                           self.H[(L, name)], stream=stream)
 
     def backward(self, stream=None, beta: float = 0.0, on_layer_done=None):
-        for name, _, _ in reversed(self.wl.projections):
-            self.layers[name].backward(self.plans[name], self.dY[name], self.x_of(name),
-                                       self.H[name], self.dX[name], beta=beta, stream=stream)
+        for L, name in reversed(self.keys):
+            lay = self.layers[(L, name)]
+            lay.backward(self.plans[name], self.dY[name], self.x_of(name), self.H[(L, name)],
+                         self.dX[name], beta=beta, stream=stream)
             if on_layer_done is not None:
-                on_layer_done(name, self.layers[name])
+                on_layer_done((L, name), lay)
 
     def enable_optimizer(self, base_lr: float = 1e-4, weight_decay: float = 0.01):
         """Per-job AdamW hyperparameters (each job is an independent fine-tuning run)."""
