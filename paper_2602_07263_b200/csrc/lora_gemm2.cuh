@@ -82,6 +82,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   cluster_sync();  // peer barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  pdl_launch_dependents();   // persistent grid: all CTAs are resident, dependents may queue
+  pdl_wait_prerequisites();  // inputs written by the previous launch are visible after this
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================

@@ -72,6 +72,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  pdl_launch_dependents();   // persistent grid: all CTAs are resident, dependents may queue
+  pdl_wait_prerequisites();  // inputs written by the previous launch are visible after this
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer

@@ -224,6 +224,24 @@ __device__ __forceinline__ void mma_commit_cg2_mc(uint64_t* bar, uint16_t cta_ma
       : "memory");
 }
 
+// ----------------------------------------------------------------------------- PDL
+// Programmatic dependent launch: a persistent kernel lets its dependent grid launch as
+// soon as it starts (its CTAs fill SMs as ours drain) and waits for its own prerequisite
+// grid only after the prologue (barrier init, TMEM alloc, tensor-map prefetch).
+#ifndef TLORA_PDL
+#define TLORA_PDL 1
+#endif
+__device__ __forceinline__ void pdl_launch_dependents() {
+#if TLORA_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait_prerequisites() {
+#if TLORA_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 // ----------------------------------------------------------------------------- descriptors
 // Shared-memory matrix descriptor (tcgen05):
 //   [0,14) start addr >> 4 | [16,30) LBO >> 4 | [32,46) SBO >> 4 | [46,48) version = 1

@@ -151,6 +151,24 @@ struct ProfScope {
 };
 
 // ------------------------------------------------------------------ launch helpers
+// Launch a persistent kernel with programmatic stream serialisation (PDL): it may begin
+// while the previous kernel on the stream drains; the kernel itself waits
+// (griddepcontrol.wait) before touching data the previous launch produced.
+template <typename Kern, typename... Args>
+void launch_pdl(Kern kern, int grid, int smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(tlora::kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = TLORA_PDL ? 1 : 0;
+  TL_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 template <int BN, bool AMN, bool BMN, int EPI, int ST>
 void launch_gemm(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1,
                  const CUtensorMap& b1, const GemmArgs& args, int sm_count, cudaStream_t s,
@@ -161,9 +179,8 @@ void launch_gemm(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap
   TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = std::min(args.num_tiles, sm_count);
   ProfScope ps(launch_kind, flops, s);
-  kern<<<grid, tlora::kGemmThreads, smem, s>>>(a0, b0, a1, b1, args);
+  launch_pdl(kern, grid, smem, s, a0, b0, a1, b1, args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  TL_CUDA(cudaGetLastError());
 }
 
 template <int EPI, int ST>
@@ -176,9 +193,8 @@ void launch_gemm2(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
   TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = std::min(2 * args.num_tiles, sm_count / 2 * 2);
   ProfScope ps(launch_kind, flops, s);
-  kern<<<grid, tlora::kGemmThreads, smem, s>>>(a0, b0, a1, b1, args);
+  launch_pdl(kern, grid, smem, s, a0, b0, a1, b1, args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  TL_CUDA(cudaGetLastError());
 }
 
 // ------------------------------------------------------------------ small kernels
@@ -1051,9 +1067,8 @@ void run_grad(tlora_layer* layer, const tlora_plan* plan, int which, const void*
     const int grid = std::min(a.num_tiles, layer->sm_count);
     ProfScope ps(launch, 2.0 * (double)plan->P.tok_rank * N, s);
     if (a.num_tiles > 0) {
-      kern<<<grid, tlora::kGemmThreads, smem, s>>>(ma, mb, a);
+      launch_pdl(kern, grid, smem, s, ma, mb, a);
       g_launches.fetch_add(1, std::memory_order_relaxed);
-      TL_CUDA(cudaGetLastError());
     }
   }
   if (nsplit > 1) {
