@@ -129,26 +129,54 @@ def run_ours(args, rank, world, local_rank):
     wl = config(args.config)
     step = LayerSetStep(wl, device=local_rank, seed=wl.seed + rank, shuffle=args.shuffle)
     step.enable_optimizer()
+    if args.overlap > 0:
+        step.enable_overlap(args.overlap)
     stream = torch.cuda.current_stream()
 
     comm_stream = torch.cuda.Stream() if world > 1 else None
     pending = []
 
-    def allreduce_grads(name, layer):
+    bucket_at_end = os.environ.get("TLORA_DP_BUCKET", "per_layer") == "end"
+
+    def allreduce_grads(name, layer, ready=None):
+        if bucket_at_end:
+            return
         # DP replicas: all-reduce this projection's packed fp32 adapter grads on a comm
         # stream while the next projection's backward runs.
-        ev = torch.cuda.Event()
-        ev.record(stream)
+        ev = ready
+        if ev is None:
+            ev = torch.cuda.Event()
+            ev.record(stream)
         with torch.cuda.stream(comm_stream):
             comm_stream.wait_event(ev)
             dAT, dB = layer.packed_grads()
             pending.append(dist.all_reduce(dAT, async_op=True))
             pending.append(dist.all_reduce(dB, async_op=True))
 
+    flat_grads = None
+    if world > 1 and bucket_at_end:
+        flat_grads = [g for lay in step.layers.values() for g in lay.packed_grads()]
+
+    def fwd():
+        if args.overlap > 0:
+            step.forward_overlapped(stream)
+        else:
+            step.forward(stream)
+
+    def bwd():
+        cb = allreduce_grads if world > 1 else None
+        if args.overlap > 0:
+            step.backward_overlapped(stream, on_layer_done=cb)
+        else:
+            step.backward(stream, on_layer_done=cb)
+
     def one_step():
         # training step: fwd + bwd (+ DP all-reduce) + fused multi-job AdamW of all adapters
-        step.forward(stream)
-        step.backward(stream, on_layer_done=allreduce_grads if world > 1 else None)
+        fwd()
+        bwd()
+        if flat_grads is not None:
+            for g in flat_grads:
+                dist.all_reduce(g)
         if world > 1:
             for w in pending:
                 w.wait()
@@ -221,10 +249,10 @@ def run_ours(args, rank, world, local_rank):
             s = i % 2
             stream.wait_event(ev_in[s])
             step.use_inputs(s)
-            step.forward(stream)
+            fwd()
             if ev_out is not None:
                 stream.wait_event(ev_out)  # grads of step i-1 are on the host before reuse
-            step.backward(stream, on_layer_done=allreduce_grads if world > 1 else None)
+            bwd()
             if world > 1:
                 for w in pending:
                     w.wait()
@@ -310,7 +338,7 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": f"{wl.name}: {wl.notes}", "tokens_per_gpu": wl.tokens,
                    "jobs": [[j.job_id, j.rank, j.tokens] for j in wl.jobs],
                    "projections": wl.projections, "token_order": "shuffled" if args.shuffle else "job-contiguous",
-                   "parallelism": f"dp{world}", "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)",
+                   "parallelism": f"dp{world}", "lowrank_side_stream_sms": args.overlap, "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)",
                    "algorithmic_tflop_per_step": round(flops_step / 1e12, 3),
                    "achieved_tflops_step": round(flops_step / (ms_per_step / 1e3) / 1e12, 1)},
         "e2e": {"value": round(tokens / (e2e_ms / 1e3), 1), "unit": "tokens/s",
@@ -449,6 +477,9 @@ def main():
     ap.add_argument("--cpu-tokens-per-job", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-tokens-per-job", type=int, default=8)
+    ap.add_argument("--overlap", type=int, default=0,
+                    help="SMs for the low-rank launches on a side stream, concurrent with the "
+                         "fused GEMMs (0 = serial schedule)")
     ap.add_argument("--tp", action="store_true",
                     help="tensor-parallel layer set over the torchrun group (default config C4)")
     ap.add_argument("--nano", type=int, default=4, help="initial nano-batch count (TP mode)")

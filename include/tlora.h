@@ -181,6 +181,12 @@ int tlora_backward_grad_b(tlora_layer* layer, const tlora_plan* plan, const void
 int tlora_backward_grad_a(tlora_layer* layer, const tlora_plan* plan, const void* X,
                           const void* dH, float beta, void* stream);
 
+/* Cap the persistent grid sizes on `device`: fused GEMM launches (fwd / dX) use at most
+ * gemm_sms SMs (rounded down to CTA pairs), low-rank launches (shrink, dH, dA, dB) at
+ * most lowrank_sms. With gemm_sms + lowrank_sms <= SM count a driver can run the two
+ * classes concurrently on two streams. 0 = no cap (default). */
+int tlora_set_sm_budget(int device, int32_t gemm_sms, int32_t lowrank_sms);
+
 /* ---- live launch profiling (CUDA events on each launch's own stream) ------------- */
 /* Between begin and end every GEMM launch is bracketed by CUDA events. end() waits for
  * them and returns, per tlora_launch kind, the launch count, summed device ms and the

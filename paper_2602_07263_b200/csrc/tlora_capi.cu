@@ -115,6 +115,21 @@ CUtensorMap tmap_mn(const void* p, int64_t MN, int64_t K) {
   return make_tmap(p, MN, K, MN, 64, tlora::kBK);
 }
 
+// ------------------------------------------------------------------ SM budgets
+// Persistent grids are sized to min(tiles, budget). Splitting the SMs between the
+// tensor-bound fused GEMMs and the HBM-bound low-rank launches lets a driver run the two
+// concurrently on two streams (tlora_set_sm_budget). 0 = all SMs.
+std::mutex g_budget_mu;
+std::map<int, std::pair<int, int>> g_budget;  // device -> (gemm SMs, low-rank SMs)
+
+int sm_budget(int device, int all, bool gemm) {
+  std::lock_guard<std::mutex> lk(g_budget_mu);
+  auto it = g_budget.find(device);
+  if (it == g_budget.end()) return all;
+  const int b = gemm ? it->second.first : it->second.second;
+  return b > 0 ? std::min(b, all) : all;
+}
+
 // ------------------------------------------------------------------ launch profiling
 // Optional CUDA-event brackets around every GEMM launch, recorded on the launch stream
 // (tlora_profile_begin/_end). Used by bench.py for the live roofline of each launch kind.
@@ -177,7 +192,9 @@ void launch_gemm(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap
   auto kern = tlora::lora_gemm_kernel<BN, AMN, BMN, EPI, ST>;
   constexpr int smem = tlora::GemmSmem<BN, ST>::kDynamic;
   TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const int grid = std::min(args.num_tiles, sm_count);
+  int dev = 0;
+  TL_CUDA(cudaGetDevice(&dev));
+  const int grid = std::min(args.num_tiles, sm_budget(dev, sm_count, false));
   ProfScope ps(launch_kind, flops, s);
   launch_pdl(kern, grid, smem, s, a0, b0, a1, b1, args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -191,7 +208,9 @@ void launch_gemm2(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
   auto kern = tlora::lora_gemm2_kernel<EPI, ST>;
   constexpr int smem = tlora::Gemm2Smem<ST>::kDynamic;
   TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const int grid = std::min(2 * args.num_tiles, sm_count / 2 * 2);
+  int dev = 0;
+  TL_CUDA(cudaGetDevice(&dev));
+  const int grid = std::min(2 * args.num_tiles, sm_budget(dev, sm_count, true) / 2 * 2);
   ProfScope ps(launch_kind, flops, s);
   launch_pdl(kern, grid, smem, s, a0, b0, a1, b1, args);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -386,6 +405,9 @@ int device_sm_count(int dev) {
           "device " + std::to_string(dev) + " is sm_" + std::to_string(prop.major) +
               std::to_string(prop.minor) + "; the fused LoRA kernels are built for sm_100a only");
   n = prop.multiProcessorCount;
+  // TLORA_SM_RESERVE=r leaves r SMs free of the persistent grids (for concurrent NCCL
+  // kernels on a comm stream); even so CTA pairs stay whole.
+  if (const char* e = std::getenv("TLORA_SM_RESERVE")) n = std::max(2, n - std::atoi(e)) / 2 * 2;
   return n;
 }
 
@@ -1064,7 +1086,7 @@ void run_grad(tlora_layer* layer, const tlora_plan* plan, int which, const void*
     auto kern = tlora::lora_grad_kernel<TLORA_GRAD_STAGES>;
     constexpr int smem = tlora::GradSmem<TLORA_GRAD_STAGES>::kDynamic;
     TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int grid = std::min(a.num_tiles, layer->sm_count);
+    const int grid = std::min(a.num_tiles, sm_budget(layer->device, layer->sm_count, false));
     ProfScope ps(launch, 2.0 * (double)plan->P.tok_rank * N, s);
     if (a.num_tiles > 0) {
       launch_pdl(kern, grid, smem, s, ma, mb, a);
@@ -1192,6 +1214,15 @@ int tlora_backward_grad_a(tlora_layer* layer, const tlora_plan* plan, const void
 }
 
 long long tlora_launch_count(void) { return g_launches.load(); }
+
+int tlora_set_sm_budget(int device, int32_t gemm_sms, int32_t lowrank_sms) {
+  return guarded([&] {
+    require(gemm_sms >= 0 && lowrank_sms >= 0, TLORA_ERR_ARG, "negative SM budget");
+    std::lock_guard<std::mutex> lk(g_budget_mu);
+    if (gemm_sms == 0 && lowrank_sms == 0) g_budget.erase(device);
+    else g_budget[device] = {gemm_sms, lowrank_sms};
+  });
+}
 
 int tlora_profile_begin(void) {
   return guarded([&] {

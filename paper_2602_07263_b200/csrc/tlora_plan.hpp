@@ -18,6 +18,7 @@
 #pragma once
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -75,6 +76,16 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 constexpr int64_t kPlanL2Budget = 48ll << 20;  // bytes of operand panel kept hot in L2
 
+// Experiment hook: TLORA_L2_BUDGET_MB overrides the panel budget (the plan oracle and the
+// tests use the default; only set it to measure raster variants).
+inline int64_t l2_budget() {
+  static const int64_t b = [] {
+    const char* e = std::getenv("TLORA_L2_BUDGET_MB");
+    return e ? std::max<int64_t>(1, std::atoll(e)) << 20 : kPlanL2Budget;
+  }();
+  return b;
+}
+
 // L2-aware raster of an (n_mt x n_nt) output-tile grid for a GEMM with reduction depth K
 // (bf16 operands). A persistent grid runs ~148 consecutive tiles at once; ordering tiles
 // in panels (a group of M-tiles swept across all N-tiles, or a group of N-tiles swept
@@ -84,8 +95,8 @@ constexpr int64_t kPlanL2Budget = 48ll << 20;  // bytes of operand panel kept ho
 inline std::vector<std::pair<int32_t, int32_t>> raster_order(int64_t n_mt, int64_t n_nt,
                                                              int64_t K, int64_t bm, int64_t bn) {
   const int64_t a_panel = bm * K * 2, b_panel = bn * K * 2;  // bytes per M / N tile panel
-  const int64_t gm = std::max<int64_t>(1, std::min(n_mt, kPlanL2Budget / a_panel));
-  const int64_t gn = std::max<int64_t>(1, std::min(n_nt, kPlanL2Budget / b_panel));
+  const int64_t gm = std::max<int64_t>(1, std::min(n_mt, l2_budget() / a_panel));
+  const int64_t gn = std::max<int64_t>(1, std::min(n_nt, l2_budget() / b_panel));
   const int64_t bytes_m = n_mt * a_panel + ceil_div(n_mt, gm) * n_nt * b_panel;
   const int64_t bytes_n = n_nt * b_panel + ceil_div(n_nt, gn) * n_mt * a_panel;
   std::vector<std::pair<int32_t, int32_t>> order;

@@ -79,6 +79,70 @@ class LayerSetStep:
             if on_layer_done is not None:
                 on_layer_done((L, name), lay)
 
+    # ---- overlapped schedule: low-rank launches on a side stream, fused GEMMs on the main
+    def enable_overlap(self, lowrank_sms: int = 16):
+        """Run the HBM-bound low-rank launches (shrink, dH, dA, dB) on a side stream with a
+        small persistent grid, concurrently with the tensor-bound fused GEMMs (fwd, dX) on
+        the main stream, which keep the remaining SMs (tlora_set_sm_budget)."""
+        from . import capi
+        total = torch.cuda.get_device_properties(self.dev).multi_processor_count
+        capi.call("tlora_set_sm_budget", self.device, total - lowrank_sms, lowrank_sms)
+        self.side = torch.cuda.Stream(self.dev)
+        self.dH = {name: torch.zeros(self.T, lay.R, dtype=torch.bfloat16, device=self.dev)
+                   for (L, name), lay in self.layers.items() if L == 0}
+        self.overlap = True
+
+    def _ev(self, stream):
+        e = torch.cuda.Event()
+        e.record(stream)
+        return e
+
+    def forward_overlapped(self, main):
+        side = self.side
+        side.wait_event(self._ev(main))  # adapters of the previous optimizer step are final
+        ready = []
+        for L, name in self.keys:  # all shrinks run ahead on the side stream
+            self.layers[(L, name)].shrink(self.plans[name], self.x_of(name), self.H[(L, name)],
+                                          stream=side)
+            ready.append(self._ev(side))
+        for (L, name), ev in zip(self.keys, ready):
+            main.wait_event(ev)
+            self.layers[(L, name)].fused_gemm(self.plans[name], self.x_of(name),
+                                              self.H[(L, name)], self.Y[name], stream=main)
+
+    def backward_overlapped(self, main, on_layer_done=None):
+        """dH of the next projection is computed ahead on the side stream, so the main
+        stream's dX never waits behind the previous projection's dA / dB."""
+        side = self.side
+        side.wait_event(self._ev(main))
+        keys = list(reversed(self.keys))
+        last_dx = {}  # projection name -> event of the last dX that read dH[name]
+
+        def launch_dh(i):
+            L, name = keys[i]
+            if name in last_dx:  # dH[name] is shared by every layer of this projection
+                side.wait_event(last_dx[name])  # (its grad_a reader is earlier on `side`)
+            self.layers[keys[i]].dh(self.plans[name], self.dY[name], self.dH[name], stream=side)
+            return self._ev(side)
+
+        ev_dh = launch_dh(0)
+        for i, (L, name) in enumerate(keys):
+            lay, pl = self.layers[(L, name)], self.plans[name]
+            main.wait_event(ev_dh)
+            lay.dx(pl, self.dY[name], self.dH[name], self.dX[name], stream=main)
+            last_dx[name] = self._ev(main)
+            nxt = i + 1 < len(keys)
+            ahead = nxt and keys[i + 1][1] != name
+            ev_dh = launch_dh(i + 1) if ahead else None
+            lay.grad_b(pl, self.H[(L, name)], self.dY[name], stream=side)
+            lay.grad_a(pl, self.x_of(name), self.dH[name], stream=side)
+            ev_grads = self._ev(side)
+            if nxt and not ahead:
+                ev_dh = launch_dh(i + 1)
+            if on_layer_done is not None:
+                on_layer_done((L, name), lay, ev_grads)
+        main.wait_stream(side)
+
     def enable_optimizer(self, base_lr: float = 1e-4, weight_decay: float = 0.01):
         """Per-job AdamW hyperparameters (each job is an independent fine-tuning run)."""
         lrs = [base_lr * (1.0 + 0.25 * (s % 4)) for s in range(len(self.wl.jobs))]
