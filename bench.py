@@ -129,7 +129,7 @@ def run_ours(args, rank, world, local_rank):
     wl = config(args.config)
     step = LayerSetStep(wl, device=local_rank, seed=wl.seed + rank, shuffle=args.shuffle)
     step.enable_optimizer()
-    if args.overlap > 0:
+    if args.overlap != 0:
         step.enable_overlap(args.overlap)
     stream = torch.cuda.current_stream()
 
@@ -158,14 +158,14 @@ def run_ours(args, rank, world, local_rank):
         flat_grads = [g for lay in step.layers.values() for g in lay.packed_grads()]
 
     def fwd():
-        if args.overlap > 0:
+        if args.overlap != 0:
             step.forward_overlapped(stream)
         else:
             step.forward(stream)
 
     def bwd():
         cb = allreduce_grads if world > 1 else None
-        if args.overlap > 0:
+        if args.overlap != 0:
             step.backward_overlapped(stream, on_layer_done=cb)
         else:
             step.backward(stream, on_layer_done=cb)
@@ -478,8 +478,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-tokens-per-job", type=int, default=8)
     ap.add_argument("--overlap", type=int, default=0,
-                    help="SMs for the low-rank launches on a side stream, concurrent with the "
-                         "fused GEMMs (0 = serial schedule)")
+                    help="low-rank launches on a side stream concurrent with the fused GEMMs: "
+                         "N>0 caps them to N SMs (GEMMs get the rest), -1 = uncapped, "
+                         "0 = serial schedule")
     ap.add_argument("--tp", action="store_true",
                     help="tensor-parallel layer set over the torchrun group (default config C4)")
     ap.add_argument("--nano", type=int, default=4, help="initial nano-batch count (TP mode)")

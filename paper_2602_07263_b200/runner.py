@@ -80,13 +80,16 @@ class LayerSetStep:
                 on_layer_done((L, name), lay)
 
     # ---- overlapped schedule: low-rank launches on a side stream, fused GEMMs on the main
-    def enable_overlap(self, lowrank_sms: int = 16):
+    def enable_overlap(self, lowrank_sms: int = -1):
         """Run the HBM-bound low-rank launches (shrink, dH, dA, dB) on a side stream with a
         small persistent grid, concurrently with the tensor-bound fused GEMMs (fwd, dX) on
         the main stream, which keep the remaining SMs (tlora_set_sm_budget)."""
         from . import capi
         total = torch.cuda.get_device_properties(self.dev).multi_processor_count
-        capi.call("tlora_set_sm_budget", self.device, total - lowrank_sms, lowrank_sms)
+        if lowrank_sms > 0:
+            capi.call("tlora_set_sm_budget", self.device, total - lowrank_sms, lowrank_sms)
+        # lowrank_sms < 0: no caps — both streams use full persistent grids and the
+        # independent launches fill the SMs freed by each other's ramp-down / tail
         self.side = torch.cuda.Stream(self.dev)
         self.dH = {name: torch.zeros(self.T, lay.R, dtype=torch.bfloat16, device=self.dev)
                    for (L, name), lay in self.layers.items() if L == 0}
