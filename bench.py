@@ -170,8 +170,20 @@ def run_ours(args, rank, world, local_rank):
         else:
             step.backward(stream, on_layer_done=cb)
 
+    graph = None
+    if not args.no_graph and world == 1 and args.overlap == 0:
+        try:
+            graph = step.capture(warmup=1)
+        except Exception as e:  # same kernels, launched eagerly instead
+            print(f"[bench] CUDA-graph capture failed, running eagerly: {e}", file=sys.stderr)
+            torch.cuda.synchronize()
+            graph = None
+
     def one_step():
         # training step: fwd + bwd (+ DP all-reduce) + fused multi-job AdamW of all adapters
+        if graph is not None:
+            graph.replay()
+            return
         fwd()
         bwd()
         if flat_grads is not None:
@@ -211,6 +223,8 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     n_launch = lib.tlora_launch_count() - n0
+    if graph is not None:  # replays bypass the host-side counter: count the captured kernels
+        n_launch = step.graph_launches * args.steps
     cnt = (C.c_int32 * 6)()
     ms6 = (C.c_double * 6)()
     fl6 = (C.c_double * 6)()
@@ -338,7 +352,8 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": f"{wl.name}: {wl.notes}", "tokens_per_gpu": wl.tokens,
                    "jobs": [[j.job_id, j.rank, j.tokens] for j in wl.jobs],
                    "projections": wl.projections, "token_order": "shuffled" if args.shuffle else "job-contiguous",
-                   "parallelism": f"dp{world}", "lowrank_side_stream_sms": args.overlap, "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)",
+                   "parallelism": f"dp{world}", "lowrank_side_stream_sms": args.overlap,
+                   "cuda_graph": graph is not None, "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)",
                    "algorithmic_tflop_per_step": round(flops_step / 1e12, 3),
                    "achieved_tflops_step": round(flops_step / (ms_per_step / 1e3) / 1e12, 1)},
         "e2e": {"value": round(tokens / (e2e_ms / 1e3), 1), "unit": "tokens/s",
@@ -481,6 +496,9 @@ def main():
                     help="low-rank launches on a side stream concurrent with the fused GEMMs: "
                          "N>0 caps them to N SMs (GEMMs get the rest), -1 = uncapped, "
                          "0 = serial schedule")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch every kernel eagerly instead of replaying the captured "
+                         "CUDA graph of the training step (graphs are used at N=1)")
     ap.add_argument("--tp", action="store_true",
                     help="tensor-parallel layer set over the torchrun group (default config C4)")
     ap.add_argument("--nano", type=int, default=4, help="initial nano-batch count (TP mode)")

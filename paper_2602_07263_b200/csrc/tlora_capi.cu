@@ -280,8 +280,9 @@ __global__ void adamw_packed_kernel(const float* __restrict__ G, float* __restri
                                     __nv_bfloat16* __restrict__ P16,
                                     __nv_bfloat16* __restrict__ P16t,
                                     const int32_t* __restrict__ row_slot,
-                                    const float4* __restrict__ hp, float b1, float b2, float eps,
-                                    float grad_scale, int64_t R, int64_t N) {
+                                    const float2* __restrict__ hp,
+                                    const int32_t* __restrict__ steps, float b1, float b2,
+                                    float eps, float grad_scale, int64_t R, int64_t N) {
   __shared__ float tile[32][33];
   const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -291,12 +292,14 @@ __global__ void adamw_packed_kernel(const float* __restrict__ G, float* __restri
       const int s = row_slot[r];
       if (s >= 0) {
         const int64_t idx = r * N + c;
-        const float4 h = hp[s];  // lr, wd, 1/(1-b1^t), 1/(1-b2^t)
+        const float2 h = hp[s];  // lr, wd
+        const float t = (float)(steps[s] + 1);
+        const float c1 = 1.f / (1.f - powf(b1, t)), c2 = 1.f / (1.f - powf(b2, t));
         const float g = G[idx] * grad_scale;
         float p = P[idx];
         const float m = b1 * Mo[idx] + (1.f - b1) * g;
         const float v = b2 * Vo[idx] + (1.f - b2) * g * g;
-        p -= h.x * (m * h.z / (sqrtf(v * h.w) + eps) + h.y * p);
+        p -= h.x * (m * c1 / (sqrtf(v * c2) + eps) + h.y * p);
         P[idx] = p;
         Mo[idx] = m;
         Vo[idx] = v;
@@ -311,6 +314,11 @@ __global__ void adamw_packed_kernel(const float* __restrict__ G, float* __restri
     const int64_t c = c0 + i, r = r0 + threadIdx.x;
     if (r < R && c < N) P16t[c * R + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
   }
+}
+
+__global__ void bump_steps_kernel(int32_t* steps, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) steps[i] += 1;
 }
 
 // Elementwise dtype conversion (device), used by the host-buffer copy entry points.
@@ -435,32 +443,38 @@ struct tlora_layer {
   // fused multi-job AdamW state (fp32 masters of the packed adapters + moments)
   DevBuf<float> ATm, Bm, mA, vA, mB, vB;
   DevBuf<int32_t> row_slot;  // packed rank row -> slot, -1 in padding gaps
-  DevBuf<float4> hparams;    // per slot {lr, weight_decay, 1/(1-b1^t), 1/(1-b2^t)}
+  DevBuf<float2> hparams;    // per slot {lr, weight_decay}
+  DevBuf<int32_t> steps_dev; // per slot AdamW step count (device-side: graph-capturable)
   std::vector<float> lr, wd;
-  std::vector<long long> steps;
   float beta1 = 0.9f, beta2 = 0.999f, eps = 1e-8f;
   bool opt_set = false;
 };
 
 namespace {
-// Per-(device, stream) scratch for the split-K partial planes and tlora_backward's dH.
-// Launches on one stream are ordered, so one buffer per stream is race-free; growing
-// reallocates (cudaFree synchronises) — it happens only while shapes are first seen.
+// Per-device scratch for the split-K partial planes and tlora_backward's dH. Gradient
+// launches (and tlora_backward) on one device are therefore serialised on one stream at a
+// time (the drivers in this repo do so). Growing reallocates (cudaFree synchronises); it
+// only happens while shapes are first seen, so a warmed-up step can be captured in a
+// CUDA graph (capture may run on a different stream than the warm-up).
 struct Workspace {
   DevBuf<char> partial, dh;
 };
 std::mutex g_ws_mu;
-std::map<std::pair<int, cudaStream_t>, std::unique_ptr<Workspace>> g_ws;
+std::map<int, std::unique_ptr<Workspace>> g_ws;
 
 template <class T>
 T* ws_get(int device, cudaStream_t s, bool dh, size_t count) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  auto& w = g_ws[{device, s}];
+  auto& w = g_ws[device];
   if (!w) w = std::make_unique<Workspace>();
   DevBuf<char>& b = dh ? w->dh : w->partial;
   const size_t bytes = count * sizeof(T);
   if (b.n < bytes) {
-    TL_CUDA(cudaStreamSynchronize(s));
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TL_CUDA(cudaStreamIsCapturing(s, &cs));
+    require(cs == cudaStreamCaptureStatusNone, TLORA_ERR_ARG,
+            "workspace must grow during CUDA-graph capture: run the step once before capturing");
+    TL_CUDA(cudaDeviceSynchronize());
     b.alloc(bytes);
     if (dh) TL_CUDA(cudaMemset(b.p, 0, bytes));
   }
@@ -779,13 +793,16 @@ int tlora_layer_set_optimizer(tlora_layer* layer, const float* lr, const float* 
       layer->mB.alloc(R * k);
       layer->vB.alloc(R * k);
       layer->hparams.alloc(S);
-      layer->steps.assign(S, 0);
+      layer->steps_dev.alloc(S);
     }
     TL_CUDA(cudaMemset(layer->mA.p, 0, R * d * 4));
     TL_CUDA(cudaMemset(layer->vA.p, 0, R * d * 4));
     TL_CUDA(cudaMemset(layer->mB.p, 0, R * k * 4));
     TL_CUDA(cudaMemset(layer->vB.p, 0, R * k * 4));
-    layer->steps.assign(S, 0);
+    TL_CUDA(cudaMemset(layer->steps_dev.p, 0, S * 4));
+    std::vector<float2> hp(S);
+    for (int i = 0; i < S; ++i) hp[i] = make_float2(layer->lr[i], layer->wd[i]);
+    TL_CUDA(cudaMemcpy(layer->hparams.p, hp.data(), S * sizeof(float2), cudaMemcpyHostToDevice));
     layer->opt_set = true;
   });
 }
@@ -798,28 +815,22 @@ int tlora_layer_optimizer_step(tlora_layer* layer, float grad_scale, void* strea
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int S = (int)layer->L.rank.size();
     const int64_t R = layer->L.R, d = layer->L.d, k = layer->L.k;
-    std::vector<float4> hp(S);
-    for (int i = 0; i < S; ++i) {
-      const long long t = ++layer->steps[i];
-      hp[i] = make_float4(layer->lr[i], layer->wd[i],
-                          (float)(1.0 / (1.0 - std::pow((double)layer->beta1, (double)t))),
-                          (float)(1.0 / (1.0 - std::pow((double)layer->beta2, (double)t))));
-    }
-    TL_CUDA(cudaMemcpyAsync(layer->hparams.p, hp.data(), S * sizeof(float4), cudaMemcpyHostToDevice, s));
-    const dim3 block(32, 8);
+    const dim3 block(32, 8);  // enqueue-only, no host data: capturable in a CUDA graph
     adamw_packed_kernel<<<dim3((unsigned)tlora::ceil_div(d, 32), (unsigned)tlora::ceil_div(R, 32)),
                           block, 0, s>>>(layer->dAT.p, layer->ATm.p, layer->mA.p, layer->vA.p,
                                          layer->AT.p, layer->Acat.p, layer->row_slot.p,
-                                         layer->hparams.p, layer->beta1, layer->beta2, layer->eps,
-                                         grad_scale, R, d);
+                                         layer->hparams.p, layer->steps_dev.p, layer->beta1,
+                                         layer->beta2, layer->eps, grad_scale, R, d);
     TL_CUDA(cudaGetLastError());
     adamw_packed_kernel<<<dim3((unsigned)tlora::ceil_div(k, 32), (unsigned)tlora::ceil_div(R, 32)),
                           block, 0, s>>>(layer->dB.p, layer->Bm.p, layer->mB.p, layer->vB.p,
                                          layer->Bcat.p, layer->BcatT.p, layer->row_slot.p,
-                                         layer->hparams.p, layer->beta1, layer->beta2, layer->eps,
-                                         grad_scale, R, k);
+                                         layer->hparams.p, layer->steps_dev.p, layer->beta1,
+                                         layer->beta2, layer->eps, grad_scale, R, k);
     TL_CUDA(cudaGetLastError());
-    g_launches.fetch_add(2, std::memory_order_relaxed);
+    bump_steps_kernel<<<(S + 127) / 128, 128, 0, s>>>(layer->steps_dev.p, S);
+    TL_CUDA(cudaGetLastError());
+    g_launches.fetch_add(3, std::memory_order_relaxed);
   });
 }
 

@@ -157,6 +157,22 @@ class LayerSetStep:
         for lay in self.layers.values():
             lay.optimizer_step(grad_scale, stream=stream)
 
+    def capture(self, warmup: int = 1):
+        """Capture one training step (fwd + bwd + AdamW) into a CUDA graph. All launches are
+        enqueue-only with device-side state (tile tables, optimizer step counters), so the
+        graph replays a fresh step each time; workspaces are sized by the eager warm-up."""
+        for _ in range(warmup):
+            self.step()
+        torch.cuda.synchronize(self.dev)
+        from . import capi
+        g = torch.cuda.CUDAGraph()
+        n0 = capi.lib().tlora_launch_count()
+        with torch.cuda.graph(g):
+            self.step()
+        self.graph_launches = capi.lib().tlora_launch_count() - n0  # kernels per replay
+        self.graph = g
+        return g
+
     def step(self, stream=None, on_layer_done=None):
         """One training step: forward, backward, fused AdamW update of every adapter."""
         self.forward(stream)
