@@ -382,7 +382,8 @@ def run_tp(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     wl = config(args.config)
-    st = TPLayerSetStep(wl, rank, world, local_rank, nano=args.nano)
+    fused = [p for p in args.fused_rs.split(",") if p]
+    st = TPLayerSetStep(wl, rank, world, local_rank, nano=args.nano, fused_rs=fused)
     st.enable_optimizer()
     stream = torch.cuda.current_stream()
     clocks = ClockSampler(local_rank)
@@ -436,6 +437,9 @@ def run_tp(args, rank, world, local_rank):
         "data": "synthetic (seeded normal activations/grads, random-init W and adapters)",
         "config": {"workload": f"{wl.name}: {wl.notes} (one layer of the stack per step)",
                    "tokens_global": wl.tokens, "parallelism": f"tp{world}",
+                   "row_parallel_reduce_scatter": {p: ("fused GEMM epilogue -> NVLink peer "
+                                                       "slots" if p in fused else "NCCL")
+                                                   for p in ("o", "down")},
                    "nano_batches": st.n, "aimd_trajectory_n_ms": trajectory,
                    "algorithmic_tflop_per_step": round(flops / 1e12, 3),
                    "achieved_tflops_aggregate": round(flops / (ms_per_step / 1e3) / 1e12, 1),
@@ -502,6 +506,10 @@ def main():
     ap.add_argument("--tp", action="store_true",
                     help="tensor-parallel layer set over the torchrun group (default config C4)")
     ap.add_argument("--nano", type=int, default=4, help="initial nano-batch count (TP mode)")
+    ap.add_argument("--fused-rs", default="",
+                    help="TP mode: comma list of row-parallel projections (o,down) whose "
+                         "reduce-scatter is fused into the GEMM epilogue (peer stores over "
+                         "NVLink); the rest use NCCL on the comm stream")
     ap.add_argument("--aimd-steps", type=int, default=8, help="AIMD exploration steps (TP mode)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup

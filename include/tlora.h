@@ -171,6 +171,18 @@ int tlora_forward_shrink(tlora_layer* layer, const tlora_plan* plan, const void*
                          void* stream);
 int tlora_forward_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X, const void* H,
                        void* Y, int y_dtype, void* stream);
+/* Row-parallel tensor-parallel forward with the reduce-scatter fused into the GEMM: each
+ * output row r (token of this plan) is stored, as its tile finishes, into the receive
+ * buffer of the rank that owns it (dest = r / (T / world)) through NVLink peer memory.
+ * recv_ptrs[world]: every rank's receive buffer [world][slot_rows][k] bf16 (peer-mapped,
+ * e.g. symmetric memory); this rank writes slot `rank`, rows dst_row0 + r % (T / world).
+ * After a cross-rank barrier, tlora_reduce_slots sums the slots in fixed order. */
+int tlora_forward_gemm_rs(tlora_layer* layer, const tlora_plan* plan, const void* X, const void* H,
+                          void* const* recv_ptrs, int32_t world, int32_t rank, int64_t slot_rows,
+                          int64_t dst_row0, void* stream);
+/* out[rows x k] = sum_{p < world} recv[p][row0 .. row0 + rows)[k] (fp32 sum, bf16 out). */
+int tlora_reduce_slots(const void* recv, int32_t world, int64_t slot_rows, int64_t row0,
+                       int64_t rows, int64_t k, void* out, void* stream);
 int tlora_backward_dh(tlora_layer* layer, const tlora_plan* plan, const void* dY, void* dH,
                       void* stream);
 /* dX = dY·Wᵀ + dH·Aᵀ + beta·dX (beta = 1 sums the dX of projections sharing an input) */

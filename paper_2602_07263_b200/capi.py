@@ -86,6 +86,11 @@ SIGNATURES = {
                                        C.c_void_p]),
     "tlora_forward_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_int, C.c_void_p]),
+    "tlora_forward_gemm_rs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int64,
+                                        C.c_int64, C.c_void_p]),
+    "tlora_reduce_slots": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_int64,
+                                     C.c_int64, C.c_void_p, C.c_void_p]),
     "tlora_backward_dh": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "tlora_backward_dx": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_float, C.c_void_p]),

@@ -40,6 +40,8 @@ enum EpiMode : int {
   EPI_BF16 = 0,       // out bf16 [M x N], ldo
   EPI_BF16_MASK = 1,  // as EPI_BF16, zero where column is outside the row's job range
   EPI_F32 = 2,        // out fp32, optional beta-accumulate, split partial buffers
+  EPI_PEER = 3,       // bf16 rows stored into the owning rank's receive slot (NVLink peer
+                      // memory): fused reduce-scatter of a row-parallel TP GEMM
 };
 
 struct GemmArgs {
@@ -54,6 +56,11 @@ struct GemmArgs {
   const int32_t* row_slot;
   const int32_t* slot_col_lo;
   const int32_t* slot_col_hi;
+  // EPI_PEER: output row r goes to rank r / rows_per_rank, into its receive buffer
+  // peer[dest] laid out [world][slot_rows][ldo], slot = this rank, row dst_row0 + r % rpr
+  void* peer[8];
+  int32_t peer_rank, peer_world;
+  int64_t rows_per_rank, slot_rows, dst_row0;
 };
 
 template <int BN, int STAGES>
@@ -73,7 +80,23 @@ __device__ __forceinline__ void epi_store32(const GemmArgs& args, int split, int
                                             const uint32_t (&v)[32], int lo, int hi) {
   using namespace ptx;
   if (row >= args.M || col0 >= args.N) return;
-  if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_MASK) {
+  if constexpr (EPI == EPI_PEER) {
+    const int64_t dest = row / args.rows_per_rank, lrow = row % args.rows_per_rank;
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.peer[dest]) +
+                       ((int64_t)args.peer_rank * args.slot_rows + args.dst_row0 + lrow) * args.ldo +
+                       col0;
+    uint4* o4 = reinterpret_cast<uint4*>(o);  // N % 32 == 0 is required for this mode
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 w;
+      w.x = pack_bf16x2(__uint_as_float(v[8 * q + 0]), __uint_as_float(v[8 * q + 1]));
+      w.y = pack_bf16x2(__uint_as_float(v[8 * q + 2]), __uint_as_float(v[8 * q + 3]));
+      w.z = pack_bf16x2(__uint_as_float(v[8 * q + 4]), __uint_as_float(v[8 * q + 5]));
+      w.w = pack_bf16x2(__uint_as_float(v[8 * q + 6]), __uint_as_float(v[8 * q + 7]));
+      o4[q] = w;
+    }
+    return;
+  } else if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_MASK) {
     float f[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {

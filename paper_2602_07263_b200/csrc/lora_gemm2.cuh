@@ -184,6 +184,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
       }
     }
+    if constexpr (EPI == EPI_PEER) __threadfence_system();  // peer stores before completion
   }
 
   tc_fence_before();

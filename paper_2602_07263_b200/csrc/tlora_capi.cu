@@ -321,6 +321,35 @@ __global__ void bump_steps_kernel(int32_t* steps, int n) {
   if (i < n) steps[i] += 1;
 }
 
+// out[r][c] = sum_{p < world} recv[p][row0 + r][c]: fixed-order (deterministic) sum of the
+// slots a fused GEMM + reduce-scatter wrote into this rank's receive buffer.
+__global__ void reduce_slots_kernel(const __nv_bfloat16* __restrict__ recv, int world,
+                                    int64_t slot_rows, int64_t row0, int64_t rows, int64_t k,
+                                    __nv_bfloat16* __restrict__ out) {
+  const int64_t n8 = rows * k / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * 8, r = e / k, c = e % k;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int p = 0; p < world; ++p) {
+      const uint4 v = *reinterpret_cast<const uint4*>(recv + ((int64_t)p * slot_rows + row0 + r) * k + c);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        acc[2 * j] += f.x;
+        acc[2 * j + 1] += f.y;
+      }
+    }
+    uint4 w;
+    w.x = tlora::ptx::pack_bf16x2(acc[0], acc[1]);
+    w.y = tlora::ptx::pack_bf16x2(acc[2], acc[3]);
+    w.z = tlora::ptx::pack_bf16x2(acc[4], acc[5]);
+    w.w = tlora::ptx::pack_bf16x2(acc[6], acc[7]);
+    *reinterpret_cast<uint4*>(out + r * k + c) = w;
+  }
+}
+
 // Elementwise dtype conversion (device), used by the host-buffer copy entry points.
 __global__ void convert_kernel(const void* src, int sdt, void* dst, int ddt, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -1157,6 +1186,64 @@ int tlora_forward_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X
             "Y dtype must be bf16 or f32");
     DeviceGuard g(layer->device);
     run_fwd_gemm(layer, plan, X, H, Y, y_dtype, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int tlora_forward_gemm_rs(tlora_layer* layer, const tlora_plan* plan, const void* X, const void* H,
+                          void* const* recv_ptrs, int32_t world, int32_t rank, int64_t slot_rows,
+                          int64_t dst_row0, void* stream) {
+  return guarded([&] {
+    check_bound(layer, plan);
+    check_align(X, "X");
+    check_align(H, "H");
+    require(recv_ptrs != nullptr && world >= 1 && world <= 8 && rank >= 0 && rank < world,
+            TLORA_ERR_ARG, "need 1..8 receive buffers and a rank in [0, world)");
+    const auto& L = layer->L;
+    const int64_t T = plan->P.T, d = L.d, k = L.k, R = L.R;
+    require(T % world == 0, TLORA_ERR_SHAPE, "tokens must divide evenly over the ranks");
+    require(k % 32 == 0, TLORA_ERR_SHAPE, "fused reduce-scatter needs k % 32 == 0");
+    require(dst_row0 >= 0 && dst_row0 + T / world <= slot_rows, TLORA_ERR_ARG,
+            "receive slot too small for this plan");
+    for (int p = 0; p < world; ++p) check_align(recv_ptrs[p], "receive buffer");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    GemmArgs a{};
+    a.tiles = plan->tiles[TLORA_L_FWD].p;
+    a.num_tiles = (int)plan->P.tiles[TLORA_L_FWD].size();
+    a.M = (int)T;
+    a.N = (int)k;
+    a.ldo = k;
+    for (int p = 0; p < world; ++p) a.peer[p] = recv_ptrs[p];
+    a.peer_rank = rank;
+    a.peer_world = world;
+    a.rows_per_rank = T / world;
+    a.slot_rows = slot_rows;
+    a.dst_row0 = dst_row0;
+    const CUtensorMap ma0 = tmap_k(X, d, T, 128);
+    const CUtensorMap mb0 = tmap_k(layer->Wt16.p, d, k, 128);
+    const CUtensorMap ma1 = tmap_k(H, R, T, 128);
+    const CUtensorMap mb1 = tmap_k(layer->BcatT.p, R, k, 128);
+    launch_gemm2<tlora::EPI_PEER, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD,
+                                     2.0 * T * d * k + 2.0 * (double)plan->P.tok_rank * k);
+  });
+}
+
+int tlora_reduce_slots(const void* recv, int32_t world, int64_t slot_rows, int64_t row0,
+                       int64_t rows, int64_t k, void* out, void* stream) {
+  return guarded([&] {
+    check_align(recv, "recv");
+    check_align(out, "out");
+    require(world >= 1 && rows >= 0 && k % 8 == 0 && row0 + rows <= slot_rows, TLORA_ERR_ARG,
+            "bad slot geometry");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t n8 = rows * k / 8;
+    if (n8 == 0) return;
+    const int blocks = (int)std::min<int64_t>(tlora::ceil_div(n8, 256), 4 * 148);
+    reduce_slots_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(recv), world,
+                                               slot_rows, row0, rows, k,
+                                               reinterpret_cast<__nv_bfloat16*>(out));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    TL_CUDA(cudaGetLastError());
   });
 }
 

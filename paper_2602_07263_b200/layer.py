@@ -211,6 +211,13 @@ class FusedLoRALayer:
         call("tlora_forward_gemm", self._h, plan._h, _ptr(X), _ptr(H), _ptr(Y), _DT[Y.dtype],
              _stream_ptr(stream))
 
+    def fused_gemm_rs(self, plan: Plan, X, H, recv_ptrs, rank, slot_rows, dst_row0, stream=None):
+        """Row-parallel TP forward with the reduce-scatter fused into the epilogue (peer
+        stores into every owner's receive slot); see tlora_forward_gemm_rs."""
+        ptrs = (C.c_void_p * len(recv_ptrs))(*[int(p) for p in recv_ptrs])
+        call("tlora_forward_gemm_rs", self._h, plan._h, _ptr(X), _ptr(H), ptrs, len(recv_ptrs),
+             int(rank), int(slot_rows), int(dst_row0), _stream_ptr(stream))
+
     def dh(self, plan: Plan, dY, dH, stream=None):
         call("tlora_backward_dh", self._h, plan._h, _ptr(dY), _ptr(dH), _stream_ptr(stream))
 
@@ -238,6 +245,11 @@ class FusedLoRALayer:
             self.close()
         except Exception:
             pass
+
+
+def reduce_slots(recv, world, slot_rows, row0, rows, k, out, stream=None):
+    call("tlora_reduce_slots", _ptr(recv), int(world), int(slot_rows), int(row0), int(rows),
+         int(k), _ptr(out), _stream_ptr(stream))
 
 
 def plan_tiles_host(d: int, k: int, ranks, token_slot, launch: int) -> np.ndarray:

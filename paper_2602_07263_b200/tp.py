@@ -33,7 +33,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .layer import AimdState, FusedLoRALayer, aimd_step, partition
+from .layer import AimdState, FusedLoRALayer, aimd_step, partition, reduce_slots
 from .workload import INPUT_GROUP, Workload
 
 COLUMN = ("q", "k", "v", "gate", "up")
@@ -88,7 +88,7 @@ def shard_rows(full: torch.Tensor, rank: int, world: int) -> torch.Tensor:
 # ------------------------------------------------------------------ the driver
 class TPLayerSetStep:
     def __init__(self, wl: Workload, rank: int, world: int, device: int, group=None,
-                 nano: int = 4, seed: int | None = None):
+                 nano: int = 4, seed: int | None = None, fused_rs=False):
         self.wl, self.rank, self.world, self.group = wl, rank, world, group
         self.dev = torch.device("cuda", device)
         self.T = wl.tokens
@@ -162,6 +162,24 @@ class TPLayerSetStep:
             self.dX_loc[name] = torch.empty(T, d // P, dtype=bf, device=self.dev)
         self._plans = {}
         self.aimd = AimdState(n=nano)
+        # fused GEMM + reduce-scatter for the row-parallel projections: every rank's receive
+        # buffer [world][T/P][k] in symmetric (peer-mapped) memory
+        # fused_rs: False, True (all row-parallel projections) or a collection of names
+        if fused_rs is True:
+            fused_rs = ROW
+        self.fused_set = set(fused_rs or ())
+        self.fused_rs = bool(self.fused_set)
+        self.recv, self.recv_hdl = {}, {}
+        if self.fused_rs:
+            import torch.distributed._symmetric_memory as symm_mem
+            grp = group if group is not None else dist.group.WORLD
+            for name in ROW:
+                if name not in dims or name not in self.fused_set:
+                    continue
+                k = dims[name][1]
+                buf = symm_mem.empty(P, T // P, k, dtype=bf, device=self.dev)
+                self.recv[name] = buf
+                self.recv_hdl[name] = symm_mem.rendezvous(buf, grp)
         torch.cuda.synchronize(self.dev)
 
     # -------------------------------------------------------------- plans per N
@@ -198,6 +216,12 @@ class TPLayerSetStep:
         C, M = self.compute, self.comm
         cols = [p for p in COLUMN if p in self.layers]
         rows = [p for p in ROW if p in self.layers]
+        if self.fused_rs:  # every rank has consumed the previous step's receive slots
+            C.wait_stream(M)
+            with torch.cuda.stream(C):
+                for p in rows:
+                    if p in self.fused_set:
+                        self.recv_hdl[p].barrier(channel=0, timeout_ms=60000)
 
         def shrink(i):
             b = nb[i]
@@ -232,14 +256,28 @@ class TPLayerSetStep:
             for p in rows:
                 lay, pl = self.layers[p], plans[i][p][0]
                 lay.shrink(pl, self._rows(self.X_loc[p], b), self._rows(self.H_row[p], b), stream=C)
-                lay.fused_gemm(pl, self._rows(self.X_loc[p], b), self._rows(self.H_row[p], b),
-                               self._rows(self.Y_part[p], b), stream=C)
+                if p in self.fused_set:
+                    # GEMM tiles go straight into the owners' receive slots over NVLink
+                    hdl = self.recv_hdl[p]
+                    lay.fused_gemm_rs(pl, self._rows(self.X_loc[p], b), self._rows(self.H_row[p], b),
+                                      hdl.buffer_ptrs, self.rank, self.T // self.world,
+                                      b.t0 // self.world, stream=C)
+                else:
+                    lay.fused_gemm(pl, self._rows(self.X_loc[p], b), self._rows(self.H_row[p], b),
+                                   self._rows(self.Y_part[p], b), stream=C)
             ev_y = torch.cuda.Event()
             ev_y.record(C)
             M.wait_event(ev_y)
-            with torch.cuda.stream(M):
+            with torch.cuda.stream(M):  # off the compute stream: overlaps nano n+1's GEMMs
                 for p in rows:
-                    self._rs(self._srows(self.Y_shard[p], b), self._rows(self.Y_part[p], b))
+                    if p in self.fused_set:  # data already moved by the GEMM: barrier + sum
+                        self.recv_hdl[p].barrier(channel=0, timeout_ms=60000)
+                        reduce_slots(self.recv[p], self.world, self.T // self.world,
+                                     b.t0 // self.world, b.tokens // self.world,
+                                     self.recv[p].shape[2], self._srows(self.Y_shard[p], b),
+                                     stream=M)
+                    else:
+                        self._rs(self._srows(self.Y_shard[p], b), self._rows(self.Y_part[p], b))
             ev_g = ev_next
         C.wait_stream(M)
 

@@ -35,7 +35,8 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = config(os.environ.get("TP_CONFIG", "C2"))
     nano = int(os.environ.get("TP_NANO", "4"))
-    st = TPLayerSetStep(wl, rank, world, local, nano=nano)
+    fused = os.environ.get("TP_FUSED_RS", "0") == "1"
+    st = TPLayerSetStep(wl, rank, world, local, nano=nano, fused_rs=fused)
     st.step()
     torch.cuda.synchronize()
     nb, _ = st.plans(nano)
@@ -111,8 +112,8 @@ def main():
                 print(f"rank{rank} {r[0]:5s} {r[1]:4s} maxrel={r[2]:.2e} frob={r[3]:.2e} "
                       f"{'ok' if r[4] else 'FAIL'}", flush=True)
     if rank == 0:
-        print("TP_CHECK", "PASS" if ok.item() == 1 else "FAIL", f"world={world} nano={nano}",
-              flush=True)
+        print("TP_CHECK", "PASS" if ok.item() == 1 else "FAIL",
+              f"world={world} nano={nano} fused_rs={fused}", flush=True)
     dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if ok.item() == 1 else 1)
