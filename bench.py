@@ -171,9 +171,11 @@ def run_ours(args, rank, world, local_rank):
             step.backward(stream, on_layer_done=cb)
 
     graph = None
+    used_graph = False
     if not args.no_graph and world == 1 and args.overlap == 0:
         try:
-            graph = step.capture(warmup=1)
+            graph = step.capture(warmup=1, profile=True)
+            used_graph = True
         except Exception as e:  # same kernels, launched eagerly instead
             print(f"[bench] CUDA-graph capture failed, running eagerly: {e}", file=sys.stderr)
             torch.cuda.synchronize()
@@ -210,7 +212,8 @@ def run_ours(args, rank, world, local_rank):
 
     lib = capi.lib()
     n0 = lib.tlora_launch_count()
-    capi.call("tlora_profile_begin")
+    if graph is None:  # (graph mode: profiling was armed at capture time)
+        capi.call("tlora_profile_begin")
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -229,6 +232,14 @@ def run_ours(args, rank, world, local_rank):
     ms6 = (C.c_double * 6)()
     fl6 = (C.c_double * 6)()
     capi.call("tlora_profile_end", cnt, ms6, fl6)
+    if graph is not None:
+        # the captured brackets hold the LAST replayed step of the timed region; scale to K
+        for i in range(6):
+            cnt[i] *= args.steps
+            ms6[i] *= args.steps
+            fl6[i] *= args.steps
+        graph = None  # its event nodes reference events released by profile_end
+        step.graph = None
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     if world > 1:
@@ -327,6 +338,9 @@ def run_ours(args, rank, world, local_rank):
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak else None,
                 "frac_of_burst": round(achieved / float(peaks["bf16_tflops"]), 4),
+                "timing": ("CUDA-event brackets captured in the step's CUDA graph; per-launch "
+                           "durations of the last replayed step x steps") if used_graph else
+                          "CUDA-event brackets around every launch of the timed region",
                 "traffic": traffic, "kernel": "lora_gemm2_kernel (2-CTA fused base+LoRA GEMM: fwd + dX)",
                 "peak_source": peaks["source"] + " sustained bf16", "per_launch": per_launch}
 
@@ -353,7 +367,7 @@ def run_ours(args, rank, world, local_rank):
                    "jobs": [[j.job_id, j.rank, j.tokens] for j in wl.jobs],
                    "projections": wl.projections, "token_order": "shuffled" if args.shuffle else "job-contiguous",
                    "parallelism": f"dp{world}", "lowrank_side_stream_sms": args.overlap,
-                   "cuda_graph": graph is not None, "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)",
+                   "cuda_graph": used_graph, "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)",
                    "algorithmic_tflop_per_step": round(flops_step / 1e12, 3),
                    "achieved_tflops_step": round(flops_step / (ms_per_step / 1e3) / 1e12, 1)},
         "e2e": {"value": round(tokens / (e2e_ms / 1e3), 1), "unit": "tokens/s",

@@ -147,6 +147,7 @@ struct ProfScope {
   ProfRec rec{};
   cudaStream_t s;
   bool on = false;
+  unsigned flags = 0;
   ProfScope(int launch, double flops, cudaStream_t st) : s(st) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     if (!g_prof_on) return;
@@ -155,11 +156,16 @@ struct ProfScope {
     rec.flops = flops;
     TL_CUDA(cudaEventCreate(&rec.e0));
     TL_CUDA(cudaEventCreate(&rec.e1));
-    TL_CUDA(cudaEventRecord(rec.e0, s));
+    // under CUDA-graph capture a plain record only expresses a dependency; External makes
+    // it an event-record node that every replay re-records
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TL_CUDA(cudaStreamIsCapturing(s, &cs));
+    flags = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+    TL_CUDA(cudaEventRecordWithFlags(rec.e0, s, flags));
   }
   ~ProfScope() {
     if (!on) return;
-    cudaEventRecord(rec.e1, s);
+    cudaEventRecordWithFlags(rec.e1, s, flags);
     std::lock_guard<std::mutex> lk(g_prof_mu);
     g_prof.push_back(rec);
   }
@@ -200,6 +206,9 @@ void launch_gemm(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
+#ifndef TLORA_GEMM2_STAGES
+#define TLORA_GEMM2_STAGES 6
+#endif
 template <int EPI, int ST>
 void launch_gemm2(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1,
                   const CUtensorMap& b1, const GemmArgs& args, int sm_count, cudaStream_t s,
@@ -925,8 +934,6 @@ int tlora_plan_create(tlora_layer* layer, int64_t tokens, const int32_t* token_s
     plan->cnt_da.alloc(plan->P.split_count_da.size());
     TL_CUDA(cudaMemcpy(plan->cnt_da.p, plan->P.split_count_da.data(),
                        plan->P.split_count_da.size() * 4, cudaMemcpyHostToDevice));
-    const int64_t R = layer->L.R;
-
     *out = plan.release();
   });
 }
@@ -1043,9 +1050,9 @@ void run_fwd_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X, con
   const CUtensorMap ma1 = tmap_k(H, R, T, 128);
   const CUtensorMap mb1 = tmap_k(layer->BcatT.p, R, k, 128);
   if (y_dtype == TLORA_BF16)
-    launch_gemm2<tlora::EPI_BF16, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD, flops);
+    launch_gemm2<tlora::EPI_BF16, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD, flops);
   else
-    launch_gemm2<tlora::EPI_F32, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD, flops);
+    launch_gemm2<tlora::EPI_F32, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD, flops);
 }
 
 // dH = dY·Bᵀ (masked; zero outside the windows, as H)
@@ -1087,7 +1094,7 @@ void run_dx(tlora_layer* layer, const tlora_plan* plan, const void* dY, const vo
   const CUtensorMap mb0 = tmap_k(layer->W16.p, k, d, 128);
   const CUtensorMap ma1 = tmap_k(dH, R, T, 128);
   const CUtensorMap mb1 = tmap_k(layer->Acat.p, R, d, 128);
-  launch_gemm2<tlora::EPI_BF16, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_DX,
+  launch_gemm2<tlora::EPI_BF16, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_DX,
                                    2.0 * T * d * k + 2.0 * (double)plan->P.tok_rank * d);
 }
 
@@ -1223,7 +1230,7 @@ int tlora_forward_gemm_rs(tlora_layer* layer, const tlora_plan* plan, const void
     const CUtensorMap mb0 = tmap_k(layer->Wt16.p, d, k, 128);
     const CUtensorMap ma1 = tmap_k(H, R, T, 128);
     const CUtensorMap mb1 = tmap_k(layer->BcatT.p, R, k, 128);
-    launch_gemm2<tlora::EPI_PEER, 6>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD,
+    launch_gemm2<tlora::EPI_PEER, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD,
                                      2.0 * T * d * k + 2.0 * (double)plan->P.tok_rank * k);
   });
 }

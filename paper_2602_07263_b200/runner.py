@@ -157,7 +157,7 @@ class LayerSetStep:
         for lay in self.layers.values():
             lay.optimizer_step(grad_scale, stream=stream)
 
-    def capture(self, warmup: int = 1):
+    def capture(self, warmup: int = 1, profile: bool = False):
         """Capture one training step (fwd + bwd + AdamW) into a CUDA graph. All launches are
         enqueue-only with device-side state (tile tables, optimizer step counters), so the
         graph replays a fresh step each time; workspaces are sized by the eager warm-up."""
@@ -167,6 +167,8 @@ class LayerSetStep:
         from . import capi
         g = torch.cuda.CUDAGraph()
         n0 = capi.lib().tlora_launch_count()
+        if profile:  # per-launch CUDA-event brackets become event-record nodes of the graph:
+            capi.call("tlora_profile_begin")  # every replay re-records them
         with torch.cuda.graph(g):
             self.step()
         self.graph_launches = capi.lib().tlora_launch_count() - n0  # kernels per replay
