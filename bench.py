@@ -323,7 +323,10 @@ def run_ours(args, rank, world, local_rank):
     achieved = fam_fl / (fam_ms / 1e3) / 1e12 if fam_ms > 0 else 0.0
     peak = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
     total_ms = sum(ms6)
-    per_launch = {capi.LAUNCH_NAMES[i]: {
+    names = list(capi.LAUNCH_NAMES)
+    if cnt[capi.L_DA] == 0 and cnt[capi.L_DB] > 0:
+        names[capi.L_DB] = "dB+dA (one launch)"
+    per_launch = {names[i]: {
         "launches": cnt[i], "ms_total": round(ms6[i], 3),
         "tflops": round(fl6[i] / (ms6[i] / 1e3) / 1e12, 1) if ms6[i] > 0 else None,
         "share_of_gemm_time": round(ms6[i] / total_ms, 4) if total_ms > 0 else None}

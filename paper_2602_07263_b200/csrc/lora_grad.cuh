@@ -30,12 +30,22 @@ struct GradSmem {
   static constexpr int kDynamic = kTotal + 1024;
 };
 
+// Up to two independent gradient problems in one persistent launch (dB and dA of a
+// projection): tiles [0, n0) come from problem 0 (operand maps tmA0 / tmB0), tiles
+// [n0, n0 + n1) from problem 1 (tmA1 / tmB1); each CTA continues across the boundary, so the
+// tail of one fills with the other.
+struct GradArgs {
+  GemmArgs job[2];
+};
+
 // Tile fields: m0 = M offset, n0 = first packed rank column of the job (chunk), kb0/ke0 =
-// token range, split = partial plane, pad = number of valid rank columns (<= 256).
+// token range, split = partial plane, pad = number of valid rank columns (<= 128).
 template <int STAGES>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    lora_grad_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const GemmArgs args) {
+    lora_grad_kernel(const __grid_constant__ CUtensorMap tmA0,
+                     const __grid_constant__ CUtensorMap tmB0,
+                     const __grid_constant__ CUtensorMap tmA1,
+                     const __grid_constant__ CUtensorMap tmB1, const GradArgs gargs) {
   using namespace ptx;
   using L = GradSmem<STAGES>;
   constexpr uint32_t kTmemCols = 256;
@@ -53,9 +63,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
 
+  const int n_first = gargs.job[0].num_tiles;
+  const int n_total = n_first + gargs.job[1].num_tiles;
+  // tile t -> (problem, its tile descriptor)
+  auto tile_of = [&](int t, int& j) -> TileDesc {
+    j = t < n_first ? 0 : 1;
+    return gargs.job[j].tiles[j == 0 ? t : t - n_first];
+  };
+
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmA0);
+    tma_prefetch_desc(&tmB0);
+    tma_prefetch_desc(&tmA1);
+    tma_prefetch_desc(&tmB1);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -79,8 +99,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {  // TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
-        const TileDesc td = args.tiles[t];
+      for (int t = blockIdx.x; t < n_total; t += gridDim.x) {
+        int j;
+        const TileDesc td = tile_of(t, j);
+        const CUtensorMap* tmA = j == 0 ? &tmA0 : &tmA1;
+        const CUtensorMap* tmB = j == 0 ? &tmB0 : &tmB1;
         const int nch = (td.pad + 63) / 64;
 #pragma unroll 1
         for (int k = td.kb0; k < td.ke0; k += kBK) {
@@ -88,19 +111,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
           mbar_arrive_expect_tx(&full_bar[stage], L::kABytes + nch * kChunk);
-          tma_load_2d(sa, &tmA, &full_bar[stage], td.m0, k);
-          tma_load_2d(sa + kChunk, &tmA, &full_bar[stage], td.m0 + 64, k);
+          tma_load_2d(sa, tmA, &full_bar[stage], td.m0, k);
+          tma_load_2d(sa + kChunk, tmA, &full_bar[stage], td.m0 + 64, k);
           for (int c = 0; c < nch; ++c)
-            tma_load_2d(sb + c * kChunk, &tmB, &full_bar[stage], td.n0 + 64 * c, k);
+            tma_load_2d(sb + c * kChunk, tmB, &full_bar[stage], td.n0 + 64 * c, k);
           // L2 prefetch one smem ring ahead (HBM latency > what the ring covers)
 #ifndef TLORA_PREFETCH_GRAD
 #define TLORA_PREFETCH_GRAD 0
 #endif
           const int kp = k + STAGES * kBK;
           if (TLORA_PREFETCH_GRAD && kp < td.ke0) {
-            tma_prefetch_2d(&tmA, td.m0, kp);
-            tma_prefetch_2d(&tmA, td.m0 + 64, kp);
-            for (int c = 0; c < nch; ++c) tma_prefetch_2d(&tmB, td.n0 + 64 * c, kp);
+            tma_prefetch_2d(tmA, td.m0, kp);
+            tma_prefetch_2d(tmA, td.m0 + 64, kp);
+            for (int c = 0; c < nch; ++c) tma_prefetch_2d(tmB, td.n0 + 64 * c, kp);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -111,8 +134,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int acc_iter = 0;
-      for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
-        const TileDesc td = args.tiles[t];
+      for (int t = blockIdx.x; t < n_total; t += gridDim.x) {
+        int j;
+        const TileDesc td = tile_of(t, j);
         const int nkb = td.ke0 > td.kb0 ? (td.ke0 - td.kb0 + kBK - 1) / kBK : 0;
         if (nkb == 0) continue;
         const uint32_t idesc = make_idesc_bf16(kBM, 64 * ((td.pad + 63) / 64), true, true);
@@ -142,8 +166,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp >= 4) {  // epilogue: transposed, column-masked fp32 store
     const int ew = warp & 3;
     int acc_iter = 0;
-    for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
-      const TileDesc td = args.tiles[t];
+    for (int t = blockIdx.x; t < n_total; t += gridDim.x) {
+      int j;
+      const TileDesc td = tile_of(t, j);
+      const GemmArgs& args = gargs.job[j];
       const bool empty_k = !(td.ke0 > td.kb0);
       const int mi = td.m0 + ew * 32 + (int)lane;  // M index (k or d)
       int acc = 0;

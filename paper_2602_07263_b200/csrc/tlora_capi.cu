@@ -389,21 +389,27 @@ __global__ void read_grad_kernel(const float* dAT, const float* dBc, int64_t d, 
   }
 }
 
-// grads[R x N] = beta * grads + sum_{s < cnt[row/128]} partial[s][R x N]  (fixed order)
-__global__ void reduce_splits_kernel(const float* __restrict__ partial, int64_t plane,
-                                     const int32_t* __restrict__ cnt, int64_t R, int64_t N,
-                                     float beta, float* __restrict__ grads) {
-  const int64_t n4 = N / 4;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R * n4;
+// Two reductions in one launch: problem j covers R x N_j; index space concatenated.
+struct ReduceJob {
+  const float* partial;
+  const int32_t* cnt;
+  float* grads;
+  int64_t N;
+};
+__global__ void reduce_splits2_kernel(ReduceJob j0, ReduceJob j1, int64_t R, float beta) {
+  const int64_t n0 = j0.partial ? R * j0.N / 4 : 0, n1 = j1.partial ? R * j1.N / 4 : 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n0 + n1;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / n4;
-    const int c = cnt[row];
+    const ReduceJob& J = i < n0 ? j0 : j1;
+    const int64_t q = i < n0 ? i : i - n0;
+    const int64_t n4 = J.N / 4, row = q / n4, plane = R * J.N;
+    const int c = J.cnt[row];
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < c; ++s) {
-      const float4 p = reinterpret_cast<const float4*>(partial + s * plane)[i];
+      const float4 p = reinterpret_cast<const float4*>(J.partial + s * plane)[q];
       acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
     }
-    float4* g = reinterpret_cast<float4*>(grads) + i;
+    float4* g = reinterpret_cast<float4*>(J.grads) + q;
     if (beta != 0.f) {
       const float4 o = *g;
       acc.x += beta * o.x; acc.y += beta * o.y; acc.z += beta * o.z; acc.w += beta * o.w;
@@ -411,6 +417,7 @@ __global__ void reduce_splits_kernel(const float* __restrict__ partial, int64_t 
     *g = acc;
   }
 }
+
 
 template <class T>
 struct DevBuf {
@@ -1098,54 +1105,83 @@ void run_dx(tlora_layer* layer, const tlora_plan* plan, const void* dY, const vo
                                    2.0 * T * d * k + 2.0 * (double)plan->P.tok_rank * d);
 }
 
-// which = 0: dBcat = Hᵀ·dY (lowrank = H, full = dY, N = k)
-// which = 1: dAᵀcat = dHᵀ·X (lowrank = dH, full = X, N = d)
-// over each rank tile's token range; grads = beta·grads + result (split-K reduced in order)
-void run_grad(tlora_layer* layer, const tlora_plan* plan, int which, const void* lowrank,
-              const void* full, float beta, cudaStream_t s) {
+// Adapter gradients, per job in transposed form (lora_grad.cuh), dB and/or dA in ONE
+// persistent launch:  dBcat = Hᵀ·dY (N = k)  and  dAᵀcat = dHᵀ·X (N = d), over each job's
+// token range; grads = beta·grads + result, split-K partials reduced in fixed order (one
+// combined reduce launch).
+void run_grads(tlora_layer* layer, const tlora_plan* plan, const void* H, const void* dY,
+               const void* dH, const void* X, bool do_b, bool do_a, float beta, cudaStream_t s) {
   const auto& L = layer->L;
   const int64_t T = plan->P.T, R = L.R;
-  const int launch = which == 0 ? TLORA_L_DB : TLORA_L_DA;
-  const int64_t N = which == 0 ? L.k : L.d;
-  const int nsplit = which == 0 ? plan->P.splits_db : plan->P.splits_da;
-  float* grads = which == 0 ? layer->dB.p : layer->dAT.p;
-  GemmArgs a{};
-  a.tiles = plan->tiles[launch].p;
-  a.num_tiles = (int)plan->P.tiles[launch].size();
-  a.M = (int)R;
-  a.N = (int)N;
-  a.ldo = N;
-  if (nsplit > 1) {
-    a.out = ws_get<float>(layer->device, s, false, (size_t)nsplit * R * N);
-    a.split_stride = R * N;
-    a.beta = 0.f;
-  } else {
-    a.out = grads;
-    a.beta = beta;
+  tlora::GradArgs g{};
+  CUtensorMap ma[2], mb[2];
+  ReduceJob rj[2] = {};
+  const bool on[2] = {do_b, do_a};
+  const int64_t Ns[2] = {L.k, L.d};
+  const int nsp[2] = {plan->P.splits_db, plan->P.splits_da};
+  float* grads[2] = {layer->dB.p, layer->dAT.p};
+  const int32_t* cnts[2] = {plan->cnt_db.p, plan->cnt_da.p};
+  const void* full[2] = {dY, X};
+  const void* low[2] = {H, dH};
+  // workspace: [problem 0 planes][problem 1 planes]
+  size_t need = 0;
+  for (int j = 0; j < 2; ++j)
+    if (on[j] && nsp[j] > 1) need += (size_t)nsp[j] * R * Ns[j];
+  float* ws = need ? ws_get<float>(layer->device, s, false, need) : nullptr;
+  size_t off = 0;
+  double flops = 0.0;
+  for (int j = 0; j < 2; ++j) {
+    const int launch = j == 0 ? TLORA_L_DB : TLORA_L_DA;
+    GemmArgs& a = g.job[j];
+    if (!on[j]) {
+      a.num_tiles = 0;
+      ma[j] = ma[0];
+      mb[j] = mb[0];
+      continue;
+    }
+    const int64_t N = Ns[j];
+    a.tiles = plan->tiles[launch].p;
+    a.num_tiles = (int)plan->P.tiles[launch].size();
+    a.M = (int)N;  // transposed form: M = layer dimension, output rows = packed rank columns
+    a.N = (int)N;
+    a.ldo = N;
+    if (nsp[j] > 1) {
+      a.out = ws + off;
+      a.split_stride = R * N;
+      a.beta = 0.f;
+      rj[j] = {ws + off, cnts[j], grads[j], N};
+      off += (size_t)nsp[j] * R * N;
+    } else {
+      a.out = grads[j];
+      a.beta = beta;
+    }
+    ma[j] = tmap_mn(full[j], N, T);
+    mb[j] = tmap_mn(low[j], R, T);
+    flops += 2.0 * (double)plan->P.tok_rank * N;
   }
-  a.M = (int)N;  // transposed form: M = layer dimension, output rows = packed rank columns
-  const CUtensorMap ma = tmap_mn(full, N, T);
-  const CUtensorMap mb = tmap_mn(lowrank, R, T);
-  {
+  if (!on[0]) {  // problem 1 alone: keep its maps in slot 1, slot 0 unused
+    ma[0] = ma[1];
+    mb[0] = mb[1];
+  }
+  const int tiles = g.job[0].num_tiles + g.job[1].num_tiles;
 #ifndef TLORA_GRAD_STAGES
 #define TLORA_GRAD_STAGES 6
 #endif
-    auto kern = tlora::lora_grad_kernel<TLORA_GRAD_STAGES>;
-    constexpr int smem = tlora::GradSmem<TLORA_GRAD_STAGES>::kDynamic;
-    TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int grid = std::min(a.num_tiles, sm_budget(layer->device, layer->sm_count, false));
-    ProfScope ps(launch, 2.0 * (double)plan->P.tok_rank * N, s);
-    if (a.num_tiles > 0) {
-      launch_pdl(kern, grid, smem, s, ma, mb, a);
+  auto kern = tlora::lora_grad_kernel<TLORA_GRAD_STAGES>;
+  constexpr int smem = tlora::GradSmem<TLORA_GRAD_STAGES>::kDynamic;
+  TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int grid = std::min(tiles, sm_budget(layer->device, layer->sm_count, false));
+  {
+    ProfScope ps(do_b ? TLORA_L_DB : TLORA_L_DA, flops, s);  // dB+dA together: booked on dB
+    if (tiles > 0) {
+      launch_pdl(kern, grid, smem, s, ma[0], mb[0], ma[1], mb[1], g);
       g_launches.fetch_add(1, std::memory_order_relaxed);
     }
   }
-  if (nsplit > 1) {
-    const int32_t* cnt = which == 0 ? plan->cnt_db.p : plan->cnt_da.p;
-    const int64_t work = R * N / 4;
+  if (rj[0].partial || rj[1].partial) {
+    const int64_t work = (rj[0].partial ? R * rj[0].N / 4 : 0) + (rj[1].partial ? R * rj[1].N / 4 : 0);
     const int blocks = (int)std::min<int64_t>(tlora::ceil_div(work, 256), 4 * layer->sm_count);
-    reduce_splits_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const float*>(a.out), R * N, cnt, R,
-                                                N, beta, grads);
+    reduce_splits2_kernel<<<blocks, 256, 0, s>>>(rj[0], rj[1], R, beta);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     TL_CUDA(cudaGetLastError());
   }
@@ -1268,8 +1304,7 @@ int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, c
         ws_get<__nv_bfloat16>(layer->device, s, true, (size_t)plan->P.T * layer->L.R);
     run_dh(layer, plan, dY, dH, s);
     if (dX) run_dx(layer, plan, dY, dH, dX, 0.f, s);
-    run_grad(layer, plan, 0, H_stash, dY, beta, s);
-    run_grad(layer, plan, 1, dH, X, beta, s);
+    run_grads(layer, plan, H_stash, dY, dH, X, true, true, beta, s);
   });
 }
 
@@ -1303,7 +1338,8 @@ int tlora_backward_grad_b(tlora_layer* layer, const tlora_plan* plan, const void
     check_align(H, "H");
     check_align(dY, "dY");
     DeviceGuard g(layer->device);
-    run_grad(layer, plan, 0, H, dY, beta, reinterpret_cast<cudaStream_t>(stream));
+    run_grads(layer, plan, H, dY, nullptr, nullptr, true, false, beta,
+              reinterpret_cast<cudaStream_t>(stream));
   });
 }
 
@@ -1314,7 +1350,8 @@ int tlora_backward_grad_a(tlora_layer* layer, const tlora_plan* plan, const void
     check_align(X, "X");
     check_align(dH, "dH");
     DeviceGuard g(layer->device);
-    run_grad(layer, plan, 1, dH, X, beta, reinterpret_cast<cudaStream_t>(stream));
+    run_grads(layer, plan, nullptr, nullptr, dH, X, false, true, beta,
+              reinterpret_cast<cudaStream_t>(stream));
   });
 }
 
