@@ -127,7 +127,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     capi.call("tlora_device_check", local_rank, None)
     wl = config(args.config)
-    step = LayerSetStep(wl, device=local_rank, seed=wl.seed + rank, shuffle=args.shuffle)
+    step = LayerSetStep(wl, device=local_rank, seed=wl.seed + rank, shuffle=args.shuffle,
+                        chain=not args.no_chain and args.overlap == 0)
     step.enable_optimizer()
     if args.overlap != 0:
         step.enable_overlap(args.overlap)
@@ -370,7 +371,8 @@ def run_ours(args, rank, world, local_rank):
                    "jobs": [[j.job_id, j.rank, j.tokens] for j in wl.jobs],
                    "projections": wl.projections, "token_order": "shuffled" if args.shuffle else "job-contiguous",
                    "parallelism": f"dp{world}", "lowrank_side_stream_sms": args.overlap,
-                   "cuda_graph": used_graph, "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)",
+                   "cuda_graph": used_graph, "chained_lowrank": step.chain,
+                   "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)",
                    "algorithmic_tflop_per_step": round(flops_step / 1e12, 3),
                    "achieved_tflops_step": round(flops_step / (ms_per_step / 1e3) / 1e12, 1)},
         "e2e": {"value": round(tokens / (e2e_ms / 1e3), 1), "unit": "tokens/s",
@@ -517,6 +519,9 @@ def main():
                     help="low-rank launches on a side stream concurrent with the fused GEMMs: "
                          "N>0 caps them to N SMs (GEMMs get the rest), -1 = uncapped, "
                          "0 = serial schedule")
+    ap.add_argument("--no-chain", action="store_true",
+                    help="one launch per shrink / dH instead of chaining them into the "
+                         "previous fused GEMM launch")
     ap.add_argument("--no-graph", action="store_true",
                     help="launch every kernel eagerly instead of replaying the captured "
                          "CUDA graph of the training step (graphs are used at N=1)")

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define TLORA_ABI_VERSION 1
+#define TLORA_ABI_VERSION 2
 
 enum tlora_status {
   TLORA_OK = 0,
@@ -63,8 +63,14 @@ enum tlora_launch {
   TLORA_L_DX = 3,      /* dX  = dY·Wᵀ + dH·A_jᵀ                            */
   TLORA_L_DB = 4,      /* dB_j = H_jᵀ·dY_j     (fp32, token-range K)       */
   TLORA_L_DA = 5,      /* dA_jᵀ = dH_jᵀ·X_j    (fp32, token-range K)       */
-  TLORA_L_COUNT = 6
+  /* the same shrink / dH work on 256-token CTA-pair tiles (N = 128 or 256 packed rank
+   * columns), run as secondary tiles inside another layer's fused GEMM launch */
+  TLORA_L_SHRINK2 = 6,
+  TLORA_L_DH2 = 7,
+  TLORA_L_COUNT = 8
 };
+/* launch kinds reported by the live profiler (tlora_profile_end arrays) */
+#define TLORA_PROF_KINDS 6
 
 typedef struct tlora_plan_info {
   int64_t tokens;          /* T                                                    */
@@ -177,6 +183,17 @@ int tlora_forward_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X
  * recv_ptrs[world]: every rank's receive buffer [world][slot_rows][k] bf16 (peer-mapped,
  * e.g. symmetric memory); this rank writes slot `rank`, rows dst_row0 + r % (T / world).
  * After a cross-rank barrier, tlora_reduce_slots sums the slots in fixed order. */
+/* tlora_forward_gemm of `layer` with the shrink of `next` (H_next = X_next·Aᵀcat masked, as
+ * tlora_forward_shrink) carried as extra CTA-pair tiles of the SAME launch (plan table
+ * TLORA_L_SHRINK2 of next_plan), so the next projection's shrink fills this GEMM's tail
+ * instead of paying its own launch ramp. H_next must be zero outside next_plan's windows:
+ * zero_next = 1 memsets it first; 0 when the caller keeps it zeroed (same-slot plans only
+ * ever write the same windows). H_next must not alias H, Y or X. Bit-identical to the
+ * two separate calls. */
+int tlora_forward_gemm_shrink(tlora_layer* layer, const tlora_plan* plan, const void* X,
+                              const void* H, void* Y, int y_dtype, tlora_layer* next,
+                              const tlora_plan* next_plan, const void* X_next, void* H_next,
+                              int zero_next, void* stream);
 int tlora_forward_gemm_rs(tlora_layer* layer, const tlora_plan* plan, const void* X, const void* H,
                           void* const* recv_ptrs, int32_t world, int32_t rank, int64_t slot_rows,
                           int64_t dst_row0, void* stream);
@@ -188,6 +205,17 @@ int tlora_backward_dh(tlora_layer* layer, const tlora_plan* plan, const void* dY
 /* dX = dY·Wᵀ + dH·Aᵀ + beta·dX (beta = 1 sums the dX of projections sharing an input) */
 int tlora_backward_dx(tlora_layer* layer, const tlora_plan* plan, const void* dY, const void* dH,
                       void* dX, float beta, void* stream);
+/* tlora_backward_dx of `layer` with the dH of `next` (dH_next = dY_next·Bᵀcat masked, as
+ * tlora_backward_dh) as extra tiles of the same launch (plan table TLORA_L_DH2); zero_next
+ * as in tlora_forward_gemm_shrink. Bit-identical to the two separate calls. */
+int tlora_backward_dx_dh(tlora_layer* layer, const tlora_plan* plan, const void* dY,
+                         const void* dH, void* dX, float beta, tlora_layer* next,
+                         const tlora_plan* next_plan, const void* dY_next, void* dH_next,
+                         int zero_next, void* stream);
+/* Both adapter gradients in ONE persistent launch (+ one split-K reduce): dB from (H, dY)
+ * and dA from (X, dH); = tlora_backward_grad_b then tlora_backward_grad_a. */
+int tlora_backward_grads(tlora_layer* layer, const tlora_plan* plan, const void* H,
+                         const void* dY, const void* X, const void* dH, float beta, void* stream);
 int tlora_backward_grad_b(tlora_layer* layer, const tlora_plan* plan, const void* H,
                           const void* dY, float beta, void* stream);
 int tlora_backward_grad_a(tlora_layer* layer, const tlora_plan* plan, const void* X,
@@ -203,7 +231,8 @@ int tlora_set_sm_budget(int device, int32_t gemm_sms, int32_t lowrank_sms);
 /* Between begin and end every GEMM launch is bracketed by CUDA events. end() waits for
  * them and returns, per tlora_launch kind, the launch count, summed device ms and the
  * summed algorithmic FLOPs (padding and packing waste excluded). Arrays have
- * TLORA_L_COUNT entries; any may be NULL. */
+ * TLORA_PROF_KINDS entries; any may be NULL. A fused GEMM launch that also carries another
+ * layer's shrink / dH tiles is booked under its main kind (FWD / DX). */
 int tlora_profile_begin(void);
 /* Total number of kernels this library has enqueued since load (monotonic). */
 long long tlora_launch_count(void);

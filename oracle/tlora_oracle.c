@@ -255,7 +255,7 @@ static void emit(TileSink* s, int32_t m0, int32_t n0, int32_t kb0, int32_t ke0, 
 
 int64_t orc_plan_tiles(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t* ranks,
                        const int32_t* slot, int32_t which, int32_t* out, int64_t cap) {
-  if (T < 1 || S < 1 || which < 0 || which > 5 || check_slots(T, S, slot)) return -1;
+  if (T < 1 || S < 1 || which < 0 || which > 7 || check_slots(T, S, slot)) return -1;
   int32_t* off = (int32_t*)malloc(sizeof(int32_t) * S);
   int32_t R = 0;
   for (int32_t s = 0; s < S; ++s) {
@@ -265,7 +265,7 @@ int64_t orc_plan_tiles(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t
   if (R < 8) R = 8;
   TileSink sink = {out, cap, 0};
   const int64_t n_mt = cdiv(T, BM);
-  if (which <= 3) {
+  if (which <= 3 || which >= 6) {
     int32_t* win_lo = (int32_t*)malloc(sizeof(int32_t) * (size_t)n_mt);
     int32_t* win_hi = (int32_t*)malloc(sizeof(int32_t) * (size_t)n_mt);
     for (int64_t m = 0; m < n_mt; ++m) {
@@ -286,6 +286,24 @@ int64_t orc_plan_tiles(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t
       if (which == 0 || which == 2)
         for (int32_t n0 = c_lo; n0 < c_hi; n0 += BN_LOW)
           emit(&sink, (int32_t)(m * BM), n0, 0, (int32_t)(which == 0 ? d : k), 0, 0, 0);
+    }
+    if (which >= 6) {
+      /* shrink / dH on 256-token pair tiles: window = union of the halves, N-chunks of <= 256
+       * each rounded up to a multiple of 128 columns */
+      const int64_t n_m2 = cdiv(T, BM2), K = which == 6 ? d : k;
+      for (int64_t m = 0; m < n_m2; ++m) {
+        int32_t lo = win_lo[2 * m], hi = win_hi[2 * m];
+        if (2 * m + 1 < n_mt) {
+          if (win_lo[2 * m + 1] < lo) lo = win_lo[2 * m + 1];
+          if (win_hi[2 * m + 1] > hi) hi = win_hi[2 * m + 1];
+        }
+        for (int32_t n0 = lo; n0 < hi; n0 += 256) {
+          int32_t n = (int32_t)(cdiv(hi - n0, 128) * 128);
+          if (n > 256) n = 256;
+          emit(&sink, (int32_t)(m * BM2), n0, 0, (int32_t)K, 0, 0, 0);
+          if (sink.n <= sink.cap) sink.out[8 * (sink.n - 1) + 7] = n;
+        }
+      }
     }
     if (which == 1 || which == 3) {
       /* fused base GEMMs: 256-token tiles (CTA pairs); window = union of the two halves.

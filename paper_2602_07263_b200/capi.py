@@ -17,7 +17,7 @@ LIB_PATH = Path(os.environ.get("TLORA_LIB", _PKG_DIR / "libtlora.so"))
 OK, ERR_ARG, ERR_SHAPE, ERR_REGISTRY, ERR_PLAN, ERR_CUDA, ERR_NO_DEVICE = range(7)
 F64, F32, BF16 = 0, 1, 2
 HOST, DEVICE = 0, 1
-L_SHRINK, L_FWD, L_DH, L_DX, L_DB, L_DA = range(6)
+L_SHRINK, L_FWD, L_DH, L_DX, L_DB, L_DA, L_SHRINK2, L_DH2 = range(8)
 LAUNCH_NAMES = ("shrink", "fwd", "dH", "dX", "dB", "dA")
 
 
@@ -32,7 +32,7 @@ class PlanInfoC(C.Structure):
         ("k", C.c_int64),
         ("num_slots", C.c_int32),
         ("rank_pad_total", C.c_int32),
-        ("num_tiles", C.c_int32 * 6),
+        ("num_tiles", C.c_int32 * 8),
         ("splits_db", C.c_int32),
         ("splits_da", C.c_int32),
         ("useful_ext_cols", C.c_int64),
@@ -86,6 +86,8 @@ SIGNATURES = {
                                        C.c_void_p]),
     "tlora_forward_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_int, C.c_void_p]),
+    "tlora_forward_gemm_shrink": (C.c_int, [C.c_void_p] * 5 + [C.c_int] + [C.c_void_p] * 4
+                                  + [C.c_int, C.c_void_p]),
     "tlora_forward_gemm_rs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int64,
                                         C.c_int64, C.c_void_p]),
@@ -94,6 +96,9 @@ SIGNATURES = {
     "tlora_backward_dh": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "tlora_backward_dx": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_float, C.c_void_p]),
+    "tlora_backward_dx_dh": (C.c_int, [C.c_void_p] * 5 + [C.c_float] + [C.c_void_p] * 4
+                             + [C.c_int, C.c_void_p]),
+    "tlora_backward_grads": (C.c_int, [C.c_void_p] * 6 + [C.c_float, C.c_void_p]),
     "tlora_backward_grad_b": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.c_float, C.c_void_p]),
     "tlora_backward_grad_a": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -34,12 +34,20 @@ struct Gemm2Smem {
   static constexpr int kDynamic = kTotal + 1024;
 };
 
+// Secondary tiles (args2, maps tmA2 / tmB2): another layer's shrink or dH on 256-token
+// pair tiles, appended after the main tiles of the launch. They do not depend on the main
+// tiles; they fill the tail of the persistent schedule. Tile: one K-segment [kb0, ke0),
+// runtime N = td.pad (128 or 256, split N/2 per CTA; tmB2 boxes are 64 rows), masked bf16
+// epilogue (EPI_BF16_MASK semantics with args2's row -> slot -> column window).
 template <int EPI, int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     lora_gemm2_kernel(const __grid_constant__ CUtensorMap tmA0,
                       const __grid_constant__ CUtensorMap tmB0,
                       const __grid_constant__ CUtensorMap tmA1,
-                      const __grid_constant__ CUtensorMap tmB1, const GemmArgs args) {
+                      const __grid_constant__ CUtensorMap tmB1,
+                      const __grid_constant__ CUtensorMap tmA2,
+                      const __grid_constant__ CUtensorMap tmB2, const GemmArgs args,
+                      const GemmArgs args2) {
   using namespace ptx;
   using L = Gemm2Smem<STAGES>;
   constexpr uint32_t kTmemCols = 2 * kBN2;
@@ -60,12 +68,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x / 2;
   const int num_clusters = gridDim.x / 2;
+  const int n_main = args.num_tiles;
+  const int n_total = n_main + args2.num_tiles;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA0);
     tma_prefetch_desc(&tmB0);
     tma_prefetch_desc(&tmA1);
     tma_prefetch_desc(&tmB1);
+    if (args2.num_tiles > 0) {
+      tma_prefetch_desc(&tmA2);
+      tma_prefetch_desc(&tmB2);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -91,9 +105,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster_id; t < args.num_tiles; t += num_clusters) {
-        const TileDesc td = args.tiles[t];
+      for (int t = cluster_id; t < n_total; t += num_clusters) {
+        const bool sec = t >= n_main;
+        const TileDesc td = sec ? args2.tiles[t - n_main] : args.tiles[t];
         const int am = td.m0 + 128 * (int)rank;
+        if (sec) {  // another layer's shrink / dH: B half = N/2 rows in 64-row boxes
+          const int half = td.pad / 2;
+          const int bn = td.n0 + half * (int)rank;
+#pragma unroll 1
+          for (int k = td.kb0; k < td.ke0; k += kBK) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * L::kStageBytes;
+            uint8_t* sb = sa + L::kABytes;
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * (L::kABytes + half * kBK * 2));
+            const uint32_t fb = full0 + stage * 8;
+            tma_load_2d_cg2(sa, &tmA2, fb, k, am);
+            for (int c = 0; c < half / 64; ++c)
+              tma_load_2d_cg2(sb + c * 64 * kBK * 2, &tmB2, fb, k, bn + 64 * c);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          continue;
+        }
         const int bn = td.n0 + 128 * (int)rank;
 #pragma unroll 1
         for (int seg = 0; seg < 2; ++seg) {
@@ -121,11 +153,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int acc_iter = 0;
-      for (int t = cluster_id; t < args.num_tiles; t += num_clusters) {
-        const TileDesc td = args.tiles[t];
+      for (int t = cluster_id; t < n_total; t += num_clusters) {
+        const bool sec = t >= n_main;
+        const TileDesc td = sec ? args2.tiles[t - n_main] : args.tiles[t];
         const int nkb = (td.ke0 > td.kb0 ? (td.ke0 - td.kb0 + kBK - 1) / kBK : 0) +
-                        (td.ke1 > td.kb1 ? (td.ke1 - td.kb1 + kBK - 1) / kBK : 0);
+                        (!sec && td.ke1 > td.kb1 ? (td.ke1 - td.kb1 + kBK - 1) / kBK : 0);
         if (nkb == 0) continue;
+        const uint32_t idesc = sec ? make_idesc_bf16(kBM2, td.pad, false, false) : kIdesc;
         const int acc = acc_iter & 1;
         const uint32_t acc_phase = (acc_iter >> 1) & 1;
         ++acc_iter;
@@ -141,7 +175,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk)
             mma_bf16_ss_cg2(d_tmem, make_smem_desc_kmajor(sa + kk * 32),
-                            make_smem_desc_kmajor(sb + kk * 32), kIdesc, (kb | kk) != 0 ? 1u : 0u);
+                            make_smem_desc_kmajor(sb + kk * 32), idesc, (kb | kk) != 0 ? 1u : 0u);
           mma_commit_cg2_mc(&empty_bar[stage], 0x3);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -153,9 +187,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const int ew = warp & 3;
     const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
     int acc_iter = 0;
-    for (int t = cluster_id; t < args.num_tiles; t += num_clusters) {
-      const TileDesc td = args.tiles[t];
-      const bool empty_k = !(td.ke0 > td.kb0) && !(td.ke1 > td.kb1);
+    for (int t = cluster_id; t < n_total; t += num_clusters) {
+      const bool sec = t >= n_main;
+      const TileDesc td = sec ? args2.tiles[t - n_main] : args.tiles[t];
+      const bool empty_k = !(td.ke0 > td.kb0) && (sec || !(td.ke1 > td.kb1));
       const int row = td.m0 + 128 * (int)rank + ew * 32 + (int)lane;
       int acc = 0;
       if (!empty_k) {
@@ -165,9 +200,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
       }
+      int lo = 0, hi = 0x7fffffff;
+      if (sec && row < args2.M) {
+        const int sl = args2.row_slot[row];
+        lo = args2.slot_col_lo[sl];
+        hi = args2.slot_col_hi[sl];
+      }
+      const int ncols = sec ? td.pad : kBN2;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * kBN2;
 #pragma unroll 1
-      for (int c = 0; c < kBN2; c += 32) {
+      for (int c = 0; c < ncols; c += 32) {
         uint32_t v[32];
         if (!empty_k) {
           tmem_ld_32x32b_x32(t_row + c, v);
@@ -176,7 +218,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = 0u;
         }
-        epi_store32<EPI>(args, td.split, row, td.n0 + c, v, 0, 0x7fffffff);
+        if (sec)
+          epi_store32<EPI_BF16_MASK>(args2, 0, row, td.n0 + c, v, lo, hi);
+        else
+          epi_store32<EPI>(args, td.split, row, td.n0 + c, v, 0, 0x7fffffff);
       }
       if (!empty_k) {
         tc_fence_before();

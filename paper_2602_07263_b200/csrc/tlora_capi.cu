@@ -209,19 +209,30 @@ void launch_gemm(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap
 #ifndef TLORA_GEMM2_STAGES
 #define TLORA_GEMM2_STAGES 6
 #endif
+// Secondary tile job of a 2-CTA launch (lora_gemm2.cuh): another layer's shrink / dH.
+struct Gemm2Secondary {
+  CUtensorMap a, b;
+  GemmArgs args;
+  double flops;
+};
+
 template <int EPI, int ST>
 void launch_gemm2(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1,
                   const CUtensorMap& b1, const GemmArgs& args, int sm_count, cudaStream_t s,
-                  int launch_kind, double flops) {
-  if (args.num_tiles == 0) return;
+                  int launch_kind, double flops, const Gemm2Secondary* sec = nullptr) {
+  GemmArgs args2{};
+  const int total = args.num_tiles + (sec ? sec->args.num_tiles : 0);
+  if (total == 0) return;
+  if (sec) args2 = sec->args;
   auto kern = tlora::lora_gemm2_kernel<EPI, ST>;
   constexpr int smem = tlora::Gemm2Smem<ST>::kDynamic;
   TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int dev = 0;
   TL_CUDA(cudaGetDevice(&dev));
-  const int grid = std::min(2 * args.num_tiles, sm_budget(dev, sm_count, true) / 2 * 2);
-  ProfScope ps(launch_kind, flops, s);
-  launch_pdl(kern, grid, smem, s, a0, b0, a1, b1, args);
+  const int grid = std::min(2 * total, sm_budget(dev, sm_count, true) / 2 * 2);
+  ProfScope ps(launch_kind, flops + (sec ? sec->flops : 0.0), s);
+  launch_pdl(kern, grid, smem, s, a0, b0, a1, b1, sec ? sec->a : a0, sec ? sec->b : b0, args,
+             args2);
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
@@ -1038,9 +1049,34 @@ void run_shrink(tlora_layer* layer, const tlora_plan* plan, const void* X, void*
                                                           2.0 * (double)plan->P.tok_rank * d);
 }
 
+// The shrink (which = 0: H = X·Aᵀcatᵀ, K = d) or dH (which = 1: dH = dY·Bᵀ, K = k) of a
+// layer as secondary pair tiles of another layer's fused GEMM launch (plan tables SHRINK2 /
+// DH2: 256-token tiles, N 128 or 256 over the token tile's rank window). Masked like
+// run_shrink / run_dh; the caller guarantees the output is zero outside the windows.
+Gemm2Secondary make_lowrank2(tlora_layer* layer, const tlora_plan* plan, int which, const void* A,
+                             void* out) {
+  const auto& L = layer->L;
+  const int64_t T = plan->P.T, R = L.R, K = which == 0 ? L.d : L.k;
+  const int launch = which == 0 ? TLORA_L_SHRINK2 : TLORA_L_DH2;
+  Gemm2Secondary g{};
+  g.args.tiles = plan->tiles[launch].p;
+  g.args.num_tiles = (int)plan->P.tiles[launch].size();
+  g.args.M = (int)T;
+  g.args.N = (int)R;
+  g.args.out = out;
+  g.args.ldo = R;
+  g.args.row_slot = plan->token_slot.p;
+  g.args.slot_col_lo = layer->col_lo.p;
+  g.args.slot_col_hi = layer->col_hi.p;
+  g.a = tmap_k(A, K, T, 128);
+  g.b = tmap_k(which == 0 ? layer->AT.p : layer->Bcat.p, K, R, 64);
+  g.flops = 2.0 * (double)plan->P.tok_rank * K;
+  return g;
+}
+
 // Y = X·W + H·Bᵀcatᵀ: 2-CTA fused GEMM, K-extension over each tile's packed-rank window.
 void run_fwd_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X, const void* H, void* Y,
-                  int y_dtype, cudaStream_t s) {
+                  int y_dtype, cudaStream_t s, const Gemm2Secondary* sec = nullptr) {
   const auto& L = layer->L;
   const int64_t T = plan->P.T, d = L.d, k = L.k, R = L.R;
   const double flops = 2.0 * T * d * k + 2.0 * (double)plan->P.tok_rank * k;
@@ -1057,9 +1093,11 @@ void run_fwd_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X, con
   const CUtensorMap ma1 = tmap_k(H, R, T, 128);
   const CUtensorMap mb1 = tmap_k(layer->BcatT.p, R, k, 128);
   if (y_dtype == TLORA_BF16)
-    launch_gemm2<tlora::EPI_BF16, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD, flops);
+    launch_gemm2<tlora::EPI_BF16, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s,
+                                                      TLORA_L_FWD, flops, sec);
   else
-    launch_gemm2<tlora::EPI_F32, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD, flops);
+    launch_gemm2<tlora::EPI_F32, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s,
+                                                     TLORA_L_FWD, flops, sec);
 }
 
 // dH = dY·Bᵀ (masked; zero outside the windows, as H)
@@ -1086,7 +1124,7 @@ void run_dh(tlora_layer* layer, const tlora_plan* plan, const void* dY, void* dH
 
 // dX = dY·Wᵀ + dH·Aᵀ (2-CTA fused GEMM)
 void run_dx(tlora_layer* layer, const tlora_plan* plan, const void* dY, const void* dH, void* dX,
-            float beta, cudaStream_t s) {
+            float beta, cudaStream_t s, const Gemm2Secondary* sec = nullptr) {
   const auto& L = layer->L;
   const int64_t T = plan->P.T, d = L.d, k = L.k, R = L.R;
   GemmArgs a{};
@@ -1101,8 +1139,10 @@ void run_dx(tlora_layer* layer, const tlora_plan* plan, const void* dY, const vo
   const CUtensorMap mb0 = tmap_k(layer->W16.p, k, d, 128);
   const CUtensorMap ma1 = tmap_k(dH, R, T, 128);
   const CUtensorMap mb1 = tmap_k(layer->Acat.p, R, d, 128);
-  launch_gemm2<tlora::EPI_BF16, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_DX,
-                                   2.0 * T * d * k + 2.0 * (double)plan->P.tok_rank * d);
+  launch_gemm2<tlora::EPI_BF16, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s,
+                                                    TLORA_L_DX,
+                                                    2.0 * T * d * k + 2.0 * (double)plan->P.tok_rank * d,
+                                                    sec);
 }
 
 // Adapter gradients, per job in transposed form (lora_grad.cuh), dB and/or dA in ONE
@@ -1232,6 +1272,32 @@ int tlora_forward_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X
   });
 }
 
+int tlora_forward_gemm_shrink(tlora_layer* layer, const tlora_plan* plan, const void* X,
+                              const void* H, void* Y, int y_dtype, tlora_layer* next,
+                              const tlora_plan* next_plan, const void* X_next, void* H_next,
+                              int zero_next, void* stream) {
+  return guarded([&] {
+    check_bound(layer, plan);
+    check_bound(next, next_plan);
+    check_align(X, "X");
+    check_align(H, "H");
+    check_align(Y, "Y");
+    check_align(X_next, "X_next");
+    check_align(H_next, "H_next");
+    require(y_dtype == TLORA_BF16 || y_dtype == TLORA_F32, TLORA_ERR_ARG,
+            "Y dtype must be bf16 or f32");
+    require(next->device == layer->device, TLORA_ERR_ARG, "layers on different devices");
+    require(H_next != H && H_next != Y && H_next != X, TLORA_ERR_ARG,
+            "H_next must not alias this layer's operands");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (zero_next)
+      TL_CUDA(cudaMemsetAsync(H_next, 0, (size_t)next_plan->P.T * next->L.R * 2, s));
+    const Gemm2Secondary sec = make_lowrank2(next, next_plan, 0, X_next, H_next);
+    run_fwd_gemm(layer, plan, X, H, Y, y_dtype, s, &sec);
+  });
+}
+
 int tlora_forward_gemm_rs(tlora_layer* layer, const tlora_plan* plan, const void* X, const void* H,
                           void* const* recv_ptrs, int32_t world, int32_t rank, int64_t slot_rows,
                           int64_t dst_row0, void* stream) {
@@ -1331,6 +1397,43 @@ int tlora_backward_dx(tlora_layer* layer, const tlora_plan* plan, const void* dY
   });
 }
 
+int tlora_backward_dx_dh(tlora_layer* layer, const tlora_plan* plan, const void* dY,
+                         const void* dH, void* dX, float beta, tlora_layer* next,
+                         const tlora_plan* next_plan, const void* dY_next, void* dH_next,
+                         int zero_next, void* stream) {
+  return guarded([&] {
+    check_bound(layer, plan);
+    check_bound(next, next_plan);
+    check_align(dY, "dY");
+    check_align(dH, "dH");
+    check_align(dX, "dX");
+    check_align(dY_next, "dY_next");
+    check_align(dH_next, "dH_next");
+    require(next->device == layer->device, TLORA_ERR_ARG, "layers on different devices");
+    require(dH_next != dH && dH_next != dX && dH_next != dY, TLORA_ERR_ARG,
+            "dH_next must not alias this layer's operands");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (zero_next)
+      TL_CUDA(cudaMemsetAsync(dH_next, 0, (size_t)next_plan->P.T * next->L.R * 2, s));
+    const Gemm2Secondary sec = make_lowrank2(next, next_plan, 1, dY_next, dH_next);
+    run_dx(layer, plan, dY, dH, dX, beta, s, &sec);
+  });
+}
+
+int tlora_backward_grads(tlora_layer* layer, const tlora_plan* plan, const void* H,
+                         const void* dY, const void* X, const void* dH, float beta, void* stream) {
+  return guarded([&] {
+    check_bound(layer, plan);
+    check_align(H, "H");
+    check_align(dY, "dY");
+    check_align(X, "X");
+    check_align(dH, "dH");
+    DeviceGuard g(layer->device);
+    run_grads(layer, plan, H, dY, dH, X, true, true, beta, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
 int tlora_backward_grad_b(tlora_layer* layer, const tlora_plan* plan, const void* H,
                           const void* dY, float beta, void* stream) {
   return guarded([&] {
@@ -1382,7 +1485,7 @@ int tlora_profile_end(int32_t* counts, double* total_ms, double* total_flops) {
   return guarded([&] {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     g_prof_on = false;
-    for (int l = 0; l < TLORA_L_COUNT; ++l) {
+    for (int l = 0; l < TLORA_PROF_KINDS; ++l) {
       if (counts) counts[l] = 0;
       if (total_ms) total_ms[l] = 0.0;
       if (total_flops) total_flops[l] = 0.0;
@@ -1391,7 +1494,7 @@ int tlora_profile_end(int32_t* counts, double* total_ms, double* total_flops) {
       TL_CUDA(cudaEventSynchronize(r.e1));
       float ms = 0.f;
       TL_CUDA(cudaEventElapsedTime(&ms, r.e0, r.e1));
-      if (r.launch >= 0 && r.launch < TLORA_L_COUNT) {
+      if (r.launch >= 0 && r.launch < TLORA_PROF_KINDS) {
         if (counts) counts[r.launch] += 1;
         if (total_ms) total_ms[r.launch] += ms;
         if (total_flops) total_flops[r.launch] += r.flops;

@@ -63,7 +63,7 @@ constexpr int kPlanMinSplitTokens = 512;
 struct PlanTables {
   RegistryLayout layout;
   int64_t T = 0;
-  std::vector<PlanTile> tiles[6];  // indexed by tlora_launch
+  std::vector<PlanTile> tiles[8];  // indexed by tlora_launch
   std::vector<int32_t> split_count_db, split_count_da;  // per packed rank row (R entries)
   int32_t splits_db = 1, splits_da = 1;
   int64_t useful_ext_cols = 0, packed_ext_cols = 0;
@@ -243,6 +243,18 @@ inline PlanTables build_plan(const RegistryLayout& L, int64_t T, const int32_t* 
       w_lo[m] = std::min(w_lo[m], c_lo[2 * m + 1]);
       w_hi[m] = std::max(w_hi[m], c_hi[2 * m + 1]);
     }
+  }
+  // shrink / dH on 256-token CTA-pair tiles (secondary tiles of a fused GEMM launch):
+  // N-chunks of <= 256 over the pair's window, each rounded up to 128 columns (the extra
+  // columns belong to other jobs and are written as masked zeros)
+  for (int which = 0; which < 2; ++which) {
+    const int64_t K = which == 0 ? L.d : L.k;
+    auto& v = P.tiles[which == 0 ? 6 : 7];
+    for (int64_t m = 0; m < n_mt2; ++m)
+      for (int32_t n0 = w_lo[m]; n0 < w_hi[m]; n0 += 256) {
+        const int32_t n = std::min<int32_t>(256, (int32_t)(ceil_div(w_hi[m] - n0, 128) * 128));
+        v.push_back({(int32_t)(m * kPlanBMBase), n0, 0, (int32_t)K, 0, 0, 0, n});
+      }
   }
   for (int which = 0; which < 2; ++which) {
     const int64_t N = which == 0 ? L.k : L.d;

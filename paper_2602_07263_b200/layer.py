@@ -211,6 +211,14 @@ class FusedLoRALayer:
         call("tlora_forward_gemm", self._h, plan._h, _ptr(X), _ptr(H), _ptr(Y), _DT[Y.dtype],
              _stream_ptr(stream))
 
+    def fused_gemm_shrink(self, plan: Plan, X, H, Y, nxt: "FusedLoRALayer", next_plan: Plan,
+                          X_next, H_next, zero_next=True, stream=None):
+        """fused_gemm of this layer + shrink of `nxt` as extra tiles of the same launch
+        (tlora_forward_gemm_shrink); bit-identical to fused_gemm then nxt.shrink."""
+        call("tlora_forward_gemm_shrink", self._h, plan._h, _ptr(X), _ptr(H), _ptr(Y),
+             _DT[Y.dtype], nxt._h, next_plan._h, _ptr(X_next), _ptr(H_next), int(zero_next),
+             _stream_ptr(stream))
+
     def fused_gemm_rs(self, plan: Plan, X, H, recv_ptrs, rank, slot_rows, dst_row0, stream=None):
         """Row-parallel TP forward with the reduce-scatter fused into the epilogue (peer
         stores into every owner's receive slot); see tlora_forward_gemm_rs."""
@@ -224,6 +232,18 @@ class FusedLoRALayer:
     def dx(self, plan: Plan, dY, dH, dX, beta=0.0, stream=None):
         call("tlora_backward_dx", self._h, plan._h, _ptr(dY), _ptr(dH), _ptr(dX), C.c_float(beta),
              _stream_ptr(stream))
+
+    def dx_dh(self, plan: Plan, dY, dH, dX, nxt: "FusedLoRALayer", next_plan: Plan, dY_next,
+              dH_next, beta=0.0, zero_next=True, stream=None):
+        """dx of this layer + dh of `nxt` in one launch (tlora_backward_dx_dh)."""
+        call("tlora_backward_dx_dh", self._h, plan._h, _ptr(dY), _ptr(dH), _ptr(dX),
+             C.c_float(beta), nxt._h, next_plan._h, _ptr(dY_next), _ptr(dH_next),
+             int(zero_next), _stream_ptr(stream))
+
+    def grads(self, plan: Plan, H, dY, X, dH, beta=0.0, stream=None):
+        """dB and dA in one launch (tlora_backward_grads)."""
+        call("tlora_backward_grads", self._h, plan._h, _ptr(H), _ptr(dY), _ptr(X), _ptr(dH),
+             C.c_float(beta), _stream_ptr(stream))
 
     def grad_b(self, plan: Plan, H, dY, beta=0.0, stream=None):
         call("tlora_backward_grad_b", self._h, plan._h, _ptr(H), _ptr(dY), C.c_float(beta),

@@ -26,8 +26,12 @@ class LayerSetStep:
     """
 
     def __init__(self, wl: Workload, device: int = 0, seed: int | None = None,
-                 shuffle: bool = False, y_dtype=torch.bfloat16):
+                 shuffle: bool = False, y_dtype=torch.bfloat16, chain: bool = True):
         self.wl = wl
+        # chain: each projection's shrink (forward) / dH (backward) rides as extra tiles in
+        # the previous projection's fused GEMM launch (tlora_forward_gemm_shrink /
+        # tlora_backward_dx_dh) instead of its own launch; bit-identical either way.
+        self.chain = chain
         self.device = device
         dev = torch.device("cuda", device)
         self.dev = dev
@@ -60,18 +64,60 @@ class LayerSetStep:
                 self.Y[name] = torch.empty(T, k, dtype=y_dtype, device=dev)
                 self.dY[name] = torch.randn(T, k, generator=g, device=dev).bfloat16()
                 self.dX[name] = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
-            self.H[(L, name)] = torch.zeros(T, lay.R, dtype=torch.bfloat16, device=dev)
+        # H stashes: one zeroed arena; the masked low-rank launches only ever write each
+        # token's window columns (zeros outside its own slot), so the rest stays zero
+        R = self.layers[self.keys[0]].R  # packed rank width: same for every projection
+        self.H_arena = torch.zeros(len(self.keys), T, R, dtype=torch.bfloat16, device=dev)
+        for i, key in enumerate(self.keys):
+            self.H[key] = self.H_arena[i]
+        self.dH2 = torch.zeros(2, T, R, dtype=torch.bfloat16, device=dev)  # chained dH ping-pong
         torch.cuda.synchronize(dev)
 
     def x_of(self, name):
         return self.X[INPUT_GROUP.get(name, name)]
 
     def forward(self, stream=None):
+        if self.chain:
+            return self.forward_chained(stream)
         for L, name in self.keys:
             self.layers[(L, name)].forward(self.plans[name], self.x_of(name), self.Y[name],
                                            self.H[(L, name)], stream=stream)
 
+    def forward_chained(self, stream=None):
+        keys = self.keys
+        k0 = keys[0]
+        self.layers[k0].shrink(self.plans[k0[1]], self.x_of(k0[1]), self.H[k0], stream=stream)
+        for i, (L, name) in enumerate(keys):
+            lay, pl = self.layers[(L, name)], self.plans[name]
+            if i + 1 < len(keys):
+                nk = keys[i + 1]
+                lay.fused_gemm_shrink(pl, self.x_of(name), self.H[(L, name)], self.Y[name],
+                                      self.layers[nk], self.plans[nk[1]], self.x_of(nk[1]),
+                                      self.H[nk], zero_next=False, stream=stream)
+            else:
+                lay.fused_gemm(pl, self.x_of(name), self.H[(L, name)], self.Y[name], stream=stream)
+
+    def backward_chained(self, stream=None, beta: float = 0.0, on_layer_done=None):
+        keys = list(reversed(self.keys))
+        k0 = keys[0]
+        self.layers[k0].dh(self.plans[k0[1]], self.dY[k0[1]], self.dH2[0], stream=stream)
+        for i, (L, name) in enumerate(keys):
+            lay, pl = self.layers[(L, name)], self.plans[name]
+            dH = self.dH2[i % 2]
+            if i + 1 < len(keys):
+                nk = keys[i + 1]
+                lay.dx_dh(pl, self.dY[name], dH, self.dX[name], self.layers[nk], self.plans[nk[1]],
+                          self.dY[nk[1]], self.dH2[(i + 1) % 2], zero_next=False, stream=stream)
+            else:
+                lay.dx(pl, self.dY[name], dH, self.dX[name], stream=stream)
+            lay.grads(pl, self.H[(L, name)], self.dY[name], self.x_of(name), dH, beta=beta,
+                      stream=stream)
+            if on_layer_done is not None:
+                on_layer_done((L, name), lay)
+
     def backward(self, stream=None, beta: float = 0.0, on_layer_done=None):
+        if self.chain:
+            return self.backward_chained(stream, beta, on_layer_done)
         for L, name in reversed(self.keys):
             lay = self.layers[(L, name)]
             lay.backward(self.plans[name], self.dY[name], self.x_of(name), self.H[(L, name)],

@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(capi.SIGNATURES), set(syms) ^ set(capi.SIGNATURES)
-    assert lib.tlora_abi_version() == 1
+    assert lib.tlora_abi_version() == 2
 
 
 def test_op_cost_via_abi_matches_reference_golden():
@@ -96,7 +96,7 @@ def _plan_cases():
 @pytest.mark.parametrize("case", range(len(_plan_cases())))
 def test_plan_bit_identical_to_plan_oracle(case):
     d, k, ranks, slots = _plan_cases()[case]
-    for launch in range(6):
+    for launch in range(8):
         got = plan_tiles_host(d, k, ranks, slots, launch)
         want = O.plan_tiles(len(slots), d, k, ranks, slots, launch)
         assert got.shape == want.shape, (launch, got.shape, want.shape)
@@ -143,3 +143,19 @@ def test_shape_errors_are_status_codes():
     rk = (C.c_int32 * 1)(0)
     code = capi.lib().tlora_layer_create(0, 64, 64, 1, rk, C.byref(h))
     assert code == capi.ERR_SHAPE
+
+
+def test_profile_end_writes_exactly_prof_kinds_entries():
+    """tlora_profile_end fills TLORA_PROF_KINDS entries per array (launch kinds 6/7, the
+    secondary SHRINK2 / DH2 tiles, are booked under FWD / DX and have no slot)."""
+    kinds = int(re.search(r"#define TLORA_PROF_KINDS (\d+)",
+                          (ROOT / "include" / "tlora.h").read_text()).group(1))
+    assert kinds == 6
+    cnt = (C.c_int32 * (kinds + 2))(*([-7] * (kinds + 2)))
+    ms = (C.c_double * (kinds + 2))(*([-7.0] * (kinds + 2)))
+    fl = (C.c_double * (kinds + 2))(*([-7.0] * (kinds + 2)))
+    assert capi.lib().tlora_profile_begin() == 0
+    assert capi.lib().tlora_profile_end(cnt, ms, fl) == 0
+    assert list(cnt[:kinds]) == [0] * kinds and list(ms[:kinds]) == [0.0] * kinds
+    assert list(cnt[kinds:]) == [-7, -7] and list(ms[kinds:]) == [-7.0, -7.0]
+    assert list(fl[kinds:]) == [-7.0, -7.0]

@@ -332,7 +332,7 @@ def test_overlapped_schedule_is_bit_identical():
                   [Job("a", 8, 2, 256), Job("b", 64, 3, 256), Job("c", 16, 1, 256)], layers=2)
     out = []
     for overlap in (False, True):
-        st = LayerSetStep(wl, device=0, seed=5)
+        st = LayerSetStep(wl, device=0, seed=5, chain=False)
         main = torch.cuda.current_stream()
         if overlap:
             st.enable_overlap(16)
@@ -377,3 +377,81 @@ def test_cuda_graph_replay_matches_eager():
                     for k, lay in st.layers.items()})
     for k in res[0]:
         assert all(torch.equal(x, y) for x, y in zip(res[0][k], res[1][k])), k
+
+
+@pytest.mark.parametrize("tokens", [(256, 256, 256), (300, 77, 513)])
+def test_chained_lowrank_tiles_are_bit_identical(tokens):
+    """Chained schedule (next projection's shrink / dH as extra CTA-pair tiles of the fused
+    GEMM launch: tlora_forward_gemm_shrink / tlora_backward_dx_dh) vs one launch per op:
+    Y, dX, H stashes and adapter gradients bitwise equal, ragged token counts included."""
+    from paper_2602_07263_b200.runner import LayerSetStep
+    from paper_2602_07263_b200.workload import Job, Workload
+
+    wl = Workload("mini", [("q", 512, 768), ("k", 512, 256), ("o", 768, 512)],
+                  [Job("a", 8, 2, tokens[0]), Job("b", 200, 3, tokens[1]),
+                   Job("c", 16, 1, tokens[2])], layers=2)
+    out = []
+    for chain in (False, True):
+        st = LayerSetStep(wl, device=0, seed=7, chain=chain)
+        st.forward()
+        st.backward()
+        torch.cuda.synchronize()
+        out.append({"Y": {k: v.clone() for k, v in st.Y.items()},
+                    "dX": {k: v.clone() for k, v in st.dX.items()},
+                    "H": {k: v.clone() for k, v in st.H.items()},
+                    "g": {k: [t.clone() for t in lay.packed_grads()] for k, lay in st.layers.items()}})
+    a, b = out
+    for k in a["Y"]:
+        assert torch.equal(a["Y"][k], b["Y"][k]) and torch.equal(a["dX"][k], b["dX"][k]), k
+    for k in a["H"]:
+        assert torch.equal(a["H"][k], b["H"][k]), k
+    for k in a["g"]:
+        assert all(torch.equal(x, y) for x, y in zip(a["g"][k], b["g"][k])), k
+
+
+def test_gemm_shrink_zero_next_clears_garbage():
+    """tlora_forward_gemm_shrink / tlora_backward_dx_dh with zero_next=1 on a garbage-filled
+    output equal the standalone shrink / dH (which memset) bitwise, and the fused GEMM part
+    equals tlora_forward_gemm / tlora_backward_dx."""
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(11)
+    ranks = [8, 64, 24, 128]
+    d0, k0, d1, k1 = 640, 384, 384, 1152
+    lays = []
+    for d, k in ((d0, k0), (d1, k1)):
+        lay = FusedLoRALayer(d, k, ranks)
+        lay.set_base((torch.randn(d, k, generator=g, device=dev) * d ** -0.5).bfloat16())
+        for s_, r in enumerate(ranks):
+            lay.set_adapter(s_, (torch.randn(d, r, generator=g, device=dev) * 0.05).bfloat16(),
+                            (torch.randn(r, k, generator=g, device=dev) * 0.05).bfloat16())
+        lays.append(lay)
+    slots = np.random.default_rng(3).integers(0, 4, 700).astype(np.int32)
+    T = len(slots)
+    p0, p1 = lays[0].plan(slots), lays[1].plan(np.sort(slots))
+    R = lays[0].R
+    X0 = torch.randn(T, d0, generator=g, device=dev).bfloat16()
+    X1 = torch.randn(T, d1, generator=g, device=dev).bfloat16()
+    H0 = torch.empty(T, R, dtype=torch.bfloat16, device=dev)
+    lays[0].shrink(p0, X0, H0)
+    Ya, Yb = (torch.empty(T, k0, dtype=torch.bfloat16, device=dev) for _ in range(2))
+    Ha = torch.empty(T, R, dtype=torch.bfloat16, device=dev)
+    Hb = torch.full((T, R), 7.0, dtype=torch.bfloat16, device=dev)
+    lays[0].fused_gemm(p0, X0, H0, Ya)
+    lays[1].shrink(p1, X1, Ha)
+    lays[0].fused_gemm_shrink(p0, X0, H0, Yb, lays[1], p1, X1, Hb, zero_next=True)
+    torch.cuda.synchronize()
+    assert torch.equal(Ya, Yb) and torch.equal(Ha, Hb)
+    dY0 = torch.randn(T, k0, generator=g, device=dev).bfloat16()
+    dY1 = torch.randn(T, k1, generator=g, device=dev).bfloat16()
+    dH0 = torch.empty(T, R, dtype=torch.bfloat16, device=dev)
+    lays[0].dh(p0, dY0, dH0)
+    dXa, dXb = (torch.empty(T, d0, dtype=torch.bfloat16, device=dev) for _ in range(2))
+    dHa = torch.empty(T, R, dtype=torch.bfloat16, device=dev)
+    dHb = torch.full((T, R), -3.0, dtype=torch.bfloat16, device=dev)
+    lays[0].dx(p0, dY0, dH0, dXa)
+    lays[1].dh(p1, dY1, dHa)
+    lays[0].dx_dh(p0, dY0, dH0, dXb, lays[1], p1, dY1, dHb, zero_next=True)
+    torch.cuda.synchronize()
+    assert torch.equal(dXa, dXb) and torch.equal(dHa, dHb)
+    for lay in lays:
+        lay.close()
