@@ -290,55 +290,109 @@ __global__ void pack_adapter_kernel(const void* A, const void* B, int dtype, int
   }
 }
 
-// Fused multi-job AdamW over one packed adapter matrix P (R x N, fp32 master) with its
+// Fused multi-job AdamW over a layer's packed adapters P (R x N, fp32 master) with
 // gradient G and moments; per-row job hyperparameters via row_slot -> hp[slot]. Writes the
-// bf16 operand copies in both layouts the kernels read: P16 (R x N) and P16t (N x R,
-// through a shared-memory transpose). Padding-gap rows stay exactly zero. HBM-bound:
-// 16 B read + 12 B written (fp32) + 4 B (bf16 x2) per parameter.
-__global__ void adamw_packed_kernel(const float* __restrict__ G, float* __restrict__ P,
-                                    float* __restrict__ Mo, float* __restrict__ Vo,
-                                    __nv_bfloat16* __restrict__ P16,
-                                    __nv_bfloat16* __restrict__ P16t,
-                                    const int32_t* __restrict__ row_slot,
-                                    const float2* __restrict__ hp,
-                                    const int32_t* __restrict__ steps, float b1, float b2,
-                                    float eps, float grad_scale, int64_t R, int64_t N) {
-  __shared__ float tile[32][33];
-  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int64_t r = r0 + i, c = c0 + threadIdx.x;
-    float val = 0.f;
+// bf16 operand copies in both layouts the kernels read: P16 (R x N) and P16t (N x R).
+// Padding-gap rows stay exactly zero. HBM-bound: 16 B read + 12 B written (fp32) + 4 B
+// (bf16 x2) per parameter.
+// One launch updates both packed matrices of a layer (job[0] = Aᵀcat R x d, job[1] = Bcat
+// R x k). Block = 32 packed rows x 64 columns; each thread moves float4s (4 consecutive
+// columns) of G, P, M, V and writes P16 as 4 x bf16; the tile goes through shared memory
+// for the transposed bf16 copy (64 B runs of P16t per column). Job hyperparameters and bias
+// corrections are per ROW (slot), computed once per row, not per element. The last block to
+// finish (atomic ticket) bumps the per-slot step counters and resets the ticket, so the
+// launch is self-contained and graph-replayable.
+struct AdamJob {
+  const float* G;
+  float* P;
+  float* M;
+  float* V;
+  __nv_bfloat16* P16;
+  __nv_bfloat16* P16t;
+  int64_t N;
+  int32_t blocks_x;
+  int32_t nblocks;
+};
+
+__global__ void __launch_bounds__(256) adamw_layer_kernel(
+    const AdamJob j0, const AdamJob j1, const int32_t* __restrict__ row_slot,
+    const float2* __restrict__ hp, int32_t* __restrict__ steps, int32_t num_slots, float b1,
+    float b2, float eps, float grad_scale, int64_t R) {
+  __shared__ float tile[32][65];
+  __shared__ bool last;
+  const bool second = (int)blockIdx.x >= j0.nblocks;
+  const AdamJob& J = second ? j1 : j0;
+  const int b = second ? (int)blockIdx.x - j0.nblocks : (int)blockIdx.x;
+  const int64_t r0 = (int64_t)(b / J.blocks_x) * 32, c0 = (int64_t)(b % J.blocks_x) * 64;
+  const int tid = threadIdx.x;
+  const int N = (int)J.N;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int i = it * 16 + tid / 16, cq = (tid % 16) * 4;
+    const int64_t r = r0 + i, c = c0 + cq;
+    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
     if (r < R && c < N) {
-      const int s = row_slot[r];
-      if (s >= 0) {
-        const int64_t idx = r * N + c;
-        const float2 h = hp[s];  // lr, wd
-        const float t = (float)(steps[s] + 1);
+      const int sl = row_slot[r];
+      const int64_t idx = r * N + c;
+      if (sl >= 0) {
+        const float2 h = hp[sl];  // lr, wd
+        const float t = (float)(steps[sl] + 1);
         const float c1 = 1.f / (1.f - powf(b1, t)), c2 = 1.f / (1.f - powf(b2, t));
-        const float g = G[idx] * grad_scale;
-        float p = P[idx];
-        const float m = b1 * Mo[idx] + (1.f - b1) * g;
-        const float v = b2 * Vo[idx] + (1.f - b2) * g * g;
-        p -= h.x * (m * c1 / (sqrtf(v * c2) + eps) + h.y * p);
-        P[idx] = p;
-        Mo[idx] = m;
-        Vo[idx] = v;
-        val = p;
+        const float4 g4 = *reinterpret_cast<const float4*>(J.G + idx);
+        float4 p4 = *reinterpret_cast<const float4*>(J.P + idx);
+        float4 m4 = *reinterpret_cast<const float4*>(J.M + idx);
+        float4 v4 = *reinterpret_cast<const float4*>(J.V + idx);
+        const float* gp = &g4.x;
+        float* pp = &p4.x;
+        float* mp = &m4.x;
+        float* vp = &v4.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float g = gp[q] * grad_scale;
+          float p = pp[q];
+          const float m = b1 * mp[q] + (1.f - b1) * g;
+          const float v = b2 * vp[q] + (1.f - b2) * g * g;
+          p -= h.x * (m * c1 / (sqrtf(v * c2) + eps) + h.y * p);
+          pp[q] = p;
+          mp[q] = m;
+          vp[q] = v;
+        }
+        *reinterpret_cast<float4*>(J.P + idx) = p4;
+        *reinterpret_cast<float4*>(J.M + idx) = m4;
+        *reinterpret_cast<float4*>(J.V + idx) = v4;
+        val = p4;
       }
-      P16[r * N + c] = __float2bfloat16_rn(val);
+      uint2 w;
+      w.x = tlora::ptx::pack_bf16x2(val.x, val.y);
+      w.y = tlora::ptx::pack_bf16x2(val.z, val.w);
+      *reinterpret_cast<uint2*>(J.P16 + idx) = w;
     }
-    tile[i][threadIdx.x] = val;
+    tile[i][cq + 0] = val.x;
+    tile[i][cq + 1] = val.y;
+    tile[i][cq + 2] = val.z;
+    tile[i][cq + 3] = val.w;
   }
   __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int64_t c = c0 + i, r = r0 + threadIdx.x;
-    if (r < R && c < N) P16t[c * R + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int cc = it * 16 + tid / 16, rr = (tid % 16) * 2;
+    const int64_t c = c0 + cc, r = r0 + rr;
+    if (c < N && r < R)  // R % 8 == 0: r + 1 < R too
+      *reinterpret_cast<uint32_t*>(J.P16t + c * R + r) =
+          tlora::ptx::pack_bf16x2(tile[rr][cc], tile[rr + 1][cc]);
   }
-}
-
-__global__ void bump_steps_kernel(int32_t* steps, int n) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) steps[i] += 1;
+  // ticket: every block has read steps[] before it arrives; the last one bumps them
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const int t = atomicAdd(steps + num_slots, 1);
+    last = t == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    for (int sl = tid; sl < num_slots; sl += blockDim.x) steps[sl] += 1;
+    if (tid == 0) steps[num_slots] = 0;
+  }
 }
 
 // out[r][c] = sum_{p < world} recv[p][row0 + r][c]: fixed-order (deterministic) sum of the
@@ -849,13 +903,13 @@ int tlora_layer_set_optimizer(tlora_layer* layer, const float* lr, const float* 
       layer->mB.alloc(R * k);
       layer->vB.alloc(R * k);
       layer->hparams.alloc(S);
-      layer->steps_dev.alloc(S);
+      layer->steps_dev.alloc(S + 1);  // + the optimizer launch's completion ticket
     }
     TL_CUDA(cudaMemset(layer->mA.p, 0, R * d * 4));
     TL_CUDA(cudaMemset(layer->vA.p, 0, R * d * 4));
     TL_CUDA(cudaMemset(layer->mB.p, 0, R * k * 4));
     TL_CUDA(cudaMemset(layer->vB.p, 0, R * k * 4));
-    TL_CUDA(cudaMemset(layer->steps_dev.p, 0, S * 4));
+    TL_CUDA(cudaMemset(layer->steps_dev.p, 0, (S + 1) * 4));
     std::vector<float2> hp(S);
     for (int i = 0; i < S; ++i) hp[i] = make_float2(layer->lr[i], layer->wd[i]);
     TL_CUDA(cudaMemcpy(layer->hparams.p, hp.data(), S * sizeof(float2), cudaMemcpyHostToDevice));
@@ -871,22 +925,25 @@ int tlora_layer_optimizer_step(tlora_layer* layer, float grad_scale, void* strea
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int S = (int)layer->L.rank.size();
     const int64_t R = layer->L.R, d = layer->L.d, k = layer->L.k;
-    const dim3 block(32, 8);  // enqueue-only, no host data: capturable in a CUDA graph
-    adamw_packed_kernel<<<dim3((unsigned)tlora::ceil_div(d, 32), (unsigned)tlora::ceil_div(R, 32)),
-                          block, 0, s>>>(layer->dAT.p, layer->ATm.p, layer->mA.p, layer->vA.p,
-                                         layer->AT.p, layer->Acat.p, layer->row_slot.p,
-                                         layer->hparams.p, layer->steps_dev.p, layer->beta1,
-                                         layer->beta2, layer->eps, grad_scale, R, d);
+    // enqueue-only, no host data: capturable in a CUDA graph
+    AdamJob job[2];
+    const int64_t Ns[2] = {d, k};
+    float* G[2] = {layer->dAT.p, layer->dB.p};
+    float* P[2] = {layer->ATm.p, layer->Bm.p};
+    float* M[2] = {layer->mA.p, layer->mB.p};
+    float* V[2] = {layer->vA.p, layer->vB.p};
+    __nv_bfloat16* P16[2] = {layer->AT.p, layer->Bcat.p};
+    __nv_bfloat16* P16t[2] = {layer->Acat.p, layer->BcatT.p};
+    for (int j = 0; j < 2; ++j) {
+      const int bx = (int)tlora::ceil_div(Ns[j], 64);
+      job[j] = {G[j], P[j], M[j], V[j], P16[j], P16t[j], Ns[j], bx,
+                bx * (int)tlora::ceil_div(R, 32)};
+    }
+    adamw_layer_kernel<<<job[0].nblocks + job[1].nblocks, 256, 0, s>>>(
+        job[0], job[1], layer->row_slot.p, layer->hparams.p, layer->steps_dev.p, S,
+        layer->beta1, layer->beta2, layer->eps, grad_scale, R);
     TL_CUDA(cudaGetLastError());
-    adamw_packed_kernel<<<dim3((unsigned)tlora::ceil_div(k, 32), (unsigned)tlora::ceil_div(R, 32)),
-                          block, 0, s>>>(layer->dB.p, layer->Bm.p, layer->mB.p, layer->vB.p,
-                                         layer->Bcat.p, layer->BcatT.p, layer->row_slot.p,
-                                         layer->hparams.p, layer->steps_dev.p, layer->beta1,
-                                         layer->beta2, layer->eps, grad_scale, R, k);
-    TL_CUDA(cudaGetLastError());
-    bump_steps_kernel<<<(S + 127) / 128, 128, 0, s>>>(layer->steps_dev.p, S);
-    TL_CUDA(cudaGetLastError());
-    g_launches.fetch_add(3, std::memory_order_relaxed);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
   });
 }
 

@@ -16,6 +16,11 @@ from paper_2602_07263_b200.workload import config  # noqa: E402
 def main():
     proj = sys.argv[1] if len(sys.argv) > 1 else "q"
     wl = config("C2")
+    if proj == "all":
+        for p in wl.projections:
+            sys.argv[1:] = [p[0]]
+            main()
+        return
     name, d, k = [p for p in wl.projections if p[0] == proj][0]
     g = torch.Generator(device="cuda").manual_seed(0)
     lay = FusedLoRALayer(d, k, wl.ranks)
@@ -39,7 +44,11 @@ def main():
         "dX": (lambda: lay.dx(plan, dY, dH, dX), 2.0 * T * d * k + 2.0 * rt * d, "TF/s"),
         "dB": (lambda: lay.grad_b(plan, H, dY), 2 * (T * k + T * lay.R) + 4 * lay.R * k, "GB/s"),
         "dA": (lambda: lay.grad_a(plan, X, dH), 2 * (T * d + T * lay.R) + 4 * lay.R * d, "GB/s"),
+        "dB+dA": (lambda: lay.grads(plan, H, dY, X, dH),
+                  2 * (T * (d + k) + 2 * T * lay.R) + 4 * lay.R * (d + k), "GB/s"),
+        "adamw": (lambda: lay.optimizer_step(), 32 * lay.R * (d + k), "GB/s"),
     }
+    lay.set_optimizer(1e-4)
     lay.shrink(plan, X, H)
     lay.dh(plan, dY, dH)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
