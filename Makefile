@@ -21,7 +21,7 @@ $(CPPTEST): tests/cpp/test_dropin.cpp include/lora_fleet/*.hpp include/tlora.h $
 	$(CXX) -std=c++20 -O2 -Iinclude -DLORA_FLEET_WITH_TEST_ORACLE -o $@ tests/cpp/test_dropin.cpp \
 	  -L$(PKG) -ltlora -Wl,-rpath,'$$ORIGIN/../../../$(PKG)'
 
-$(LIB): $(CSRC)/tlora_capi.cu $(CSRC)/lora_gemm.cuh $(CSRC)/sm100_ptx.cuh $(CSRC)/tlora_plan.hpp include/tlora.h
+$(LIB): $(CSRC)/tlora_capi.cu $(CSRC)/tlora_comm.cuh $(CSRC)/lora_gemm2.cuh $(CSRC)/lora_grad.cuh $(CSRC)/lora_gemm.cuh $(CSRC)/sm100_ptx.cuh $(CSRC)/tlora_plan.hpp include/tlora.h
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(CSRC)/tlora_capi.cu 2> build_ptxas.log || (cat build_ptxas.log; false)
 
 $(ORACLE): oracle/tlora_oracle.c oracle/tlora_oracle.h

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define TLORA_ABI_VERSION 2
+#define TLORA_ABI_VERSION 3
 
 enum tlora_status {
   TLORA_OK = 0,
@@ -36,7 +36,8 @@ enum tlora_status {
   TLORA_ERR_REGISTRY = 3,  /* unknown / unregistered adapter slot (":73 has no adapter") */
   TLORA_ERR_PLAN = 4,      /* invalid plan / partition / AIMD arguments                  */
   TLORA_ERR_CUDA = 5,      /* CUDA runtime / driver failure                              */
-  TLORA_ERR_NO_DEVICE = 6  /* no sm_100 device available: there is no CPU fallback      */
+  TLORA_ERR_NO_DEVICE = 6, /* no sm_100 device available: there is no CPU fallback      */
+  TLORA_ERR_NCCL = 7       /* NCCL missing or a collective failed                        */
 };
 
 enum tlora_dtype { TLORA_F64 = 0, TLORA_F32 = 1, TLORA_BF16 = 2 };
@@ -44,6 +45,7 @@ enum tlora_where { TLORA_HOST = 0, TLORA_DEVICE = 1 };
 
 typedef struct tlora_layer tlora_layer;
 typedef struct tlora_plan tlora_plan;
+typedef struct tlora_comm tlora_comm;
 
 /* One output tile of a plan launch and its (up to two) K-segments, in elements.
  * Mirrors tlora::TileDesc in paper_2602_07263_b200/csrc/lora_gemm.cuh. */
@@ -250,6 +252,34 @@ int tlora_partition(int32_t group_batch, int32_t n, int32_t* n_out, int32_t* per
 /* has_prev/t_prev carry std::optional<double>; updates n / has_prev / t_prev in place. */
 int tlora_aimd_step(int32_t* n, int32_t* has_prev, double* t_prev, int32_t alpha, double beta,
                     double tau_rel, double t_t);
+
+/* ---- communicator (SURVEY §8(b) "comm"; no reference counterpart: the reference
+ * simulates its multi-GPU timeline, sim_engine.hpp:306-315) ------------------------------
+ * One communicator per rank over NCCL (loaded at run time; TLORA_ERR_NCCL if absent).
+ * world = tp_size * dp; rank = dp_index * tp_size + tp_index. Groups: WORLD, TP (the
+ * tp_size consecutive ranks of one replica) and DP (ranks with the same tp_index).
+ * Rank 0 makes the id, the host shares it out of band, every rank calls create
+ * (collective). Collectives are enqueued on `stream`. */
+#define TLORA_UNIQUE_ID_BYTES 128
+enum tlora_group { TLORA_GROUP_WORLD = 0, TLORA_GROUP_TP = 1, TLORA_GROUP_DP = 2 };
+int tlora_comm_get_unique_id(uint8_t* id /* [TLORA_UNIQUE_ID_BYTES] */);
+int tlora_comm_create(int device, const uint8_t* id, int32_t world, int32_t rank,
+                      int32_t tp_size, tlora_comm** out);
+int tlora_comm_destroy(tlora_comm* comm);
+int tlora_comm_info(const tlora_comm* comm, int32_t* world, int32_t* rank, int32_t* tp_size,
+                    int32_t* dp_size);
+/* recv = concat over the group's ranks of send (send_count elements each) */
+int tlora_comm_all_gather(tlora_comm* comm, int group, const void* send, void* recv,
+                          size_t send_count, int dtype, void* stream);
+/* recv (recv_count elements) = this rank's slice of the sum over the group of send */
+int tlora_comm_reduce_scatter(tlora_comm* comm, int group, const void* send, void* recv,
+                              size_t recv_count, int dtype, void* stream);
+int tlora_comm_all_reduce(tlora_comm* comm, int group, const void* send, void* recv,
+                          size_t count, int dtype, int average, void* stream);
+/* Data-parallel exchange: all-reduce (sum, or mean if average) of the layer's fp32
+ * adapter gradients dA / dB over `group` (normally TLORA_GROUP_DP), in place. */
+int tlora_layer_allreduce_grads(tlora_layer* layer, tlora_comm* comm, int group, int average,
+                                void* stream);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,9 @@ from pathlib import Path
 _PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("TLORA_LIB", _PKG_DIR / "libtlora.so"))
 
-OK, ERR_ARG, ERR_SHAPE, ERR_REGISTRY, ERR_PLAN, ERR_CUDA, ERR_NO_DEVICE = range(7)
+OK, ERR_ARG, ERR_SHAPE, ERR_REGISTRY, ERR_PLAN, ERR_CUDA, ERR_NO_DEVICE, ERR_NCCL = range(8)
+GROUP_WORLD, GROUP_TP, GROUP_DP = range(3)
+UNIQUE_ID_BYTES = 128
 F64, F32, BF16 = 0, 1, 2
 HOST, DEVICE = 0, 1
 L_SHRINK, L_FWD, L_DH, L_DX, L_DB, L_DA, L_SHRINK2, L_DH2 = range(8)
@@ -98,6 +100,19 @@ SIGNATURES = {
                                     C.c_float, C.c_void_p]),
     "tlora_backward_dx_dh": (C.c_int, [C.c_void_p] * 5 + [C.c_float] + [C.c_void_p] * 4
                              + [C.c_int, C.c_void_p]),
+    "tlora_comm_get_unique_id": (C.c_int, [C.c_void_p]),
+    "tlora_comm_create": (C.c_int, [C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                    C.POINTER(C.c_void_p)]),
+    "tlora_comm_destroy": (C.c_int, [C.c_void_p]),
+    "tlora_comm_info": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_int32)] * 4),
+    "tlora_comm_all_gather": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t,
+                                        C.c_int, C.c_void_p]),
+    "tlora_comm_reduce_scatter": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                            C.c_size_t, C.c_int, C.c_void_p]),
+    "tlora_comm_all_reduce": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t,
+                                        C.c_int, C.c_int, C.c_void_p]),
+    "tlora_layer_allreduce_grads": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                              C.c_void_p]),
     "tlora_backward_grads": (C.c_int, [C.c_void_p] * 6 + [C.c_float, C.c_void_p]),
     "tlora_backward_grad_b": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.c_float, C.c_void_p]),

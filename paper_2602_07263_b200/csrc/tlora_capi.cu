@@ -1629,3 +1629,5 @@ int tlora_aimd_step(int32_t* n, int32_t* has_prev, double* t_prev, int32_t alpha
 }
 
 }  // extern "C"
+
+#include "tlora_comm.cuh"

@@ -17,6 +17,7 @@
 #include <string>
 #include <vector>
 
+#include "lora_fleet/comm.hpp"
 #include "lora_fleet/fused_lora.hpp"
 #include "lora_fleet/nano_pipeline.hpp"
 #include "lora_fleet/ssm_plan.hpp"
@@ -167,6 +168,14 @@ void cpu_costs() {  // test_fused_lora.cpp:115-136
   CHECK(trainable_param_count(job) == 4LL * (64 + 64) * 4);
 }
 
+void cpu_comm_arguments() {  // communicator handle: argument errors surface as exceptions
+  lora_fleet::Communicator::Id id{};
+  CHECK(throws_with<std::runtime_error>([&] { lora_fleet::Communicator c(0, id, 4, 0, 3); },
+                                        "tp_size"));
+  CHECK(throws_with<std::runtime_error>([&] { lora_fleet::Communicator c(0, id, 2, 5, 1); },
+                                        "rank"));
+}
+
 void cpu_nano_and_fuse() {  // test_nano_pipeline.cpp:28-38, 90-123; test_ssm_plan.cpp:62-78
   auto s = partition(10, 4);
   CHECK(s.n == 4);
@@ -300,6 +309,7 @@ int main(int argc, char** argv) {
     cases.push_back({"shape errors name the offending segment", cpu_shape_errors});
     cases.push_back({"fused cost dominates unfused; param/flop counts", cpu_costs});
     cases.push_back({"partition / aimd_step / fuse", cpu_nano_and_fuse});
+    cases.push_back({"communicator argument errors", cpu_comm_arguments});
   }
   if (mode == "gpu" || mode == "all") {
     cases.push_back({"fused_forward matches the materialized oracle", gpu_matches_oracle});
