@@ -119,6 +119,16 @@ inline std::vector<double> padded(const Matrix& m, Index rows, Index cols) {
   return v;
 }
 
+// Row-major, zero-padded copy with rows gathered through perm: out row i = m.row(perm[i]).
+inline std::vector<double> padded_rows(const Matrix& m, const std::vector<int64_t>& perm,
+                                       Index cols) {
+  std::vector<double> v(perm.size() * static_cast<size_t>(cols), 0.0);
+  for (size_t i = 0; i < perm.size(); ++i)
+    for (Index j = 0; j < m.cols(); ++j)
+      v[i * static_cast<size_t>(cols) + static_cast<size_t>(j)] = m(static_cast<Index>(perm[i]), j);
+  return v;
+}
+
 // RAII device buffer through the C-ABI.
 struct DeviceBuffer {
   int dev = 0;
@@ -130,7 +140,11 @@ struct DeviceBuffer {
 };
 
 // One fused layer built from the reference-style inputs: registry (slots in std::map
-// order), padded bf16 device copies, and the plan of this batch.
+// order), padded bf16 device copies, and the plan of this batch. The batch is laid out on
+// the device job-sorted (tlora_segments: the CSR form of segment_rows for every job, rows
+// ascending within a job), gathered during the host-side conversion at no extra cost, so
+// arbitrarily interleaved segment maps (test_fused_lora.cpp:45-46) run as job-contiguous
+// tiles; results are scattered back to the caller's row order.
 class DeviceLayer {
  public:
   DeviceLayer(const TokenBatch& batch, const Matrix& W,
@@ -161,10 +175,16 @@ class DeviceLayer {
     tl_check(tlora_layer_layout(layer_, nullptr, &R_));
     std::vector<int32_t> slots(static_cast<size_t>(T_));
     for (Index t = 0; t < T_; ++t) slots[static_cast<size_t>(t)] = slot_of[batch.segment_map[t]];
-    tl_check(tlora_plan_create(layer_, T_, slots.data(), &plan_));
+    perm_.resize(static_cast<size_t>(T_));
+    std::vector<int64_t> offsets(ranks.size() + 1);
+    tl_check(tlora_segments(T_, slots.data(), static_cast<int32_t>(ranks.size()), perm_.data(),
+                            offsets.data()));
+    std::vector<int32_t> sorted(static_cast<size_t>(T_));
+    for (size_t i = 0; i < perm_.size(); ++i) sorted[i] = slots[static_cast<size_t>(perm_[i])];
+    tl_check(tlora_plan_create(layer_, T_, sorted.data(), &plan_));
     X_ = std::make_unique<DeviceBuffer>(dev_, static_cast<size_t>(T_ * dp_ * 2));
     H_ = std::make_unique<DeviceBuffer>(dev_, static_cast<size_t>(T_ * R_ * 2));
-    const auto xp = padded(batch.rows, T_, dp_);
+    const auto xp = padded_rows(batch.rows, perm_, dp_);
     tl_check(tlora_copy_to_device(X_->p, TLORA_BF16, xp.data(), TLORA_F64, T_ * dp_, nullptr));
   }
   ~DeviceLayer() {
@@ -178,23 +198,25 @@ class DeviceLayer {
     std::vector<double> y(static_cast<size_t>(T_ * kp_));
     tl_check(tlora_copy_to_host(y.data(), TLORA_F64, Y.p, TLORA_F32, T_ * kp_, nullptr));
     Matrix out(T_, k_);
-    for (Index t = 0; t < T_; ++t)
-      for (Index j = 0; j < k_; ++j) out(t, j) = y[static_cast<size_t>(t * kp_ + j)];
+    for (Index i = 0; i < T_; ++i)
+      for (Index j = 0; j < k_; ++j)
+        out(static_cast<Index>(perm_[static_cast<size_t>(i)]), j) = y[static_cast<size_t>(i * kp_ + j)];
     return out;
   }
 
   FusedGradients backward(const Matrix& dY) {
     DeviceBuffer g(dev_, static_cast<size_t>(T_ * kp_ * 2));
     DeviceBuffer dX(dev_, static_cast<size_t>(T_ * dp_ * 2));
-    const auto gp = padded(dY, T_, kp_);
+    const auto gp = padded_rows(dY, perm_, kp_);
     tl_check(tlora_copy_to_device(g.p, TLORA_BF16, gp.data(), TLORA_F64, T_ * kp_, nullptr));
     tl_check(tlora_backward(layer_, plan_, g.p, X_->p, H_->p, dX.p, 0.0f, nullptr));
     FusedGradients out;
     std::vector<double> dx(static_cast<size_t>(T_ * dp_));
     tl_check(tlora_copy_to_host(dx.data(), TLORA_F64, dX.p, TLORA_BF16, T_ * dp_, nullptr));
     out.dX = Matrix(T_, d_);
-    for (Index t = 0; t < T_; ++t)
-      for (Index j = 0; j < d_; ++j) out.dX(t, j) = dx[static_cast<size_t>(t * dp_ + j)];
+    for (Index i = 0; i < T_; ++i)
+      for (Index j = 0; j < d_; ++j)
+        out.dX(static_cast<Index>(perm_[static_cast<size_t>(i)]), j) = dx[static_cast<size_t>(i * dp_ + j)];
     for (size_t s = 0; s < ids_.size(); ++s) {
       const auto& id = ids_[s];
       const Index r = rank_of(s);
@@ -224,6 +246,7 @@ class DeviceLayer {
   tlora_plan* plan_ = nullptr;
   std::vector<std::string> ids_;
   std::vector<Index> ranks_;
+  std::vector<int64_t> perm_;  // device row i holds the caller's token perm_[i]
   std::unique_ptr<DeviceBuffer> X_, H_;
 };
 

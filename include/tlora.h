@@ -246,6 +246,15 @@ int tlora_op_cost(int64_t tokens, int64_t d, int64_t k, int32_t num_slots,
                   const int64_t* tokens_per_slot, const int32_t* ranks, int fused,
                   double* flops, double* bytes_moved, long long* kernel_launches);
 
+/* ---- job segments (fused_lora.hpp:56-61 detail::segment_rows, for every job at once) -- */
+/* CSR form of the ragged batch: offsets[s] .. offsets[s+1] index into perm the rows owned
+ * by slot s, ascending within a slot (= segment_rows of that job); perm is therefore the
+ * stable job-sorted permutation (device row i <- token perm[i]). Host-only, O(T + S).
+ * perm: tokens entries; offsets: num_slots + 1 entries. Slots outside [0, num_slots)
+ * -> TLORA_ERR_REGISTRY. */
+int tlora_segments(int64_t tokens, const int32_t* token_slot, int32_t num_slots, int64_t* perm,
+                   int64_t* offsets);
+
 /* ---- nano-batch plan + AIMD (nano_pipeline.hpp:51-60, 99-112) --------------------- */
 /* per_nano must hold min(n, group_batch) entries; *n_out receives the clamped N. */
 int tlora_partition(int32_t group_batch, int32_t n, int32_t* n_out, int32_t* per_nano);

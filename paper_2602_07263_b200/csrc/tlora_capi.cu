@@ -1593,6 +1593,26 @@ int tlora_op_cost(int64_t tokens, int64_t d, int64_t k, int32_t num_slots,
   });
 }
 
+int tlora_segments(int64_t tokens, const int32_t* token_slot, int32_t num_slots, int64_t* perm,
+                   int64_t* offsets) {
+  return guarded([&] {
+    require(tokens >= 0 && num_slots >= 1, TLORA_ERR_ARG, "bad sizes");
+    require(tokens == 0 || (token_slot && perm), TLORA_ERR_ARG, "null argument");
+    require(offsets != nullptr, TLORA_ERR_ARG, "offsets is null");
+    std::vector<int64_t> cnt(num_slots + 1, 0);  // counting sort: stable, rows ascending
+    for (int64_t t = 0; t < tokens; ++t) {
+      const int32_t s = token_slot[t];
+      require(s >= 0 && s < num_slots, TLORA_ERR_REGISTRY,
+              "token " + std::to_string(t) + " names slot " + std::to_string(s) +
+                  " outside the registry");
+      ++cnt[s + 1];
+    }
+    for (int32_t s = 0; s < num_slots; ++s) cnt[s + 1] += cnt[s];
+    std::memcpy(offsets, cnt.data(), (num_slots + 1) * sizeof(int64_t));
+    for (int64_t t = 0; t < tokens; ++t) perm[cnt[token_slot[t]]++] = t;
+  });
+}
+
 int tlora_partition(int32_t group_batch, int32_t n, int32_t* n_out, int32_t* per_nano) {
   return guarded([&] {
     // nano_pipeline.hpp:51-60

@@ -296,6 +296,17 @@ def op_cost(tokens: int, d: int, k: int, tokens_per_slot, ranks, fused: bool = T
     return f.value, b.value, l.value
 
 
+def segments(token_slot, num_slots: int):
+    """Job-sorted permutation + CSR offsets (tlora_segments; fused_lora.hpp:56-61
+    segment_rows for every job at once): perm[offsets[s]:offsets[s+1]] = rows of slot s."""
+    slots = np.ascontiguousarray(token_slot, dtype=np.int32)
+    perm = np.empty(slots.shape[0], np.int64)
+    offsets = np.empty(num_slots + 1, np.int64)
+    call("tlora_segments", slots.shape[0], slots.ctypes.data, int(num_slots), perm.ctypes.data,
+         offsets.ctypes.data)
+    return perm, offsets
+
+
 def partition(group_batch: int, n: int):
     """nano_pipeline.hpp:51-60 — returns (n, per_nano_samples)."""
     out_n = C.c_int32()

@@ -159,3 +159,26 @@ def test_profile_end_writes_exactly_prof_kinds_entries():
     assert list(cnt[:kinds]) == [0] * kinds and list(ms[:kinds]) == [0.0] * kinds
     assert list(cnt[kinds:]) == [-7, -7] and list(ms[kinds:]) == [-7.0, -7.0]
     assert list(fl[kinds:]) == [-7.0, -7.0]
+
+
+def test_segments_match_reference_segment_rows():
+    """tlora_segments == detail::segment_rows (fused_lora.hpp:56-61: ascending rows whose
+    segment_map entry is the job id) for every job, on the reference's own golden batches
+    (shuffled segment maps, test_fused_lora.cpp:45-46) — bit-exact index lists."""
+    from paper_2602_07263_b200.layer import segments
+    n = 0
+    for name in ("fused_2024.bin", "fused_101.bin"):
+        for inst in read_records((ROOT / "tests" / "golden" / name).read_bytes()):
+            order = inst.slot_order()
+            slot_of_adapter = {a: s for s, a in enumerate(order)}
+            ids = [inst.job_ids[a] for a in order]
+            owner_ids = [inst.job_ids[a] for a in inst.owner]
+            slots = np.array([slot_of_adapter[order[ids.index(j)]] for j in owner_ids], np.int32)
+            perm, off = segments(slots, len(order))
+            for s, jid in enumerate(ids):
+                ref_rows = [t for t, j in enumerate(owner_ids) if j == jid]  # segment_rows
+                assert perm[off[s]:off[s + 1]].tolist() == ref_rows
+            n += 1
+    assert n > 0
+    with pytest.raises(capi.TloraError):
+        segments(np.array([0, 3], np.int32), 2)
