@@ -129,7 +129,14 @@ __device__ __forceinline__ void epi_store32(const GemmArgs& args, int split, int
         w.y = pack_bf16x2(f[8 * q + 2], f[8 * q + 3]);
         w.z = pack_bf16x2(f[8 * q + 4], f[8 * q + 5]);
         w.w = pack_bf16x2(f[8 * q + 6], f[8 * q + 7]);
-        o4[q] = w;
+        // Y / dX: nothing in the step re-reads them soon, so they go out evict-first and
+        // their DRAM write-back happens under this tensor-bound GEMM instead of being left
+        // dirty in L2 for the next (HBM-bound) launch to pay. H / dH (MASK) stay normal:
+        // the next fused GEMM reads them.
+        if constexpr (EPI == EPI_BF16 && TLORA_EPI_EVICT_FIRST)
+          st_global_v4_evict_first(o4 + q, w);
+        else
+          o4[q] = w;
       }
     } else {
 #pragma unroll
