@@ -234,7 +234,7 @@ int orc_aimd_step(int32_t* n, int32_t* has_prev, double* t_prev, int32_t alpha, 
 
 /* ---------------------------------------------------------------- plan oracle */
 enum { BM = 128, BM2 = 256, BK = 64, BN_BASE = 256, BN_LOW = 128, GRAD_MAX_N = 128,
-       GRAD_TARGET = 2 * 148 };
+       GRAD_TARGET = 74 };
 #define L2_BUDGET (48ll << 20)
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }

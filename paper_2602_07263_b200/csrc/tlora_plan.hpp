@@ -57,7 +57,10 @@ constexpr int kPlanBK = 64;       // K block
 constexpr int kPlanBNBase = 256;  // N tile of the fused base GEMMs (fwd, dX)
 constexpr int kPlanBNLow = 128;   // N tile of the low-rank launches (shrink, dH, dA, dB)
 constexpr int kPlanGradMaxN = 128;            // rank columns per gradient tile
-constexpr int kPlanGradTargetTiles = 2 * 148;  // split-K target: ~2 waves of CTAs
+#ifndef TLORA_GRAD_TARGET_TILES
+#define TLORA_GRAD_TARGET_TILES 74  // dB + dA share a launch: ~one wave of tiles in total
+#endif
+constexpr int kPlanGradTargetTiles = TLORA_GRAD_TARGET_TILES;  // split-K target per problem
 constexpr int kPlanMinSplitTokens = 512;
 
 struct PlanTables {
