@@ -39,66 +39,102 @@ def load_peaks():
     return dict(FALLBACK_PEAKS)
 
 
+_SAMPLER_SRC = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByUUID(sys.argv[1].encode())
+mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+out = open(sys.argv[2], "w", buffering=1)
+while True:
+    try:
+        out.write("%.3f,%d,%d,%.1f,%d\n" % (time.time(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx,
+                  pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0,
+                  pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+    except pynvml.NVMLError:
+        pass
+    time.sleep(0.05)
+"""
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms while the GPU is busy
-    (started before the warm-up so even a short timed region is covered)."""
+    """SM clock, power and clock-event (throttle) reasons sampled every ~50 ms from NVML by
+    a separate sampler process (so a busy driver thread cannot starve it), started before
+    the warm-up so even a short timed region is covered. The GPU is found by the CUDA
+    device's UUID. Falls back to `nvidia-smi -lms 200` when NVML is unavailable."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+               ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4),
+               ("hw_power_brake_slowdown", 0x80))
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
+    def __init__(self, device: int):
+        self.device = device
         self.proc = None
-        self.rows = []
-        self.thread = None
+        self.source = None
 
     def start(self):
+        import tempfile
+        self.out = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
+        self.out.close()
         try:
-            self.proc = subprocess.Popen(
-                ["stdbuf", "-oL", "nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
+            import pynvml  # noqa: F401
+            import torch
+            uuid = "GPU-" + str(torch.cuda.get_device_properties(self.device).uuid)
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER_SRC, uuid, self.out.name],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            self.source = "nvml"
+            return
         except Exception:
             self.proc = None
-            return
-        def reader():
-            for line in self.proc.stdout:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 9:
-                    self.rows.append(parts)
-        self.thread = threading.Thread(target=reader, daemon=True)
-        self.thread.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=timestamp,clocks.sm,clocks.max.sm,"
+                 "power.draw,clocks_event_reasons.active", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-f", self.out.name], stdout=subprocess.DEVNULL,
+                stderr=subprocess.DEVNULL)
+            self.source = "nvidia-smi"
+        except Exception:
+            self.proc = None
 
-    def stop(self):
+    def stop(self, window=None):
+        """window = (t_start, t_end) wall-clock seconds: statistics over the samples taken
+        inside it (the settle steps + the timed region); all samples if it holds < 3."""
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock source"]}
+        time.sleep(0.1)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        if self.thread is not None:
-            self.thread.join(timeout=2)
-        rows = list(self.rows)
+        rows = []
+        with open(self.out.name) as f:
+            for line in f:
+                p = [x.strip() for x in line.split(",")]
+                try:
+                    if self.source == "nvml":
+                        ts = float(p[0])
+                    else:  # nvidia-smi timestamp "YYYY/MM/DD HH:MM:SS.mmm"
+                        import datetime
+                        ts = datetime.datetime.strptime(p[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    rows.append((float(p[1]), float(p[2]), float(p[3]), int(p[4], 0), ts))
+                except (ValueError, IndexError):
+                    pass
+        os.unlink(self.out.name)
+        n_all = len(rows)
+        if window is not None:
+            inside = [r for r in rows if window[0] <= r[4] <= window[1]]
+            if len(inside) >= 3:
+                rows = inside
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-
-        def num(x):
-            try:
-                return float(x)
-            except ValueError:
-                return None
-        sm = [v for v in (num(r[1]) for r in rows) if v is not None]
-        mx = [v for v in (num(r[2]) for r in rows) if v is not None]
-        pw = [v for v in (num(r[3]) for r in rows) if v is not None]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
-        loaded = [v for v in sm if mx and v > 0.5 * max(mx)] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "power_w_max": max(pw) if pw else None, "samples": len(rows)}
+        pmax = max(r[2] for r in rows)
+        loaded = [r for r in rows if r[2] >= 0.5 * pmax]  # under load: >= half peak power
+        reasons = sorted({n for r in loaded for n, bit in self.REASONS if r[3] & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "power_w_max": round(pmax, 1), "samples": len(rows), "samples_all": n_all,
+                "samples_under_load": len(loaded), "source": self.source,
+                "window": "settle steps + timed region" if window is not None else "whole run"}
 
 
 # ------------------------------------------------------------------------------ CPU arm
@@ -221,6 +257,7 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([n_settle], device="cuda", dtype=torch.int64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         n_settle = int(t.item())
+    t_clk0 = time.time()
     for _ in range(n_settle):
         one_step()
         torch.cuda.synchronize()
@@ -257,7 +294,7 @@ def run_ours(args, rank, world, local_rank):
             fl6[i] *= args.steps
         graph = graph_prof = None  # event nodes reference events released by profile_end
         step.graph = None
-    clk = clocks.stop()
+    clk = clocks.stop(window=(t_clk0, time.time()))
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -551,9 +588,10 @@ def main():
                          "reduce-scatter is fused into the GEMM epilogue (peer stores over "
                          "NVLink); the rest use NCCL on the comm stream")
     ap.add_argument("--aimd-steps", type=int, default=8, help="AIMD exploration steps (TP mode)")
-    ap.add_argument("--dp-reserve-sms", type=int, default=8,
+    ap.add_argument("--dp-reserve-sms", type=int, default=0,
                     help="DP (N>1): SMs kept free of the persistent grids for the concurrent "
-                         "NCCL all-reduce (NCCL gets half as many channels); 0 = defaults")
+                         "NCCL all-reduce (NCCL gets half as many channels); 0 = defaults "
+                         "(measured best: DP2 2.89 M vs 2.79 M tokens/s with 8 reserved)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -575,8 +613,8 @@ def main():
     if world > 1 and not args.tp and args.dp_reserve_sms > 0:
         # DP: the gradient all-reduce runs on a comm stream concurrently with the persistent
         # GEMMs. Give NCCL a few channels and keep that many SMs (+ slack, whole CTA pairs)
-        # out of the persistent grids, so neither waits for the other to drain an SM
-        # (measured at DP2: 2.85 M tokens/s vs 2.76 M with NCCL's defaults).
+        # out of the persistent grids, so neither waits for the other to drain an SM.
+        # Off by default: 3 A/B runs each at DP2 gave 2.79 M (8 reserved) vs 2.89 M.
         os.environ.setdefault("TLORA_SM_RESERVE", str(args.dp_reserve_sms))
         os.environ.setdefault("NCCL_MAX_NCHANNELS", str(max(1, args.dp_reserve_sms // 2)))
     if world > 1 or args.tp:
