@@ -385,11 +385,13 @@ def run_ours(args, rank, world, local_rank):
         "tflops": round(fl6[i] / (ms6[i] / 1e3) / 1e12, 1) if ms6[i] > 0 else None,
         "share_of_gemm_time": round(ms6[i] / total_ms, 4) if total_ms > 0 else None}
         for i in range(6)}
-    traffic = None
+    traffic = traffic_alg = None
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
         try:
-            traffic = json.loads(tp.read_text()).get("fwd_bytes_per_launch")
+            tj = json.loads(tp.read_text())
+            traffic = tj.get("dram_bytes_per_launch_mean", tj.get("fwd_bytes_per_launch"))
+            traffic_alg = tj.get("algorithmic_bytes_per_launch_mean")
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
@@ -398,7 +400,9 @@ def run_ours(args, rank, world, local_rank):
                 "timing": ("CUDA-event brackets captured in a second graph of the step, replayed "
                            "as the LAST timed step; per-launch durations of that step x steps") if used_graph else
                           "CUDA-event brackets around every launch of the timed region",
-                "traffic": traffic, "kernel": "lora_gemm2_kernel (2-CTA fused base+LoRA GEMM: fwd + dX)",
+                "traffic": traffic, "traffic_algorithmic_bytes": traffic_alg,
+                "traffic_source": "profiles/traffic.json (ncu dram bytes, mean per fused-GEMM launch)",
+                "kernel": "lora_gemm2_kernel (2-CTA fused base+LoRA GEMM: fwd + dX)",
                 "peak_source": peaks["source"] + " sustained bf16", "per_launch": per_launch}
 
     cpu = None

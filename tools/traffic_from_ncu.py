@@ -1,0 +1,81 @@
+"""profiles/traffic.json from an ncu launch list of ONE step's 14 fused-GEMM launches.
+
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \\
+      --clock-control none -k regex:lora_gemm2 --launch-skip 14 -c 14 --csv \\
+      --log-file traffic14.csv python bench.py --steps 1 --warmup 3 --no-graph
+  python tools/traffic_from_ncu.py traffic14.csv
+
+Launch order of a chained C2 step: fwd q,k,v,o,gate,up,down (each carrying the next
+projection's shrink tiles), then dX down,up,gate,o,v,k,q (each carrying the next dH).
+`traffic` in bench.py's roofline = mean DRAM bytes (read + write) per launch; the
+algorithmic bytes per launch (each operand / output touched once) are reported beside it.
+"""
+import csv
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+from paper_2602_07263_b200.workload import INPUT_GROUP, config  # noqa: E402
+
+
+def main():
+    src = Path(sys.argv[1])
+    rows = list(csv.reader(src.open()))
+    hdr, by = None, {}
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            by.setdefault(int(d["ID"]), {})[d["Metric Name"]] = float(d["Metric Value"])
+    wl = config("C2")
+    T = wl.tokens
+    R = sum((j.rank + 7) // 8 * 8 for j in wl.jobs)
+    projs = wl.projections
+    fwd = [(p, projs[i + 1] if i + 1 < len(projs) else None) for i, p in enumerate(projs)]
+    rev = list(reversed(projs))
+    bwd = [(p, rev[i + 1] if i + 1 < len(rev) else None) for i, p in enumerate(rev)]
+    launches = []
+    for kind, seq in (("fwd", fwd), ("dX", bwd)):
+        for (name, d, k), nxt in seq:
+            main_b = 2 * (T * d + d * k + T * k + T * R + R * (k if kind == "fwd" else d))
+            sec = 0
+            if nxt is not None:
+                nn, nd, nk = nxt
+                if kind == "fwd":  # X_next (unless shared with this projection's X) + Aᵀ + H_next
+                    shared = INPUT_GROUP.get(nn) == INPUT_GROUP.get(name)
+                    sec = 2 * ((0 if shared else T * nd) + R * nd + T * R)
+                else:              # dY_next + Bcat + dH_next
+                    sec = 2 * (T * nk + R * nk + T * R)
+            launches.append({"launch": f"{kind} {name}" + (f" + {'shrink' if kind == 'fwd' else 'dH'} {nxt[0]}" if nxt else ""),
+                             "algorithmic_bytes": main_b + sec})
+    ids = sorted(by)
+    assert len(ids) == len(launches), (len(ids), len(launches))
+    for i, L in zip(ids, launches):
+        m = by[i]
+        L["dram_read_bytes"] = int(m["dram__bytes_read.sum"])
+        L["dram_write_bytes"] = int(m["dram__bytes_write.sum"])
+        L["duration_ns"] = int(m["gpu__time_duration.sum"])
+    n = len(launches)
+    mean_dram = sum(L["dram_read_bytes"] + L["dram_write_bytes"] for L in launches) / n
+    mean_alg = sum(L["algorithmic_bytes"] for L in launches) / n
+    out = {"fwd_bytes_per_launch": int(mean_dram),
+           "kernel": "lora_gemm2_kernel, the 14 fused GEMM launches (fwd + dX) of one chained C2 step",
+           "dram_bytes_per_launch_mean": int(mean_dram),
+           "algorithmic_bytes_per_launch_mean": int(mean_alg),
+           "traffic_over_algorithmic": round(mean_dram / mean_alg, 2),
+           "source": f"{src.name}: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
+                     "--clock-control none (cache flushed per launch)",
+           "note": "the launches are tensor-pipe bound (~90% tensor active, DRAM ~20% of peak); "
+                   "the L2 panel raster (48 MB budget) minimises DRAM bytes among the budgets "
+                   "swept (8..64 MB: 6.2 .. 2.35 GB for gate fwd); the re-reads do not bind",
+           "launches": launches}
+    (ROOT / "profiles" / "traffic.json").write_text(json.dumps(out, indent=1))
+    print(json.dumps({k: v for k, v in out.items() if k != "launches"}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
