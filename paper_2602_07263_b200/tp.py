@@ -316,24 +316,42 @@ class TPLayerSetStep:
             b = nb[i]
             beta = 1.0 if i else 0.0
             C.wait_event(ev_dy)
-            for p in rows:  # row-parallel: dH exact, dX local, dA local, dB partial
-                lay, pl = self.layers[p], plans[i][p][0]
-                dYf = self._rows(self.dY_full[p], b)
-                lay.dh(pl, dYf, self._rows(self.dH_row[p], b), stream=C)
-                lay.dx(pl, dYf, self._rows(self.dH_row[p], b), self._rows(self.dX_loc[p], b), stream=C)
-                lay.grad_b(pl, self._rows(self.H_row[p], b), dYf, beta=beta, stream=C)
-                lay.grad_a(pl, self._rows(self.X_loc[p], b), self._rows(self.dH_row[p], b),
-                           beta=beta, stream=C)
+            # Chained schedule (as runner.LayerSetStep): each dX launch also computes the
+            # NEXT projection's dH as extra tiles (tlora_backward_dx_dh), so only the first
+            # dH of the nano-batch has a launch of its own. Order: row-parallel projections,
+            # then the column-parallel ones in reverse.
+            seq = [("row", p) for p in rows] + [("col", p) for p in reversed(cols)]
+
+            def dy_dh(kind, p):
+                if kind == "row":
+                    return self._rows(self.dY_full[p], b), self._rows(self.dH_row[p], b)
+                return self._rows(self.dY[p], b), self._rows(self.dH_part[p], b)
+
+            k0, p0 = seq[0]
+            dY0, dH0 = dy_dh(k0, p0)
+            self.layers[p0].dh(plans[i][p0][0], dY0, dH0, stream=C)
             first = {}
-            for p in reversed(cols):  # column-parallel: partial dH / dX, local dB
+            for j, (kind, p) in enumerate(seq):
                 lay, pl = self.layers[p], plans[i][p][0]
-                g = INPUT_GROUP[p]
-                dYl = self._rows(self.dY[p], b)
-                lay.dh(pl, dYl, self._rows(self.dH_part[p], b), stream=C)
-                lay.dx(pl, dYl, self._rows(self.dH_part[p], b), self._rows(self.dX_part[g], b),
-                       beta=1.0 if g in first else 0.0, stream=C)
-                first[g] = True
-                lay.grad_b(pl, self._rows(self.H_full[p], b), dYl, beta=beta, stream=C)
+                dYp, dHp = dy_dh(kind, p)
+                if kind == "row":  # dH exact, dX local, dA local, dB partial
+                    dXp, bx = self._rows(self.dX_loc[p], b), 0.0
+                else:              # partial dH / dX (summed per input group), local dB
+                    g = INPUT_GROUP[p]
+                    dXp, bx = self._rows(self.dX_part[g], b), 1.0 if g in first else 0.0
+                    first[g] = True
+                if j + 1 < len(seq):
+                    kn, pn = seq[j + 1]
+                    dYn, dHn = dy_dh(kn, pn)
+                    lay.dx_dh(pl, dYp, dHp, dXp, self.layers[pn], plans[i][pn][0], dYn, dHn,
+                              beta=bx, zero_next=True, stream=C)
+                else:
+                    lay.dx(pl, dYp, dHp, dXp, beta=bx, stream=C)
+                if kind == "row":
+                    lay.grads(pl, self._rows(self.H_row[p], b), dYp, self._rows(self.X_loc[p], b),
+                              dHp, beta=beta, stream=C)
+                else:
+                    lay.grad_b(pl, self._rows(self.H_full[p], b), dYp, beta=beta, stream=C)
             ev_c = torch.cuda.Event()
             ev_c.record(C)
             M.wait_event(ev_c)
