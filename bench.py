@@ -166,6 +166,8 @@ def run_ours(args, rank, world, local_rank):
     step = LayerSetStep(wl, device=local_rank, seed=wl.seed + rank, shuffle=args.shuffle,
                         chain=not args.no_chain and args.overlap == 0)
     step.enable_optimizer()
+    if os.environ.get("TLORA_SIDE_GRADS", "1") == "1" and step.chain:
+        step.enable_side_grads()
     if args.overlap != 0:
         step.enable_overlap(args.overlap)
     stream = torch.cuda.current_stream()
@@ -231,6 +233,9 @@ def run_ours(args, rank, world, local_rank):
             (graph_prof if last and graph_prof is not None else graph).replay()
             return
         fwd()
+        if world == 1 and args.overlap == 0:
+            step.backward_and_update(stream)
+            return
         bwd()
         if flat_grads is not None:
             for g in flat_grads:
@@ -331,13 +336,16 @@ def run_ours(args, rank, world, local_rank):
             fwd()
             if ev_out is not None:
                 stream.wait_event(ev_out)  # grads of step i-1 are on the host before reuse
-            bwd()
-            if world > 1:
-                for w in pending:
-                    w.wait()
-                pending.clear()
-                stream.wait_stream(comm_stream)
-            step.optimizer_step(stream, grad_scale=1.0 / world)
+            if world == 1 and args.overlap == 0:
+                step.backward_and_update(stream)
+            else:
+                bwd()
+                if world > 1:
+                    for w in pending:
+                        w.wait()
+                    pending.clear()
+                    stream.wait_stream(comm_stream)
+                step.optimizer_step(stream, grad_scale=1.0 / world)
             done[i].record(stream)
             with torch.cuda.stream(copy):
                 if i + 1 < nsteps:

@@ -97,7 +97,53 @@ class LayerSetStep:
             else:
                 lay.fused_gemm(pl, self.x_of(name), self.H[(L, name)], self.Y[name], stream=stream)
 
-    def backward_chained(self, stream=None, beta: float = 0.0, on_layer_done=None):
+    def enable_side_grads(self):
+        """Chained backward with each projection's dB+dA launch on a side stream: it reads
+        only H, X, dY and the projection's dH (produced by the previous dX launch), so it
+        can run while the main stream's next fused GEMM runs, filling that GEMM's tail. dH
+        uses a ring of 4 buffers; a dX launch waits for the side-stream reader of the
+        buffer it overwrites."""
+        self.side = torch.cuda.Stream(self.dev)
+        self.dH4 = torch.zeros(4, self.T, self.dH2.shape[2], dtype=torch.bfloat16, device=self.dev)
+        self.side_grads = True
+
+    def _backward_side(self, main, beta, on_layer_done, opt_inline=False):
+        side, keys = self.side, list(reversed(self.keys))
+        ev = torch.cuda.Event()
+        ev.record(main)
+        side.wait_event(ev)  # adapters / grads of the previous step are settled
+        done = {}            # key index -> event after its grads launch (side stream)
+        k0 = keys[0]
+        self.layers[k0].dh(self.plans[k0[1]], self.dY[k0[1]], self.dH4[0], stream=main)
+        for i, (L, name) in enumerate(keys):
+            lay, pl = self.layers[(L, name)], self.plans[name]
+            dH = self.dH4[i % 4]
+            if i + 1 < len(keys):
+                nk = keys[i + 1]
+                if i - 3 in done:  # buffer (i+1)%4 was last read by grads(i-3)
+                    main.wait_event(done[i - 3])
+                lay.dx_dh(pl, self.dY[name], dH, self.dX[name], self.layers[nk], self.plans[nk[1]],
+                          self.dY[nk[1]], self.dH4[(i + 1) % 4], zero_next=False, stream=main)
+            else:
+                lay.dx(pl, self.dY[name], dH, self.dX[name], stream=main)
+            ready = torch.cuda.Event()
+            ready.record(main)  # dH(i) was written by the previous launch on main
+            side.wait_event(ready)
+            lay.grads(pl, self.H[(L, name)], self.dY[name], self.x_of(name), dH, beta=beta,
+                      stream=side)
+            if opt_inline:  # nothing later in the step reads this projection's adapters
+                lay.optimizer_step(stream=side)
+            done[i] = torch.cuda.Event()
+            done[i].record(side)
+            if on_layer_done is not None:
+                on_layer_done((L, name), lay, done[i])
+        main.wait_stream(side)
+
+    def backward_chained(self, stream=None, beta: float = 0.0, on_layer_done=None,
+                         opt_inline=False):
+        if getattr(self, "side_grads", False):
+            return self._backward_side(stream if stream is not None else torch.cuda.current_stream(self.dev),
+                                       beta, on_layer_done, opt_inline)
         keys = list(reversed(self.keys))
         k0 = keys[0]
         self.layers[k0].dh(self.plans[k0[1]], self.dY[k0[1]], self.dH2[0], stream=stream)
@@ -222,11 +268,22 @@ class LayerSetStep:
         return g
 
     def step(self, stream=None, on_layer_done=None):
-        """One training step: forward, backward, fused AdamW update of every adapter."""
+        """One training step: forward, backward, fused AdamW update of every adapter. With
+        side-stream gradients and no cross-replica exchange, each projection's AdamW runs
+        on the side stream right after its dB+dA (overlapping the remaining GEMMs)."""
         self.forward(stream)
+        self.backward_and_update(stream, on_layer_done)
+
+    def backward_and_update(self, stream=None, on_layer_done=None, grad_scale: float = 1.0):
+        optim = getattr(self, "optim", False)
+        inline = (optim and on_layer_done is None and grad_scale == 1.0 and self.chain
+                  and getattr(self, "side_grads", False))
+        if inline:
+            self.backward_chained(stream, opt_inline=True)
+            return
         self.backward(stream, on_layer_done=on_layer_done)
-        if getattr(self, "optim", False):
-            self.optimizer_step(stream)
+        if optim:
+            self.optimizer_step(stream, grad_scale)
 
     def input_tensors(self):
         """Every tensor a step reads from outside the layer (for the e2e host copies)."""

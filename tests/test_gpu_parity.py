@@ -391,8 +391,10 @@ def test_chained_lowrank_tiles_are_bit_identical(tokens):
                   [Job("a", 8, 2, tokens[0]), Job("b", 200, 3, tokens[1]),
                    Job("c", 16, 1, tokens[2])], layers=2)
     out = []
-    for chain in (False, True):
+    for chain, side in ((False, False), (True, False), (True, True)):
         st = LayerSetStep(wl, device=0, seed=7, chain=chain)
+        if side:  # dB+dA launches on a side stream (runner.enable_side_grads)
+            st.enable_side_grads()
         st.forward()
         st.backward()
         torch.cuda.synchronize()
@@ -400,13 +402,14 @@ def test_chained_lowrank_tiles_are_bit_identical(tokens):
                     "dX": {k: v.clone() for k, v in st.dX.items()},
                     "H": {k: v.clone() for k, v in st.H.items()},
                     "g": {k: [t.clone() for t in lay.packed_grads()] for k, lay in st.layers.items()}})
-    a, b = out
-    for k in a["Y"]:
-        assert torch.equal(a["Y"][k], b["Y"][k]) and torch.equal(a["dX"][k], b["dX"][k]), k
-    for k in a["H"]:
-        assert torch.equal(a["H"][k], b["H"][k]), k
-    for k in a["g"]:
-        assert all(torch.equal(x, y) for x, y in zip(a["g"][k], b["g"][k])), k
+    a = out[0]
+    for b in out[1:]:
+        for k in a["Y"]:
+            assert torch.equal(a["Y"][k], b["Y"][k]) and torch.equal(a["dX"][k], b["dX"][k]), k
+        for k in a["H"]:
+            assert torch.equal(a["H"][k], b["H"][k]), k
+        for k in a["g"]:
+            assert all(torch.equal(x, y) for x, y in zip(a["g"][k], b["g"][k])), k
 
 
 def test_gemm_shrink_zero_next_clears_garbage():
