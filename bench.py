@@ -468,7 +468,10 @@ def run_tp(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     wl = config(args.config)
-    fused = [p for p in args.fused_rs.split(",") if p]
+    spec = args.fused_rs
+    if spec == "auto":  # fused GEMM + reduce-scatter is the default at TP > 1 (measured
+        spec = "o,down" if world > 1 else ""  # 1-3% faster than NCCL at TP2 / TP4)
+    fused = [p for p in spec.split(",") if p and p != "none"]
     st = TPLayerSetStep(wl, rank, world, local_rank, nano=args.nano, fused_rs=fused)
     st.enable_optimizer()
     stream = torch.cuda.current_stream()
@@ -600,10 +603,11 @@ def main():
     ap.add_argument("--tp", action="store_true",
                     help="tensor-parallel layer set over the torchrun group (default config C4)")
     ap.add_argument("--nano", type=int, default=4, help="initial nano-batch count (TP mode)")
-    ap.add_argument("--fused-rs", default="",
+    ap.add_argument("--fused-rs", default="auto",
                     help="TP mode: comma list of row-parallel projections (o,down) whose "
-                         "reduce-scatter is fused into the GEMM epilogue (peer stores over "
-                         "NVLink); the rest use NCCL on the comm stream")
+                         "reduce-scatter is fused into the GEMM epilogue (bulk copies into "
+                         "the owner's receive slot over NVLink); the rest use NCCL on the "
+                         "comm stream. auto = o,down when TP > 1; none = NCCL for all")
     ap.add_argument("--aimd-steps", type=int, default=8, help="AIMD exploration steps (TP mode)")
     ap.add_argument("--dp-reserve-sms", type=int, default=0,
                     help="DP (N>1): SMs kept free of the persistent grids for the concurrent "

@@ -32,6 +32,13 @@ struct Gemm2Smem {
   static constexpr int kBarOffset = STAGES * kStageBytes;
   static constexpr int kTotal = kBarOffset + (2 * STAGES + 4) * 8 + 16;
   static constexpr int kDynamic = kTotal + 1024;
+  // EPI_PEER staging: per epilogue warp two buffers of 32 rows x 64 bf16 columns, rows
+  // padded to 144 B (conflict-free 16-B shared stores; each row stays one contiguous
+  // 128-B bulk copy source)
+  static constexpr int kStgRow = 144;
+  static constexpr int kStgBuf = 32 * kStgRow;
+  static constexpr int kStagingOffset = (kTotal + 127) / 128 * 128;
+  static constexpr int kDynamicPeer = kStagingOffset + 4 * 2 * kStgBuf + 1024;
 };
 
 // Secondary tiles (args2, maps tmA2 / tmB2): another layer's shrink or dH on 256-token
@@ -208,6 +215,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       }
       const int ncols = sec ? td.pad : kBN2;
       const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * kBN2;
+      if constexpr (EPI == EPI_PEER) {
+        if (!sec) {
+          // Reduce-scatter epilogue: 64-column row chunks are converted to bf16 into a
+          // shared-memory staging row, and each lane bulk-copies its row's 128 B straight
+          // into the owner rank's receive slot (cp.async.bulk over NVLink): one 128-B
+          // transfer per row and chunk instead of eight 16-B stores.
+          uint8_t* stg = smem + L::kStagingOffset + ew * 2 * L::kStgBuf;
+          const bool live = row < args.M;
+          __nv_bfloat16* dst = nullptr;
+          if (live) {
+            const int64_t dest = row / args.rows_per_rank, lrow = row % args.rows_per_rank;
+            dst = reinterpret_cast<__nv_bfloat16*>(args.peer[dest]) +
+                  ((int64_t)args.peer_rank * args.slot_rows + args.dst_row0 + lrow) * args.ldo +
+                  td.n0;
+          }
+#pragma unroll 1
+          for (int c = 0; c < kBN2; c += 64) {
+            uint32_t v0[32], v1[32];
+            if (!empty_k) {
+              tmem_ld_32x32b_x32(t_row + c, v0);
+              tmem_ld_32x32b_x32(t_row + c + 32, v1);
+              tmem_wait_ld();
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v0[i] = v1[i] = 0u;
+            }
+            uint8_t* rowp = stg + ((c >> 6) & 1) * L::kStgBuf + lane * L::kStgRow;
+            bulk_wait_read<1>();  // the copy that last read this buffer has finished reading
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const uint32_t* src = q < 4 ? v0 + 8 * q : v1 + 8 * (q - 4);
+              uint4 w;
+              w.x = pack_bf16x2(__uint_as_float(src[0]), __uint_as_float(src[1]));
+              w.y = pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
+              w.z = pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));
+              w.w = pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
+              *reinterpret_cast<uint4*>(rowp + 16 * q) = w;
+            }
+            fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk copy
+            if (live && td.n0 + c < args.N) bulk_store_s2g(dst + c, rowp, 128);
+            bulk_commit();
+          }
+          if (!empty_k) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
+          }
+          continue;
+        }
+      }
 #pragma unroll 1
       for (int c = 0; c < ncols; c += 32) {
         uint32_t v[32];
@@ -229,7 +286,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);
       }
     }
-    if constexpr (EPI == EPI_PEER) __threadfence_system();  // peer stores before completion
+    if constexpr (EPI == EPI_PEER) {
+      bulk_wait_all();        // every bulk copy to a peer has been performed
+      __threadfence_system();  // peer stores before completion
+    }
   }
 
   tc_fence_before();

@@ -225,7 +225,8 @@ void launch_gemm2(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
   if (total == 0) return;
   if (sec) args2 = sec->args;
   auto kern = tlora::lora_gemm2_kernel<EPI, ST>;
-  constexpr int smem = tlora::Gemm2Smem<ST>::kDynamic;
+  constexpr int smem = EPI == tlora::EPI_PEER ? tlora::Gemm2Smem<ST>::kDynamicPeer
+                                              : tlora::Gemm2Smem<ST>::kDynamic;
   TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int dev = 0;
   TL_CUDA(cudaGetDevice(&dev));
@@ -1367,7 +1368,7 @@ int tlora_forward_gemm_rs(tlora_layer* layer, const tlora_plan* plan, const void
     const auto& L = layer->L;
     const int64_t T = plan->P.T, d = L.d, k = L.k, R = L.R;
     require(T % world == 0, TLORA_ERR_SHAPE, "tokens must divide evenly over the ranks");
-    require(k % 32 == 0, TLORA_ERR_SHAPE, "fused reduce-scatter needs k % 32 == 0");
+    require(k % 64 == 0, TLORA_ERR_SHAPE, "fused reduce-scatter needs k % 64 == 0");
     require(dst_row0 >= 0 && dst_row0 + T / world <= slot_rows, TLORA_ERR_ARG,
             "receive slot too small for this plan");
     for (int p = 0; p < world; ++p) check_align(recv_ptrs[p], "receive buffer");
@@ -1389,7 +1390,7 @@ int tlora_forward_gemm_rs(tlora_layer* layer, const tlora_plan* plan, const void
     const CUtensorMap mb0 = tmap_k(layer->Wt16.p, d, k, 128);
     const CUtensorMap ma1 = tmap_k(H, R, T, 128);
     const CUtensorMap mb1 = tmap_k(layer->BcatT.p, R, k, 128);
-    launch_gemm2<tlora::EPI_PEER, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD,
+    launch_gemm2<tlora::EPI_PEER, 5>(ma0, mb0, ma1, mb1, a, layer->sm_count, s, TLORA_L_FWD,
                                      2.0 * T * d * k + 2.0 * (double)plan->P.tok_rank * k);
   });
 }
