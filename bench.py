@@ -524,6 +524,30 @@ def run_tp(args, rank, world, local_rank):
     ms_per_step = t.item() / args.steps
     flops = wl.flops_fwd_bwd() / wl.layers
     value = wl.tokens / (ms_per_step / 1e3)
+    n_launch = int(lib.tlora_launch_count() - n0)
+    # one extra step with every launch bracketed by CUDA events (after the timed region):
+    # where this rank's step time goes, and the fused GEMM family's achieved TFLOP/s
+    import ctypes as C
+    capi.call("tlora_profile_begin")
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    st.step(st.n)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    cnt, ms6, fl6 = (C.c_int32 * 6)(), (C.c_double * 6)(), (C.c_double * 6)()
+    capi.call("tlora_profile_end", cnt, ms6, fl6)
+    prof_ms = e2.elapsed_time(e3)
+    fam_ms, fam_fl = ms6[capi.L_FWD] + ms6[capi.L_DX], fl6[capi.L_FWD] + fl6[capi.L_DX]
+    peaks = load_peaks()
+    peak = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+    ach = fam_fl / (fam_ms / 1e3) / 1e12 if fam_ms > 0 else 0.0
+    roofline = {"bound": "tensor", "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s",
+                "frac": round(ach / peak, 4) if peak else None,
+                "kernel": "lora_gemm2_kernel (fused GEMM fwd + dX, per rank, this rank's shards)",
+                "timing": "CUDA-event brackets of one extra profiled step after the timed region",
+                "gemm_share_of_profiled_step": round(fam_ms / prof_ms, 4) if prof_ms else None,
+                "per_launch": {capi.LAUNCH_NAMES[i]: {"launches": cnt[i], "ms": round(ms6[i], 3)}
+                               for i in range(6)}}
     return {
         "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
@@ -538,7 +562,8 @@ def run_tp(args, rank, world, local_rank):
                    "algorithmic_tflop_per_step": round(flops / 1e12, 3),
                    "achieved_tflops_aggregate": round(flops / (ms_per_step / 1e3) / 1e12, 1),
                    "achieved_tflops_per_gpu": round(flops / world / (ms_per_step / 1e3) / 1e12, 1)},
-        "gpu_launches": int(lib.tlora_launch_count() - n0),
+        "gpu_launches": n_launch,
+        "roofline": roofline,
         "clocks": clk,
     }
 
