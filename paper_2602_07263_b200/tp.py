@@ -95,6 +95,11 @@ class TPLayerSetStep:
         self.n = nano
         self.compute = torch.cuda.current_stream(self.dev)
         self.comm = torch.cuda.Stream(self.dev)
+        # adapter-gradient launches (HBM-bound) run on their own stream, overlapping the
+        # fused GEMMs of the compute stream (as runner.LayerSetStep.enable_side_grads)
+        import os
+        self.gside = (torch.cuda.Stream(self.dev) if os.environ.get("TLORA_TP_SIDE_GRADS", "1") != "0"
+                      else self.compute)
         seed = wl.seed if seed is None else seed
         self.layers, self.R = {}, {}
         self.full_weights = {}
@@ -285,11 +290,17 @@ class TPLayerSetStep:
     def backward(self, n: int | None = None):
         n = self.n if n is None else n
         nb, plans = self.plans(n)
-        C, M = self.compute, self.comm
+        C, M, G = self.compute, self.comm, self.gside
         cols = [p for p in COLUMN if p in self.layers]
         rows = [p for p in ROW if p in self.layers]
         start = torch.cuda.Event()
         start.record(C)
+        G.wait_event(start)
+
+        def on_g(ev_src):  # the gradient stream waits for an event of another stream
+            e = torch.cuda.Event()
+            e.record(ev_src)
+            G.wait_event(e)
 
         def gather_dy(i):
             b = nb[i]
@@ -303,11 +314,11 @@ class TPLayerSetStep:
 
         def grad_a_cols(i, ev):
             b = nb[i]
-            C.wait_event(ev)
+            G.wait_event(ev)
             for p in cols:
                 self.layers[p].grad_a(plans[i][p][1], self._srows(self.X_shard[INPUT_GROUP[p]], b),
                                       self._srows(self.dH_shard[p], b), beta=1.0 if i else 0.0,
-                                      stream=C)
+                                      stream=G)
 
         ev_dy = gather_dy(0)
         pending = None
@@ -347,11 +358,12 @@ class TPLayerSetStep:
                               beta=bx, zero_next=True, stream=C)
                 else:
                     lay.dx(pl, dYp, dHp, dXp, beta=bx, stream=C)
+                on_g(C)  # dH of p (written by the previous launch on C) and dY are ready
                 if kind == "row":
                     lay.grads(pl, self._rows(self.H_row[p], b), dYp, self._rows(self.X_loc[p], b),
-                              dHp, beta=beta, stream=C)
+                              dHp, beta=beta, stream=G)
                 else:
-                    lay.grad_b(pl, self._rows(self.H_full[p], b), dYp, beta=beta, stream=C)
+                    lay.grad_b(pl, self._rows(self.H_full[p], b), dYp, beta=beta, stream=G)
             ev_c = torch.cuda.Event()
             ev_c.record(C)
             M.wait_event(ev_c)
@@ -368,6 +380,7 @@ class TPLayerSetStep:
             ev_dy = ev_dy_next
         grad_a_cols(*pending)
         # replicated adapter halves: sum the TP partials once per step
+        C.wait_stream(G)
         ev = torch.cuda.Event()
         ev.record(C)
         M.wait_event(ev)
