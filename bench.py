@@ -18,7 +18,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 from pathlib import Path
 
@@ -72,7 +71,6 @@ class ClockSampler:
         self.source = None
 
     def start(self):
-        import tempfile
         self.out = tempfile.NamedTemporaryFile(mode="w+", suffix=".csv", delete=False)
         self.out.close()
         try:
@@ -168,6 +166,11 @@ def run_ours(args, rank, world, local_rank):
     step.enable_optimizer()
     if os.environ.get("TLORA_SIDE_GRADS", "1") == "1" and step.chain:
         step.enable_side_grads()
+        g_sms = int(os.environ.get("TLORA_GRAD_SMS", "0"))
+        if g_sms > 0:  # experiment knob: GEMMs on (SMs - g), gradients on g (measured much
+            # slower: 8 / 16 / 24 SMs -> 14.5 / 12.5 / 12.2 ms vs 10.87 ms per C2 step)
+            total = torch.cuda.get_device_properties(local_rank).multi_processor_count
+            capi.call("tlora_set_sm_budget", local_rank, total - g_sms, g_sms)
     if args.overlap != 0:
         step.enable_overlap(args.overlap)
     stream = torch.cuda.current_stream()

@@ -7,7 +7,7 @@ no activation: the layer is the unit of work).
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 

@@ -17,7 +17,7 @@ import torch.distributed as dist
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2602_07263_b200.layer import FusedLoRALayer  # noqa: E402
-from paper_2602_07263_b200.tp import COLUMN, ROW, TPLayerSetStep  # noqa: E402
+from paper_2602_07263_b200.tp import COLUMN, TPLayerSetStep  # noqa: E402
 from paper_2602_07263_b200.workload import INPUT_GROUP, config  # noqa: E402
 
 

@@ -1,4 +1,8 @@
-import torch, time
+"""Raw pinned-host <-> device copy bandwidth (the e2e path's PCIe ceiling).
+
+  python tools/pcie_probe.py
+"""
+import torch
 for mb in (256, 1024):
     h = torch.empty(mb << 20, dtype=torch.uint8).pin_memory()
     d = torch.empty(mb << 20, dtype=torch.uint8, device="cuda")
