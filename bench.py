@@ -161,6 +161,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     capi.call("tlora_device_check", local_rank, None)
     wl = config(args.config)
+    if args.layers > 0:  # e.g. one layer of C4's 64-layer stack on a single GPU
+        wl.layers = args.layers
     step = LayerSetStep(wl, device=local_rank, seed=wl.seed + rank, shuffle=args.shuffle,
                         chain=not args.no_chain and args.overlap == 0)
     step.enable_optimizer()
@@ -435,7 +437,8 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (seeded normal activations/grads, random-init W and adapters)",
-        "config": {"workload": f"{wl.name}: {wl.notes}", "tokens_per_gpu": wl.tokens,
+        "config": {"workload": f"{wl.name}: {wl.notes}", "layers_per_step": wl.layers,
+                   "tokens_per_gpu": wl.tokens,
                    "jobs": [[j.job_id, j.rank, j.tokens] for j in wl.jobs],
                    "projections": wl.projections, "token_order": "shuffled" if args.shuffle else "job-contiguous",
                    "parallelism": f"dp{world}", "lowrank_side_stream_sms": args.overlap,
@@ -613,6 +616,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
+    ap.add_argument("--layers", type=int, default=0,
+                    help="override the config's layer count (0 = as configured)")
     ap.add_argument("--shuffle", action="store_true", help="interleave jobs' tokens")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens-per-job", type=int, default=8)
