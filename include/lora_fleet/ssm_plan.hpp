@@ -41,6 +41,59 @@ inline SsmGraph fuse(const std::vector<JobSpec>& group) {
   return g;
 }
 
+// ---- projection-level extension (new): the reference adapts ONE projection per layer
+// (fused_lora.hpp:166-176 counts r·(d+k) per layer). A transformer layer of the configs C2-C4
+// adapts seven (q, k, v, o, gate, up, down), each a fused multi-LoRA layer with its own
+// registry; every (layer, projection, job) branch maps to registry slot = the job's
+// position in the job_id-sorted group, identical for all projections.
+struct Projection {
+  std::string name;
+  long long d = 0, k = 0;  // in-features, out-features
+};
+
+// q/k/v/o + gated MLP of a decoder layer (hidden, key/value width, intermediate size).
+inline std::vector<Projection> decoder_projections(long long hidden, long long q_out,
+                                                   long long kv_out, long long intermediate) {
+  return {{"q", hidden, q_out},          {"k", hidden, kv_out},         {"v", hidden, kv_out},
+          {"o", q_out, hidden},          {"gate", hidden, intermediate}, {"up", hidden, intermediate},
+          {"down", intermediate, hidden}};
+}
+
+struct SsmLayerSet {
+  SsmGraph graph;
+  std::vector<Projection> projections;
+  struct Branch {
+    int layer;
+    int projection;  // index into projections
+    std::string job_id;
+    int slot;        // registry slot of the projection's fused layer
+  };
+  std::vector<Branch> branches;  // layer-major, then projection, then job_id order
+};
+
+inline SsmLayerSet fuse_projections(const std::vector<JobSpec>& group,
+                                    std::vector<Projection> projections) {
+  if (projections.empty()) throw std::invalid_argument("fuse_projections: no projections");
+  SsmLayerSet s;
+  s.graph = fuse(group);
+  s.projections = std::move(projections);
+  for (int layer : s.graph.backbone_nodes)
+    for (int p = 0; p < (int)s.projections.size(); ++p)
+      for (int slot = 0; slot < (int)s.graph.jobs.size(); ++slot)
+        s.branches.push_back({layer, p, s.graph.jobs[slot].job_id, slot});
+  return s;
+}
+
+// r·Σ_p(d_p + k_p) per layer × layers: the trainable parameters of one job when every
+// listed projection of every layer is adapted (reduces to trainable_param_count(job) for
+// the single projection {hidden_dim -> proj_dim}).
+inline long long trainable_param_count(const JobSpec& job, const std::vector<Projection>& projections) {
+  job.validate();
+  long long per_layer = 0;
+  for (const auto& p : projections) per_layer += p.d + p.k;
+  return static_cast<long long>(job.rank) * per_layer * job.model.num_layers;
+}
+
 // Registry slot order of a fused layer for this graph: position of each job in g.jobs.
 inline std::vector<int> registry_ranks(const SsmGraph& g) {
   std::vector<int> r;

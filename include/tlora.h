@@ -151,6 +151,12 @@ int tlora_plan_get_info(const tlora_plan* plan, tlora_plan_info* info);
 int tlora_plan_get_tiles(const tlora_plan* plan, int launch, tlora_tile* out, int32_t cap,
                          int32_t* count);
 
+/* Debug readback of what the device actually holds for a plan: the tile table of `launch`
+ * as uploaded (copied back from device memory; cap entries max) and, if token_slot is
+ * non-NULL, the uploaded owner slot of every token (tokens entries). Synchronous. Lets a
+ * test memcmp the device plan against the plan oracle. */
+int tlora_plan_read_device(const tlora_plan* plan, int launch, tlora_tile* out, int32_t cap,
+                           int32_t* count, int32_t* token_slot);
 /* Host-only plan builder (no device needed): the same tile table tlora_plan_create
  * uploads, for the registry layout `ranks` and the token->slot map. For bit-exact checks
  * against the plan oracle and for planning on a host without a GPU. */

@@ -100,6 +100,8 @@ SIGNATURES = {
                                     C.c_float, C.c_void_p]),
     "tlora_backward_dx_dh": (C.c_int, [C.c_void_p] * 5 + [C.c_float] + [C.c_void_p] * 4
                              + [C.c_int, C.c_void_p]),
+    "tlora_plan_read_device": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int32,
+                                         C.POINTER(C.c_int32), C.c_void_p]),
     "tlora_segments": (C.c_int, [C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "tlora_comm_get_unique_id": (C.c_int, [C.c_void_p]),
     "tlora_comm_create": (C.c_int, [C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,

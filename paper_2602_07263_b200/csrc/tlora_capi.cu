@@ -1050,6 +1050,24 @@ int tlora_plan_get_tiles(const tlora_plan* plan, int launch, tlora_tile* out, in
   });
 }
 
+int tlora_plan_read_device(const tlora_plan* plan, int launch, tlora_tile* out, int32_t cap,
+                           int32_t* count, int32_t* token_slot) {
+  return guarded([&] {
+    require(plan != nullptr, TLORA_ERR_ARG, "plan is null");
+    require(launch >= 0 && launch < TLORA_L_COUNT, TLORA_ERR_ARG, "unknown launch id");
+    DeviceGuard g(plan->device);
+    const int32_t n = (int32_t)plan->P.tiles[launch].size();
+    if (count) *count = n;
+    const int32_t m = std::min(cap, n);
+    if (out && m > 0)
+      TL_CUDA(cudaMemcpy(out, plan->tiles[launch].p, (size_t)m * sizeof(tlora_tile),
+                         cudaMemcpyDeviceToHost));
+    if (token_slot)
+      TL_CUDA(cudaMemcpy(token_slot, plan->token_slot.p, (size_t)plan->P.T * sizeof(int32_t),
+                         cudaMemcpyDeviceToHost));
+  });
+}
+
 int tlora_plan_tiles_host(int64_t d, int64_t k, int32_t num_slots, const int32_t* ranks,
                           int64_t tokens, const int32_t* token_slot, int launch, tlora_tile* out,
                           int32_t cap, int32_t* count) {

@@ -84,6 +84,16 @@ class Plan:
         arr = np.frombuffer(buf, dtype=np.int32).reshape(-1, 8)[: n.value]
         return arr.copy()
 
+    def device_tiles(self, launch: int):
+        """(tile table as uploaded, token slots as uploaded), read back from device memory."""
+        n = C.c_int32()
+        call("tlora_plan_read_device", self._h, launch, None, 0, C.byref(n), None)
+        buf = (capi.TileC * max(1, n.value))()
+        slots = np.empty(self.tokens, np.int32)
+        call("tlora_plan_read_device", self._h, launch, buf, n.value, C.byref(n),
+             slots.ctypes.data)
+        return np.frombuffer(buf, dtype=np.int32).reshape(-1, 8)[: n.value].copy(), slots
+
     def close(self):
         if getattr(self, "_h", None):
             capi.lib().tlora_plan_destroy(self._h)

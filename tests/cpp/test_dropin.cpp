@@ -168,6 +168,25 @@ void cpu_costs() {  // test_fused_lora.cpp:115-136
   CHECK(trainable_param_count(job) == 4LL * (64 + 64) * 4);
 }
 
+void cpu_projection_layer_set() {  // projection-level SSM extension (ssm_plan.hpp)
+  auto m = tiny_model();
+  std::vector<JobSpec> group = {make_job("b", m, 8), make_job("a", m, 4), make_job("c", m, 16)};
+  auto projs = decoder_projections(64, 64, 16, 128);
+  CHECK(projs.size() == 7 && projs[6].name == "down" && projs[6].d == 128);
+  auto s = fuse_projections(group, projs);
+  CHECK((int)s.branches.size() == m.num_layers * 7 * 3);
+  CHECK(s.branches[0].job_id == "a" && s.branches[0].slot == 0 && s.branches[0].projection == 0);
+  CHECK(s.branches[2].job_id == "c" && s.branches[2].slot == 2);
+  CHECK(s.branches[3].projection == 1 && s.branches[3].job_id == "a");
+  // one projection {hidden -> proj} reproduces the reference's count
+  const auto& job = group[0];
+  CHECK(trainable_param_count(job, {{"x", m.hidden_dim, m.proj_dim}}) == trainable_param_count(job));
+  long long dk = 0;
+  for (const auto& p : projs) dk += p.d + p.k;
+  CHECK(trainable_param_count(job, projs) == 8LL * dk * m.num_layers);
+  CHECK(throws_with<std::invalid_argument>([&] { fuse_projections(group, {}); }, ""));
+}
+
 void cpu_comm_arguments() {  // communicator handle: argument errors surface as exceptions
   lora_fleet::Communicator::Id id{};
   CHECK(throws_with<std::runtime_error>([&] { lora_fleet::Communicator c(0, id, 4, 0, 3); },
@@ -310,6 +329,7 @@ int main(int argc, char** argv) {
     cases.push_back({"fused cost dominates unfused; param/flop counts", cpu_costs});
     cases.push_back({"partition / aimd_step / fuse", cpu_nano_and_fuse});
     cases.push_back({"communicator argument errors", cpu_comm_arguments});
+    cases.push_back({"projection-level layer set", cpu_projection_layer_set});
   }
   if (mode == "gpu" || mode == "all") {
     cases.push_back({"fused_forward matches the materialized oracle", gpu_matches_oracle});

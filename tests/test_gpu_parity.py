@@ -458,3 +458,28 @@ def test_gemm_shrink_zero_next_clears_garbage():
     assert torch.equal(dXa, dXb) and torch.equal(dHa, dHb)
     for lay in lays:
         lay.close()
+
+
+def test_uploaded_plan_is_bit_identical_to_plan_oracle():
+    """What the kernels actually read: every tile table and the token-slot array copied
+    back from device memory (tlora_plan_read_device) memcmp-equal to the plan oracle
+    (bit-exact plan + owner-id readback)."""
+    rs = np.random.RandomState(4)
+    c2 = config("C2")
+    cases = [(1024, 1024, [8, 16, 32, 64], rs.randint(0, 4, 7680).astype(np.int32)),
+             (4096, 4096, c2.ranks, c2.token_slots()),
+             (256, 264, [4, 256, 8, 1], np.array([1] * 300 + [3] * 5, np.int32))]
+    dev = torch.device("cuda", 0)
+    for d, k, ranks, slots in cases:
+        lay = FusedLoRALayer(d, k, ranks)
+        lay.set_base(torch.zeros(d, k, dtype=torch.bfloat16, device=dev))
+        for s_, r in enumerate(ranks):
+            lay.set_adapter(s_, torch.zeros(d, r, dtype=torch.bfloat16, device=dev),
+                            torch.zeros(r, k, dtype=torch.bfloat16, device=dev))
+        plan = lay.plan(slots)
+        for launch in range(8):
+            tiles, dev_slots = plan.device_tiles(launch)
+            want = O.plan_tiles(len(slots), d, k, ranks, slots, launch)
+            assert tiles.shape == want.shape and np.array_equal(tiles, want), (d, k, launch)
+            assert np.array_equal(dev_slots, slots)
+        lay.close()
