@@ -559,6 +559,18 @@ def run_tp(args, rank, world, local_rank):
     cnt, ms6, fl6 = (C.c_int32 * 6)(), (C.c_double * 6)(), (C.c_double * 6)()
     capi.call("tlora_profile_end", cnt, ms6, fl6)
     prof_ms = e2.elapsed_time(e3)
+    # one traced step: per nano-batch compute / boundary-traffic intervals -> the reference's
+    # PipelineTrace and monitor() reading (nano_pipeline.hpp:28-34, 114-126), measured
+    st.enable_trace(True)
+    e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e4.record(stream)
+    st.step(st.n)
+    e5.record(stream)
+    torch.cuda.synchronize()
+    reading = st.trace_reading(e4.elapsed_time(e5))
+    st.enable_trace(False)
+    reading = {k: (round(v, 6) if isinstance(v, float) else [round(x, 6) for x in v])
+               for k, v in reading.items()}
     fam_ms, fam_fl = ms6[capi.L_FWD] + ms6[capi.L_DX], fl6[capi.L_FWD] + fl6[capi.L_DX]
     peaks = load_peaks()
     peak = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
@@ -586,6 +598,7 @@ def run_tp(args, rank, world, local_rank):
                    "achieved_tflops_per_gpu": round(flops / world / (ms_per_step / 1e3) / 1e12, 1)},
         "gpu_launches": n_launch,
         "roofline": roofline,
+        "pipeline_monitor": reading,
         "clocks": clk,
     }
 

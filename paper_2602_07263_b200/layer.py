@@ -317,6 +317,16 @@ def segments(token_slot, num_slots: int):
     return perm, offsets
 
 
+def monitor(t_comp, t_comm, t_iter_event: float, t_iter_analytic: float, num_stages: int = 1):
+    """nano_pipeline.hpp:114-126 MonitorReading of a PipelineTrace (:28-34): eta_util =
+    sum(t_comp) / (num_stages * t_iter_event) (0 if t_iter_event <= 0 or no stages),
+    delta_stall = t_iter_event - t_iter_analytic. t_comm is part of the trace but, as in
+    the reference, does not enter the reading."""
+    sum_c = float(sum(t_comp))
+    eta = sum_c / (num_stages * t_iter_event) if t_iter_event > 0.0 and num_stages > 0 else 0.0
+    return eta, t_iter_event - t_iter_analytic
+
+
 def partition(group_batch: int, n: int):
     """nano_pipeline.hpp:51-60 — returns (n, per_nano_samples)."""
     out_n = C.c_int32()

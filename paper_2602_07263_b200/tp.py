@@ -214,6 +214,43 @@ class TPLayerSetStep:
     def _rs(self, out, inp):
         dist.reduce_scatter_tensor(out, inp, group=self.group)
 
+    # -------------------------------------------------------------- pipeline trace
+    def enable_trace(self, on: bool = True):
+        """Record CUDA events around every nano-batch's compute (compute stream) and
+        boundary traffic (comm stream) — the measured PipelineTrace of the reference's
+        monitor (nano_pipeline.hpp:28-34, 114-126)."""
+        self._trace = {} if on else None
+
+    def _mark(self, stream, kind: str, i: int, edge: int):
+        tr = getattr(self, "_trace", None)
+        if tr is None:
+            return
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        tr.setdefault((kind, i), [None, None])[edge] = e
+
+    def trace_reading(self, step_ms: float):
+        """PipelineTrace of the last traced step (seconds): t_comp / t_comm per nano-batch
+        (forward + backward intervals summed), t_iter_event = the measured step time,
+        t_iter_analytic = max(sum t_comp, sum t_comm) (the overlap ideal); and the
+        reference's monitor() of it."""
+        torch.cuda.synchronize(self.dev)
+        comp, comm = {}, {}
+        for (kind, i), (e0, e1) in self._trace.items():
+            if e0 is None or e1 is None:
+                continue
+            dst = comp if kind.startswith("comp") else comm
+            dst[i] = dst.get(i, 0.0) + e0.elapsed_time(e1) / 1e3
+        n = max(list(comp) + list(comm)) + 1 if comp or comm else 0
+        t_comp = [comp.get(i, 0.0) for i in range(n)]
+        t_comm = [comm.get(i, 0.0) for i in range(n)]
+        t_event = step_ms / 1e3
+        t_analytic = max(sum(t_comp), sum(t_comm))
+        from .layer import monitor
+        eta, stall = monitor(t_comp, t_comm, t_event, t_analytic, num_stages=1)
+        return {"t_comp_s": t_comp, "t_comm_s": t_comm, "t_iter_event_s": t_event,
+                "t_iter_analytic_s": t_analytic, "eta_util": eta, "delta_stall_s": stall}
+
     # -------------------------------------------------------------- forward
     def forward(self, n: int | None = None):
         n = self.n if n is None else n
@@ -240,11 +277,13 @@ class TPLayerSetStep:
         def gather(i, ev):
             b = nb[i]
             M.wait_event(ev)
+            self._mark(M, "comm_ag_f", i, 0)
             with torch.cuda.stream(M):
                 for g in self.groups:
                     self._ag(self._rows(self.X_full[g], b), self._srows(self.X_shard[g], b))
                 for p in cols:
                     self._ag(self._rows(self.H_full[p], b), self._srows(self.H_shard[p], b))
+            self._mark(M, "comm_ag_f", i, 1)
             ev2 = torch.cuda.Event()
             ev2.record(M)
             return ev2
@@ -254,6 +293,7 @@ class TPLayerSetStep:
             ev_next = gather(i + 1, shrink(i + 1)) if i + 1 < len(nb) else None
             b = nb[i]
             C.wait_event(ev_g)
+            self._mark(C, "comp_f", i, 0)
             for p in cols:
                 self.layers[p].fused_gemm(plans[i][p][0], self._rows(self.X_full[INPUT_GROUP[p]], b),
                                           self._rows(self.H_full[p], b), self._rows(self.Y[p], b),
@@ -270,9 +310,11 @@ class TPLayerSetStep:
                 else:
                     lay.fused_gemm(pl, self._rows(self.X_loc[p], b), self._rows(self.H_row[p], b),
                                    self._rows(self.Y_part[p], b), stream=C)
+            self._mark(C, "comp_f", i, 1)
             ev_y = torch.cuda.Event()
             ev_y.record(C)
             M.wait_event(ev_y)
+            self._mark(M, "comm_rs_f", i, 0)
             with torch.cuda.stream(M):  # off the compute stream: overlaps nano n+1's GEMMs
                 for p in rows:
                     if p in self.fused_set:  # data already moved by the GEMM: barrier + sum
@@ -283,6 +325,7 @@ class TPLayerSetStep:
                                      stream=M)
                     else:
                         self._rs(self._srows(self.Y_shard[p], b), self._rows(self.Y_part[p], b))
+            self._mark(M, "comm_rs_f", i, 1)
             ev_g = ev_next
         C.wait_stream(M)
 
@@ -305,9 +348,11 @@ class TPLayerSetStep:
         def gather_dy(i):
             b = nb[i]
             M.wait_event(start)
+            self._mark(M, "comm_ag_b", i, 0)
             with torch.cuda.stream(M):
                 for p in rows:
                     self._ag(self._rows(self.dY_full[p], b), self._srows(self.dY_shard[p], b))
+            self._mark(M, "comm_ag_b", i, 1)
             ev = torch.cuda.Event()
             ev.record(M)
             return ev
@@ -327,6 +372,7 @@ class TPLayerSetStep:
             b = nb[i]
             beta = 1.0 if i else 0.0
             C.wait_event(ev_dy)
+            self._mark(C, "comp_b", i, 0)
             # Chained schedule (as runner.LayerSetStep): each dX launch also computes the
             # NEXT projection's dH as extra tiles (tlora_backward_dx_dh), so only the first
             # dH of the nano-batch has a launch of its own. Order: row-parallel projections,
@@ -364,14 +410,17 @@ class TPLayerSetStep:
                               dHp, beta=beta, stream=G)
                 else:
                     lay.grad_b(pl, self._rows(self.H_full[p], b), dYp, beta=beta, stream=G)
+            self._mark(C, "comp_b", i, 1)
             ev_c = torch.cuda.Event()
             ev_c.record(C)
             M.wait_event(ev_c)
+            self._mark(M, "comm_rs_b", i, 0)
             with torch.cuda.stream(M):
                 for g in self.groups:
                     self._rs(self._srows(self.dX_shard[g], b), self._rows(self.dX_part[g], b))
                 for p in cols:
                     self._rs(self._srows(self.dH_shard[p], b), self._rows(self.dH_part[p], b))
+            self._mark(M, "comm_rs_b", i, 1)
             ev_r = torch.cuda.Event()
             ev_r.record(M)
             if pending is not None:

@@ -104,3 +104,13 @@ def test_tp_parity_multi_gpu():
                        capture_output=True, text=True, timeout=900)
     print(p.stdout[-3000:])
     assert p.returncode == 0 and "TP_CHECK PASS" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+def test_monitor_restates_reference():
+    """monitor() == nano_pipeline.hpp:114-126 on hand-built traces, including the degenerate
+    ones (zero event time, zero stages)."""
+    from paper_2602_07263_b200.layer import monitor
+    eta, stall = monitor([1.0, 2.0, 3.0], [0.5, 0.5, 0.5], 8.0, 6.0, num_stages=2)
+    assert eta == 6.0 / 16.0 and stall == 2.0
+    assert monitor([1.0], [1.0], 0.0, 1.0) == (0.0, -1.0)
+    assert monitor([1.0], [1.0], 2.0, 1.0, num_stages=0) == (0.0, 1.0)
