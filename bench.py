@@ -135,6 +135,27 @@ class ClockSampler:
                 "window": "settle steps + timed region" if window is not None else "whole run"}
 
 
+def bind_host_numa(device: int):
+    """Pin this process to the CPUs NVML reports as closest to `device` (NVML CPU
+    affinity), so the pinned host buffers of the e2e path are first-touched on the GPU's
+    own NUMA node and its host->device copies do not cross the inter-socket link."""
+    try:
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(device).uuid)
+        h = pynvml.nvmlDeviceGetHandleByUUID(uuid.encode())
+        n = (os.cpu_count() + 63) // 64
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, n)
+        cpus = {64 * w + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return sorted(cpus)
+    except Exception:
+        return None
+
+
 # ------------------------------------------------------------------------------ CPU arm
 def cpu_reference_sample(wl, tokens_per_job: int, seconds_budget: float, threads: int):
     """Time the reference CPU implementation of the path on a bounded sample.
@@ -334,6 +355,7 @@ def run_ours(args, rank, world, local_rank):
     # adapter gradients. Inputs are double-buffered on a copy stream so the H2D of step i+1
     # overlaps the compute of step i; step i+1's backward waits for the D2H of step i.
     dev_sets = step.make_input_sets(2)
+    bind_host_numa(local_rank)  # pinned host buffers on the GPU's own NUMA node
     host_in = [t.cpu().pin_memory() for t in dev_sets[0]]
     grads = [g for lay in step.layers.values() for g in lay.packed_grads()]
     host_out = [torch.empty(g.shape, dtype=g.dtype, pin_memory=True) for g in grads]
