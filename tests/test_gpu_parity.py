@@ -483,3 +483,20 @@ def test_uploaded_plan_is_bit_identical_to_plan_oracle():
             assert tiles.shape == want.shape and np.array_equal(tiles, want), (d, k, launch)
             assert np.array_equal(dev_slots, slots)
         lay.close()
+
+
+@pytest.mark.parametrize("shape", [("C3", "gate"), ("C3", "down"), ("C4", "q"), ("C4", "down"),
+                                   ("C2", "k")])
+def test_model_projection_shapes(shape):
+    """The real projection shapes of the Llama-3-8B (C3) and Qwen3-32B (C4) stacks and
+    Qwen3-8B's narrow k projection, with each config's 16 / 8 heterogeneous jobs on a
+    small ragged token batch (10-30 tokens per job, not tile multiples), vs the oracle."""
+    name, proj = shape
+    wl = config(name)
+    _, d, k = [p for p in wl.projections if p[0] == proj][0]
+    rs = np.random.RandomState(len(proj) + d)
+    counts = [int(rs.randint(10, 30)) for _ in wl.jobs]
+    X, W, A, B, slots, dY = _random_problem(sum(counts), d, k, wl.ranks, counts=counts,
+                                            seed=d + k)
+    got = gpu_run(X, W, A, B, slots, dY)
+    check(got, X, W, A, B, slots, dY)
