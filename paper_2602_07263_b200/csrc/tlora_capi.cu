@@ -456,6 +456,29 @@ __global__ void read_grad_kernel(const float* dAT, const float* dBc, int64_t d, 
 }
 
 // Two reductions in one launch: problem j covers R x N_j; index space concatenated.
+// out[i, :] = in[perm[i], :] for up to four bf16 row-major tensors (row widths in 16-byte
+// units): the job-sorted operand copies of an interleaved batch's gradient launches.
+struct GatherJob {
+  const uint4* src;
+  uint4* dst;
+  int64_t w16;
+};
+__global__ void gather_rows_kernel(GatherJob j0, GatherJob j1, GatherJob j2, GatherJob j3,
+                                   const int32_t* __restrict__ perm, int64_t rows) {
+  const GatherJob js[4] = {j0, j1, j2, j3};
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int q = 0; q < 4; ++q) {
+    const GatherJob& J = js[q];
+    if (!J.src) continue;
+    const int64_t n = rows * J.w16;
+    for (int64_t i = tid; i < n; i += stride) {
+      const int64_t r = i / J.w16, c = i % J.w16;
+      J.dst[i] = J.src[(int64_t)perm[r] * J.w16 + c];
+    }
+  }
+}
+
 struct ReduceJob {
   const float* partial;
   const int32_t* cnt;
@@ -568,17 +591,18 @@ namespace {
 // only happens while shapes are first seen, so a warmed-up step can be captured in a
 // CUDA graph (capture may run on a different stream than the warm-up).
 struct Workspace {
-  DevBuf<char> partial, dh;
+  DevBuf<char> partial, dh, gather;
 };
 std::mutex g_ws_mu;
 std::map<int, std::unique_ptr<Workspace>> g_ws;
 
 template <class T>
-T* ws_get(int device, cudaStream_t s, bool dh, size_t count) {
+T* ws_get(int device, cudaStream_t s, int kind, size_t count) {  // kind: 0 partial, 1 dH, 2 gather
   std::lock_guard<std::mutex> lk(g_ws_mu);
   auto& w = g_ws[device];
   if (!w) w = std::make_unique<Workspace>();
-  DevBuf<char>& b = dh ? w->dh : w->partial;
+  const bool dh = kind == 1;
+  DevBuf<char>& b = kind == 0 ? w->partial : kind == 1 ? w->dh : w->gather;
   const size_t bytes = count * sizeof(T);
   if (b.n < bytes) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -600,6 +624,14 @@ struct tlora_plan {
   tlora::PlanTables P;
   DevBuf<TileDesc> tiles[TLORA_L_COUNT];
   DevBuf<int32_t> token_slot, cnt_db, cnt_da;
+  // Interleaved batches (some job's token range also holds other jobs' tokens): the
+  // per-job gradient launches would stream every interleaved row once per job. They run
+  // instead on job-sorted gathered copies (stable order: rows keep their order within a
+  // job) with the gradient tables of the sorted order's plan.
+  bool interleaved = false;
+  tlora::PlanTables Ps;             // plan of the job-sorted token order (grad tables used)
+  DevBuf<TileDesc> stiles[2];       // Ps.tiles[TLORA_L_DB], Ps.tiles[TLORA_L_DA]
+  DevBuf<int32_t> scnt_db, scnt_da, perm;  // sorted row i <- token perm[i]
 };
 
 namespace {
@@ -1004,6 +1036,37 @@ int tlora_plan_create(tlora_layer* layer, int64_t tokens, const int32_t* token_s
     }
     plan->token_slot.alloc(tokens);
     TL_CUDA(cudaMemcpy(plan->token_slot.p, token_slot, tokens * 4, cudaMemcpyHostToDevice));
+    {
+      const auto& P = plan->P;
+      const int S = (int)layer->L.rank.size();
+      std::vector<int64_t> cnt(S + 1, 0);
+      for (int64_t t = 0; t < tokens; ++t) ++cnt[token_slot[t] + 1];
+      for (int s_ = 0; s_ < S; ++s_)
+        if (P.slot_first[s_] >= 0 && P.slot_last[s_] + 1 - P.slot_first[s_] > cnt[s_ + 1])
+          plan->interleaved = true;
+      if (plan->interleaved) {
+        for (int s_ = 0; s_ < S; ++s_) cnt[s_ + 1] += cnt[s_];
+        std::vector<int32_t> perm(tokens), sorted(tokens);
+        for (int64_t t = 0; t < tokens; ++t) perm[cnt[token_slot[t]]++] = (int32_t)t;
+        for (int64_t i = 0; i < tokens; ++i) sorted[i] = token_slot[perm[i]];
+        plan->Ps = tlora::build_plan(layer->L, tokens, sorted.data());
+        for (int w = 0; w < 2; ++w) {
+          const auto& v = plan->Ps.tiles[w == 0 ? TLORA_L_DB : TLORA_L_DA];
+          plan->stiles[w].alloc(v.size());
+          if (!v.empty())
+            TL_CUDA(cudaMemcpy(plan->stiles[w].p, v.data(), v.size() * sizeof(TileDesc),
+                               cudaMemcpyHostToDevice));
+        }
+        plan->scnt_db.alloc(plan->Ps.split_count_db.size());
+        TL_CUDA(cudaMemcpy(plan->scnt_db.p, plan->Ps.split_count_db.data(),
+                           plan->Ps.split_count_db.size() * 4, cudaMemcpyHostToDevice));
+        plan->scnt_da.alloc(plan->Ps.split_count_da.size());
+        TL_CUDA(cudaMemcpy(plan->scnt_da.p, plan->Ps.split_count_da.data(),
+                           plan->Ps.split_count_da.size() * 4, cudaMemcpyHostToDevice));
+        plan->perm.alloc(tokens);
+        TL_CUDA(cudaMemcpy(plan->perm.p, perm.data(), tokens * 4, cudaMemcpyHostToDevice));
+      }
+    }
     plan->cnt_db.alloc(plan->P.split_count_db.size());
     TL_CUDA(cudaMemcpy(plan->cnt_db.p, plan->P.split_count_db.data(),
                        plan->P.split_count_db.size() * 4, cudaMemcpyHostToDevice));
@@ -1234,16 +1297,42 @@ void run_grads(tlora_layer* layer, const tlora_plan* plan, const void* H, const 
   ReduceJob rj[2] = {};
   const bool on[2] = {do_b, do_a};
   const int64_t Ns[2] = {L.k, L.d};
-  const int nsp[2] = {plan->P.splits_db, plan->P.splits_da};
+  // interleaved batch: gather job-sorted copies of the operands, use the sorted plan
+  const bool srt = plan->interleaved;
+  const tlora::PlanTables& PT = srt ? plan->Ps : plan->P;
+  const int nsp[2] = {PT.splits_db, PT.splits_da};
   float* grads[2] = {layer->dB.p, layer->dAT.p};
-  const int32_t* cnts[2] = {plan->cnt_db.p, plan->cnt_da.p};
+  const int32_t* cnts[2] = {srt ? plan->scnt_db.p : plan->cnt_db.p,
+                            srt ? plan->scnt_da.p : plan->cnt_da.p};
   const void* full[2] = {dY, X};
   const void* low[2] = {H, dH};
+  if (srt) {
+    const int64_t widths[4] = {L.k, R, L.d, R};  // dY, H, X, dH (bf16 row widths)
+    const void* src[4] = {dY, H, X, dH};
+    size_t total = 0;
+    for (int q = 0; q < 4; ++q)
+      if (on[q / 2]) total += (size_t)T * widths[q];
+    __nv_bfloat16* gbuf = ws_get<__nv_bfloat16>(layer->device, s, 2, total);
+    GatherJob jobs[4] = {};
+    size_t o = 0;
+    for (int q = 0; q < 4; ++q) {
+      if (!on[q / 2]) continue;
+      jobs[q] = {reinterpret_cast<const uint4*>(src[q]), reinterpret_cast<uint4*>(gbuf + o),
+                 widths[q] / 8};
+      (q % 2 == 0 ? full : low)[q / 2] = gbuf + o;
+      o += (size_t)T * widths[q];
+    }
+    const int64_t work = T * ((on[0] ? L.k + R : 0) + (on[1] ? L.d + R : 0)) / 8;
+    const int blocks = (int)std::min<int64_t>(tlora::ceil_div(work, 256), 8 * layer->sm_count);
+    gather_rows_kernel<<<blocks, 256, 0, s>>>(jobs[0], jobs[1], jobs[2], jobs[3], plan->perm.p, T);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    TL_CUDA(cudaGetLastError());
+  }
   // workspace: [problem 0 planes][problem 1 planes]
   size_t need = 0;
   for (int j = 0; j < 2; ++j)
     if (on[j] && nsp[j] > 1) need += (size_t)nsp[j] * R * Ns[j];
-  float* ws = need ? ws_get<float>(layer->device, s, false, need) : nullptr;
+  float* ws = need ? ws_get<float>(layer->device, s, 0, need) : nullptr;
   size_t off = 0;
   double flops = 0.0;
   for (int j = 0; j < 2; ++j) {
@@ -1256,8 +1345,8 @@ void run_grads(tlora_layer* layer, const tlora_plan* plan, const void* H, const 
       continue;
     }
     const int64_t N = Ns[j];
-    a.tiles = plan->tiles[launch].p;
-    a.num_tiles = (int)plan->P.tiles[launch].size();
+    a.tiles = srt ? plan->stiles[j].p : plan->tiles[launch].p;
+    a.num_tiles = (int)PT.tiles[launch].size();
     a.M = (int)N;  // transposed form: M = layer dimension, output rows = packed rank columns
     a.N = (int)N;
     a.ldo = N;
@@ -1443,7 +1532,7 @@ int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, c
     DeviceGuard g(layer->device);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     __nv_bfloat16* dH =
-        ws_get<__nv_bfloat16>(layer->device, s, true, (size_t)plan->P.T * layer->L.R);
+        ws_get<__nv_bfloat16>(layer->device, s, 1, (size_t)plan->P.T * layer->L.R);
     run_dh(layer, plan, dY, dH, s);
     if (dX) run_dx(layer, plan, dY, dH, dX, 0.f, s);
     run_grads(layer, plan, H_stash, dY, dH, X, true, true, beta, s);
