@@ -92,8 +92,8 @@ def main():
     A = np.array([[2.0, r["gemm_flops"]] for r in grid])
     y = np.array([r["gemm_ms"] * 1e-3 for r in grid])
     (g_over, g_inv), *_ = np.linalg.lstsq(A, y, rcond=None)
-    # low-rank launches: t = a + bytes / BW (four launches per step)
-    A2 = np.array([[4.0, r["lowrank_bytes"]] for r in grid])
+    # low-rank launches: t = a + bytes / BW (three per step: shrink, dH, dB+dA)
+    A2 = np.array([[3.0, r["lowrank_bytes"]] for r in grid])
     y2 = np.array([r["lowrank_ms"] * 1e-3 for r in grid])
     (l_over, l_inv), *_ = np.linalg.lstsq(A2, y2, rcond=None)
     F, BW = 1.0 / g_inv, 1.0 / l_inv
@@ -101,13 +101,13 @@ def main():
     other_per_byte = np.median([o / r["optimizer_bytes"] for o, r in zip(other, grid)])
 
     def predict(r):
-        return (2 * g_over + r["gemm_flops"] / F + 4 * l_over + r["lowrank_bytes"] / BW
+        return (2 * g_over + r["gemm_flops"] / F + 3 * l_over + r["lowrank_bytes"] / BW
                 + other_per_byte * r["optimizer_bytes"])
 
     errs = [abs(predict(r) - r["step_ms"] * 1e-3) / (r["step_ms"] * 1e-3) for r in grid]
     out = {
         "device": torch.cuda.get_device_name(0),
-        "model": "step_s = 2*gemm_overhead + gemm_flops/F + 4*lowrank_overhead + "
+        "model": "step_s = 2*gemm_overhead + gemm_flops/F + 3*lowrank_overhead + "
                  "lowrank_bytes/BW + optimizer_s_per_byte*optimizer_bytes",
         "F_flops_per_s": F, "gemm_launch_overhead_s": g_over,
         "BW_bytes_per_s": BW, "lowrank_launch_overhead_s": l_over,
@@ -115,7 +115,7 @@ def main():
         "fit_rel_err_median": float(np.median(errs)), "fit_rel_err_max": float(np.max(errs)),
         "hardware_spec": {  # drop-in values for proj/include/lora_fleet/hardware.hpp
             "gpu_flops": F,
-            "kernel_launch_overhead": float((2 * g_over + 4 * l_over) / 6),
+            "kernel_launch_overhead": float((2 * g_over + 3 * l_over) / 5),
             "note": "gpu_flops = sustained fused base+LoRA GEMM rate under the 1 kW cap; "
                     "kernel_launch_overhead = mean fixed cost per fused-layer launch"},
         "grid": grid,
