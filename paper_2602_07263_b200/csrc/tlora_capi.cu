@@ -1167,10 +1167,29 @@ void check_bound(const tlora_layer* layer, const tlora_plan* plan) {
 // H = X·Aᵀcatᵀ masked to each token's own packed columns. Shrink tiles write only their
 // token tile's rank window; the gradient launches read H over whole job token ranges, so
 // every other column must be an exact zero (memset first).
+Gemm2Secondary make_lowrank2(tlora_layer* layer, const tlora_plan* plan, int which, const void* A,
+                             void* out);
+void launch_lowrank_pairs(tlora_layer* layer, const Gemm2Secondary& sec, int kind, cudaStream_t s);
+
+// Standalone shrink / dH on CTA pairs (the SHRINK2 / DH2 tables, lora_gemm2_kernel with no
+// main tiles) instead of the 1-CTA kernel; identical results (same K order per element).
+// TLORA_LOWRANK_PAIR=0 selects the 1-CTA kernel.
+bool lowrank_pairs() {
+  static const bool on = [] {
+    const char* e = std::getenv("TLORA_LOWRANK_PAIR");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
 void run_shrink(tlora_layer* layer, const tlora_plan* plan, const void* X, void* H, cudaStream_t s) {
   const auto& L = layer->L;
   const int64_t T = plan->P.T, d = L.d, R = L.R;
   TL_CUDA(cudaMemsetAsync(H, 0, (size_t)T * R * 2, s));
+  if (lowrank_pairs()) {
+    launch_lowrank_pairs(layer, make_lowrank2(layer, plan, 0, X, H), TLORA_L_SHRINK, s);
+    return;
+  }
   GemmArgs a{};
   a.tiles = plan->tiles[TLORA_L_SHRINK].p;
   a.num_tiles = (int)plan->P.tiles[TLORA_L_SHRINK].size();
@@ -1213,6 +1232,16 @@ Gemm2Secondary make_lowrank2(tlora_layer* layer, const tlora_plan* plan, int whi
   return g;
 }
 
+void launch_lowrank_pairs(tlora_layer* layer, const Gemm2Secondary& sec, int kind,
+                          cudaStream_t s) {
+  GemmArgs none{};  // no main tiles: every tile of the launch is a secondary (low-rank) tile
+  Gemm2Secondary g = sec;
+  const double flops = g.flops;
+  g.flops = 0.0;
+  launch_gemm2<tlora::EPI_BF16, TLORA_GEMM2_STAGES>(g.a, g.b, g.a, g.b, none, layer->sm_count, s,
+                                                    kind, flops, &g);
+}
+
 // Y = X·W + H·Bᵀcatᵀ: 2-CTA fused GEMM, K-extension over each tile's packed-rank window.
 void run_fwd_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X, const void* H, void* Y,
                   int y_dtype, cudaStream_t s, const Gemm2Secondary* sec = nullptr) {
@@ -1244,6 +1273,10 @@ void run_dh(tlora_layer* layer, const tlora_plan* plan, const void* dY, void* dH
   const auto& L = layer->L;
   const int64_t T = plan->P.T, k = L.k, R = L.R;
   TL_CUDA(cudaMemsetAsync(dH, 0, (size_t)T * R * 2, s));
+  if (lowrank_pairs()) {
+    launch_lowrank_pairs(layer, make_lowrank2(layer, plan, 1, dY, dH), TLORA_L_DH, s);
+    return;
+  }
   GemmArgs a{};
   a.tiles = plan->tiles[TLORA_L_DH].p;
   a.num_tiles = (int)plan->P.tiles[TLORA_L_DH].size();
