@@ -191,6 +191,13 @@ int tlora_forward_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X
  * recv_ptrs[world]: every rank's receive buffer [world][slot_rows][k] bf16 (peer-mapped,
  * e.g. symmetric memory); this rank writes slot `rank`, rows dst_row0 + r % (T / world).
  * After a cross-rank barrier, tlora_reduce_slots sums the slots in fixed order. */
+/* tlora_forward_gemm with the dH of `next` (dH_next = dY_next·Bᵀcat masked, as
+ * tlora_backward_dh) as extra tiles: a training step's LAST forward launch can carry the
+ * FIRST dH of its backward (dY is an input of the step). zero_next as above. */
+int tlora_forward_gemm_dh(tlora_layer* layer, const tlora_plan* plan, const void* X,
+                          const void* H, void* Y, int y_dtype, tlora_layer* next,
+                          const tlora_plan* next_plan, const void* dY_next, void* dH_next,
+                          int zero_next, void* stream);
 /* tlora_forward_gemm of `layer` with the shrink of `next` (H_next = X_next·Aᵀcat masked, as
  * tlora_forward_shrink) carried as extra CTA-pair tiles of the SAME launch (plan table
  * TLORA_L_SHRINK2 of next_plan), so the next projection's shrink fills this GEMM's tail

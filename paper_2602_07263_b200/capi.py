@@ -90,6 +90,8 @@ SIGNATURES = {
                                      C.c_int, C.c_void_p]),
     "tlora_forward_gemm_shrink": (C.c_int, [C.c_void_p] * 5 + [C.c_int] + [C.c_void_p] * 4
                                   + [C.c_int, C.c_void_p]),
+    "tlora_forward_gemm_dh": (C.c_int, [C.c_void_p] * 5 + [C.c_int] + [C.c_void_p] * 4
+                              + [C.c_int, C.c_void_p]),
     "tlora_forward_gemm_rs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int64,
                                         C.c_int64, C.c_void_p]),

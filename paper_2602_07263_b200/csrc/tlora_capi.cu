@@ -1496,6 +1496,32 @@ int tlora_forward_gemm_shrink(tlora_layer* layer, const tlora_plan* plan, const 
   });
 }
 
+int tlora_forward_gemm_dh(tlora_layer* layer, const tlora_plan* plan, const void* X,
+                          const void* H, void* Y, int y_dtype, tlora_layer* next,
+                          const tlora_plan* next_plan, const void* dY_next, void* dH_next,
+                          int zero_next, void* stream) {
+  return guarded([&] {
+    check_bound(layer, plan);
+    check_bound(next, next_plan);
+    check_align(X, "X");
+    check_align(H, "H");
+    check_align(Y, "Y");
+    check_align(dY_next, "dY_next");
+    check_align(dH_next, "dH_next");
+    require(y_dtype == TLORA_BF16 || y_dtype == TLORA_F32, TLORA_ERR_ARG,
+            "Y dtype must be bf16 or f32");
+    require(next->device == layer->device, TLORA_ERR_ARG, "layers on different devices");
+    require(dH_next != H && dH_next != Y && dH_next != X, TLORA_ERR_ARG,
+            "dH_next must not alias this layer's operands");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (zero_next)
+      TL_CUDA(cudaMemsetAsync(dH_next, 0, (size_t)next_plan->P.T * next->L.R * 2, s));
+    const Gemm2Secondary sec = make_lowrank2(next, next_plan, 1, dY_next, dH_next);
+    run_fwd_gemm(layer, plan, X, H, Y, y_dtype, s, &sec);
+  });
+}
+
 int tlora_forward_gemm_rs(tlora_layer* layer, const tlora_plan* plan, const void* X, const void* H,
                           void* const* recv_ptrs, int32_t world, int32_t rank, int64_t slot_rows,
                           int64_t dst_row0, void* stream) {

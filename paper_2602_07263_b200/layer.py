@@ -229,6 +229,13 @@ class FusedLoRALayer:
              _DT[Y.dtype], nxt._h, next_plan._h, _ptr(X_next), _ptr(H_next), int(zero_next),
              _stream_ptr(stream))
 
+    def fused_gemm_dh(self, plan: Plan, X, H, Y, nxt: "FusedLoRALayer", next_plan: Plan,
+                      dY_next, dH_next, zero_next=True, stream=None):
+        """fused_gemm of this layer + dh of `nxt` in one launch (tlora_forward_gemm_dh)."""
+        call("tlora_forward_gemm_dh", self._h, plan._h, _ptr(X), _ptr(H), _ptr(Y),
+             _DT[Y.dtype], nxt._h, next_plan._h, _ptr(dY_next), _ptr(dH_next), int(zero_next),
+             _stream_ptr(stream))
+
     def fused_gemm_rs(self, plan: Plan, X, H, recv_ptrs, rank, slot_rows, dst_row0, stream=None):
         """Row-parallel TP forward with the reduce-scatter fused into the epilogue (peer
         stores into every owner's receive slot); see tlora_forward_gemm_rs."""

@@ -78,12 +78,19 @@ class LayerSetStep:
 
     def forward(self, stream=None):
         if self.chain:
-            return self.forward_chained(stream)
+            import os
+            return self.forward_chained(stream, os.environ.get("TLORA_PREFETCH_DH", "1") != "0")
         for L, name in self.keys:
             self.layers[(L, name)].forward(self.plans[name], self.x_of(name), self.Y[name],
                                            self.H[(L, name)], stream=stream)
 
-    def forward_chained(self, stream=None):
+    def _first_dh_buffer(self):
+        return self.dH4[0] if getattr(self, "side_grads", False) else self.dH2[0]
+
+    def forward_chained(self, stream=None, prefetch_dh: bool = True):
+        """prefetch_dh: the last forward launch also computes the backward's first dH (the
+        last projection's, from its upstream gradient dY) as extra tiles
+        (tlora_forward_gemm_dh), so the backward starts with a fused dX launch."""
         keys = self.keys
         k0 = keys[0]
         self.layers[k0].shrink(self.plans[k0[1]], self.x_of(k0[1]), self.H[k0], stream=stream)
@@ -94,6 +101,11 @@ class LayerSetStep:
                 lay.fused_gemm_shrink(pl, self.x_of(name), self.H[(L, name)], self.Y[name],
                                       self.layers[nk], self.plans[nk[1]], self.x_of(nk[1]),
                                       self.H[nk], zero_next=False, stream=stream)
+            elif prefetch_dh:
+                lay.fused_gemm_dh(pl, self.x_of(name), self.H[(L, name)], self.Y[name], lay, pl,
+                                  self.dY[name], self._first_dh_buffer(), zero_next=False,
+                                  stream=stream)
+                self._dh_prefetched = True
             else:
                 lay.fused_gemm(pl, self.x_of(name), self.H[(L, name)], self.Y[name], stream=stream)
 
@@ -114,7 +126,9 @@ class LayerSetStep:
         side.wait_event(ev)  # adapters / grads of the previous step are settled
         done = {}            # key index -> event after its grads launch (side stream)
         k0 = keys[0]
-        self.layers[k0].dh(self.plans[k0[1]], self.dY[k0[1]], self.dH4[0], stream=main)
+        if not getattr(self, "_dh_prefetched", False):
+            self.layers[k0].dh(self.plans[k0[1]], self.dY[k0[1]], self.dH4[0], stream=main)
+        self._dh_prefetched = False
         for i, (L, name) in enumerate(keys):
             lay, pl = self.layers[(L, name)], self.plans[name]
             dH = self.dH4[i % 4]
@@ -146,7 +160,9 @@ class LayerSetStep:
                                        beta, on_layer_done, opt_inline)
         keys = list(reversed(self.keys))
         k0 = keys[0]
-        self.layers[k0].dh(self.plans[k0[1]], self.dY[k0[1]], self.dH2[0], stream=stream)
+        if not getattr(self, "_dh_prefetched", False):
+            self.layers[k0].dh(self.plans[k0[1]], self.dY[k0[1]], self.dH2[0], stream=stream)
+        self._dh_prefetched = False
         for i, (L, name) in enumerate(keys):
             lay, pl = self.layers[(L, name)], self.plans[name]
             dH = self.dH2[i % 2]
