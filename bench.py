@@ -93,6 +93,18 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def wait_ready(self, timeout_s: float = 20.0):
+        """Block until the sampler has written its first sample (bounded)."""
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < timeout_s:
+            try:
+                if os.path.getsize(self.out.name) > 0:
+                    return True
+            except OSError:
+                pass
+            time.sleep(0.05)
+        return False
+
     def stop(self, window=None):
         """window = (t_start, t_end) wall-clock seconds: statistics over the samples taken
         inside it (the settle steps + the timed region); all samples if it holds < 3."""
@@ -117,6 +129,9 @@ class ClockSampler:
                     rows.append((float(p[1]), float(p[2]), float(p[3]), int(p[4], 0), ts))
                 except (ValueError, IndexError):
                     pass
+        if os.environ.get("TLORA_CLOCK_DUMP"):  # debugging aid: keep the raw samples
+            import shutil
+            shutil.copy(self.out.name, os.environ["TLORA_CLOCK_DUMP"])
         os.unlink(self.out.name)
         n_all = len(rows)
         if window is not None:
@@ -181,6 +196,10 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     capi.call("tlora_device_check", local_rank, None)
+    # the sampler process needs a few seconds to come up: start it before building the
+    # layer set so it is sampling well before the warm-up / settle / timed steps
+    clocks = ClockSampler(local_rank)
+    clocks.start()
     wl = config(args.config)
     if args.layers > 0:  # e.g. one layer of C4's 64-layer stack on a single GPU
         wl.layers = args.layers
@@ -281,25 +300,25 @@ def run_ours(args, rank, world, local_rank):
         if not opt_inline:
             step.optimizer_step(stream, grad_scale=1.0 / world)
 
-    clocks = ClockSampler(local_rank)
-    clocks.start()
-    t_w = time.perf_counter()
+    clocks.wait_ready()
     for i in range(args.warmup):
         one_step(last=i == args.warmup - 1)  # the profiled graph is uploaded / warm too
     torch.cuda.synchronize()
-    # untimed steps for ~1 s more: clocks settle and get sampled. The count must be the
-    # SAME on every rank (each DP step issues collectives; a time-based loop let ranks
-    # disagree by one step and deadlock), so it is agreed with a MAX all-reduce.
-    per_step = (time.perf_counter() - t_w) / max(1, args.warmup)
-    n_settle = int(max(0.0, 1.0 - (time.perf_counter() - t_w)) / max(per_step, 1e-4)) + 1
-    if world > 1:
-        t = torch.tensor([n_settle], device="cuda", dtype=torch.int64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        n_settle = int(t.item())
+    # untimed settle steps for >= 1 s of wall time: clocks settle under load and get
+    # sampled. Every rank must run the SAME number of steps (each DP step issues
+    # collectives; a per-rank time-based loop deadlocked), so steps run in chunks and the
+    # ranks agree after each chunk (MAX of elapsed time) whether to run another.
     t_clk0 = time.time()
-    for _ in range(n_settle):
-        one_step()
+    chunk = 3
+    while True:
+        for _ in range(chunk):
+            one_step()
         torch.cuda.synchronize()
+        el = torch.tensor([time.time() - t_clk0], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        if el.item() >= 1.0:
+            break
     if world > 1:
         dist.barrier()
 
@@ -333,7 +352,10 @@ def run_ours(args, rank, world, local_rank):
             fl6[i] *= args.steps
         graph = graph_prof = None  # event nodes reference events released by profile_end
         step.graph = None
-    clk = clocks.stop(window=(t_clk0, time.time()))
+    t_clk1 = time.time()
+    clk = clocks.stop(window=(t_clk0, t_clk1))
+    if os.environ.get("TLORA_CLOCK_DUMP"):
+        print(f"[bench] clock window {t_clk0:.3f} .. {t_clk1:.3f}", file=sys.stderr)
     if os.environ.get("TLORA_BENCH_CHECKSUM") and rank == 0:  # debugging aid: schedule
         tot = 0.0                                             # variants must agree bitwise
         for lay in step.layers.values():
