@@ -503,7 +503,8 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": f"{wl.name}: {wl.notes}", "layers_per_step": wl.layers,
                    "tokens_per_gpu": wl.tokens,
                    "jobs": [[j.job_id, j.rank, j.tokens] for j in wl.jobs],
-                   "projections": wl.projections, "token_order": "shuffled" if args.shuffle else "job-contiguous",
+                   "projections": wl.projections, "token_order": ("shuffled" + (" (gathered plan)" if step.gathered else " (plain plan)"))
+                   if args.shuffle else "job-contiguous",
                    "parallelism": f"dp{world}", "lowrank_side_stream_sms": args.overlap,
                    "dp_sm_reserve": os.environ.get("TLORA_SM_RESERVE") if world > 1 else None,
                    "nccl_max_nchannels": os.environ.get("NCCL_MAX_NCHANNELS") if world > 1 else None,

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define TLORA_ABI_VERSION 3
+#define TLORA_ABI_VERSION 4
 
 enum tlora_status {
   TLORA_OK = 0,
@@ -145,6 +145,20 @@ int tlora_layer_read_adapter(tlora_layer* layer, int32_t slot, float* A, float* 
  * used with any layer of the same registry layout (d, k, ranks) on the same device. */
 int tlora_plan_create(tlora_layer* layer, int64_t tokens, const int32_t* token_slot,
                       tlora_plan** out);
+/* Gathered plan for interleaved batches: the plan of the stable job-sorted order of
+ * token_slot (rows of one job keep their order, fused_lora.hpp:56-61), so every tile sees
+ * one job's rank window, as for a job-contiguous batch. Operands X / dY passed with it must
+ * be in that gathered order (tlora_gather_rows); the H / dH stashes stay in it; the fused
+ * forward / dX epilogues store Y / dX row i straight to the caller's token row_map[i], so
+ * outputs come back in the original order. Not accepted by the reduce-scatter epilogue. */
+int tlora_plan_create_gathered(tlora_layer* layer, int64_t tokens, const int32_t* token_slot,
+                               tlora_plan** out);
+/* row_map[i] = original token of gathered row i (identity for a plain plan). Synchronous. */
+int tlora_plan_row_map(const tlora_plan* plan, int32_t* row_map);
+/* dst[i][r, :] = src[i][row_map[r], :] for n bf16 row-major T x width[i] tensors (width a
+ * multiple of 8, 16-byte aligned, dst != src); four tensors per launch. Enqueue-only. */
+int tlora_gather_rows(const tlora_plan* plan, int32_t n, const void* const* src, void* const* dst,
+                      const int64_t* width, void* stream);
 int tlora_plan_destroy(tlora_plan* plan);
 int tlora_plan_get_info(const tlora_plan* plan, tlora_plan_info* info);
 /* Copy the tile table of `launch` into out[cap]; *count gets the table length. */

@@ -61,6 +61,9 @@ struct GemmArgs {
   void* peer[8];
   int32_t peer_rank, peer_world;
   int64_t rows_per_rank, slot_rows, dst_row0;
+  // EPI_BF16 / EPI_F32 (non-split): accumulator row r is stored to output row row_map[r]
+  // (gathered plans: operands in job-sorted order, Y / dX in the caller's token order)
+  const int32_t* row_map;
 };
 
 template <int BN, int STAGES>
@@ -106,7 +109,8 @@ __device__ __forceinline__ void epi_store32(const GemmArgs& args, int split, int
         if (col < lo || col >= hi) f[i] = 0.f;
       }
     }
-    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + (int64_t)row * args.ldo + col0;
+    const int64_t orow = (EPI == EPI_BF16 && args.row_map) ? (int64_t)args.row_map[row] : row;
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + orow * args.ldo + col0;
     if (col0 + 32 <= args.N) {
       uint4* o4 = reinterpret_cast<uint4*>(o);
       if (args.beta != 0.f) {  // out = acc + beta * out (in fp32, one bf16 rounding)
@@ -146,8 +150,9 @@ __device__ __forceinline__ void epi_store32(const GemmArgs& args, int split, int
                                                       : f[i]);
     }
   } else {
+    const int64_t orow = args.row_map ? (int64_t)args.row_map[row] : row;
     float* o = reinterpret_cast<float*>(args.out) + (int64_t)split * args.split_stride +
-               (int64_t)row * args.ldo + col0;
+               orow * args.ldo + col0;
     if (col0 + 32 <= args.N) {
       float4* o4 = reinterpret_cast<float4*>(o);
 #pragma unroll

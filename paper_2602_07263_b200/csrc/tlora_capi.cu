@@ -632,6 +632,11 @@ struct tlora_plan {
   tlora::PlanTables Ps;             // plan of the job-sorted token order (grad tables used)
   DevBuf<TileDesc> stiles[2];       // Ps.tiles[TLORA_L_DB], Ps.tiles[TLORA_L_DA]
   DevBuf<int32_t> scnt_db, scnt_da, perm;  // sorted row i <- token perm[i]
+  // Gathered plan (tlora_plan_create_gathered): P is the plan of the job-sorted order;
+  // X / dY operands come in that order (tlora_gather_rows), H / dH stay in it, and the
+  // fused GEMM epilogues store Y / dX row i to the caller's token row_map[i].
+  bool gathered = false;
+  DevBuf<int32_t> row_map;
 };
 
 namespace {
@@ -1077,6 +1082,83 @@ int tlora_plan_create(tlora_layer* layer, int64_t tokens, const int32_t* token_s
   });
 }
 
+int tlora_plan_create_gathered(tlora_layer* layer, int64_t tokens, const int32_t* token_slot,
+                               tlora_plan** out) {
+  return guarded([&] {
+    require(out != nullptr && layer != nullptr, TLORA_ERR_ARG, "null argument");
+    *out = nullptr;
+    require(tokens >= 1, TLORA_ERR_SHAPE, "plan needs at least one token");
+    require(tokens < (int64_t(1) << 31) - 256, TLORA_ERR_SHAPE, "too many tokens for one plan");
+    require(token_slot != nullptr, TLORA_ERR_ARG, "token_slot is null");
+    const int32_t S = (int32_t)layer->L.rank.size();
+    std::vector<int64_t> perm64(tokens), offsets(S + 1);
+    // stable job-sorted order: the segment permutation (fused_lora.hpp:56-61 for all jobs)
+    const int rc = tlora_segments(tokens, token_slot, S, perm64.data(), offsets.data());
+    if (rc != TLORA_OK) throw Status(rc, g_last_error);
+    std::vector<int32_t> perm(tokens), sorted(tokens);
+    for (int64_t i = 0; i < tokens; ++i) {
+      perm[i] = (int32_t)perm64[i];
+      sorted[i] = token_slot[perm[i]];
+    }
+    tlora_plan* p = nullptr;
+    const int rc2 = tlora_plan_create(layer, tokens, sorted.data(), &p);
+    if (rc2 != TLORA_OK) throw Status(rc2, g_last_error);
+    std::unique_ptr<tlora_plan> plan(p);
+    DeviceGuard g(layer->device);
+    plan->gathered = true;
+    plan->row_map.alloc(tokens);
+    TL_CUDA(cudaMemcpy(plan->row_map.p, perm.data(), tokens * 4, cudaMemcpyHostToDevice));
+    *out = plan.release();
+  });
+}
+
+int tlora_plan_row_map(const tlora_plan* plan, int32_t* row_map) {
+  return guarded([&] {
+    require(plan != nullptr && row_map != nullptr, TLORA_ERR_ARG, "null argument");
+    const int64_t T = plan->P.T;
+    if (!plan->gathered) {
+      for (int64_t i = 0; i < T; ++i) row_map[i] = (int32_t)i;
+      return;
+    }
+    DeviceGuard g(plan->device);
+    TL_CUDA(cudaMemcpy(row_map, plan->row_map.p, (size_t)T * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int tlora_gather_rows(const tlora_plan* plan, int32_t n, const void* const* src, void* const* dst,
+                      const int64_t* width, void* stream) {
+  return guarded([&] {
+    require(plan != nullptr, TLORA_ERR_ARG, "plan is null");
+    require(plan->gathered, TLORA_ERR_PLAN, "tlora_gather_rows needs a gathered plan");
+    require(n >= 0 && (n == 0 || (src && dst && width)), TLORA_ERR_ARG, "null argument");
+    DeviceGuard g(plan->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t T = plan->P.T;
+    for (int32_t i0 = 0; i0 < n; i0 += 4) {  // four tensors per launch
+      GatherJob jobs[4] = {};
+      int64_t work = 0;
+      for (int q = 0; q < 4 && i0 + q < n; ++q) {
+        const int32_t i = i0 + q;
+        require(src[i] && dst[i] && src[i] != dst[i], TLORA_ERR_ARG,
+                "gather needs distinct non-null source and destination");
+        require(width[i] > 0 && width[i] % 8 == 0, TLORA_ERR_SHAPE,
+                "gather row width must be a positive multiple of 8 bf16 elements");
+        require(((uintptr_t)src[i] | (uintptr_t)dst[i]) % 16 == 0, TLORA_ERR_ARG,
+                "gather operands must be 16-byte aligned");
+        jobs[q] = {reinterpret_cast<const uint4*>(src[i]), reinterpret_cast<uint4*>(dst[i]),
+                   width[i] / 8};
+        work += T * (width[i] / 8);
+      }
+      const int blocks = (int)std::min<int64_t>(tlora::ceil_div(work, 256),
+                                                8 * (int64_t)device_sm_count(plan->device));
+      gather_rows_kernel<<<blocks, 256, 0, s>>>(jobs[0], jobs[1], jobs[2], jobs[3],
+                                                plan->row_map.p, T);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      TL_CUDA(cudaGetLastError());
+    }
+  });
+}
+
 int tlora_plan_destroy(tlora_plan* plan) {
   return guarded([&] {
     if (!plan) return;
@@ -1256,6 +1338,7 @@ void run_fwd_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X, con
   a.out = Y;
   a.ldo = k;
   a.beta = 0.f;
+  a.row_map = plan->row_map.p;  // null unless gathered
   const CUtensorMap ma0 = tmap_k(X, d, T, 128);
   const CUtensorMap mb0 = tmap_k(layer->Wt16.p, d, k, 128);
   const CUtensorMap ma1 = tmap_k(H, R, T, 128);
@@ -1307,6 +1390,7 @@ void run_dx(tlora_layer* layer, const tlora_plan* plan, const void* dY, const vo
   a.out = dX;
   a.ldo = d;
   a.beta = beta;
+  a.row_map = plan->row_map.p;  // null unless gathered
   const CUtensorMap ma0 = tmap_k(dY, k, T, 128);
   const CUtensorMap mb0 = tmap_k(layer->W16.p, k, d, 128);
   const CUtensorMap ma1 = tmap_k(dH, R, T, 128);
@@ -1529,6 +1613,8 @@ int tlora_forward_gemm_rs(tlora_layer* layer, const tlora_plan* plan, const void
     check_bound(layer, plan);
     check_align(X, "X");
     check_align(H, "H");
+    require(!plan->gathered, TLORA_ERR_PLAN,
+            "the fused reduce-scatter epilogue does not take a gathered plan");
     require(recv_ptrs != nullptr && world >= 1 && world <= 8 && rank >= 0 && rank < world,
             TLORA_ERR_ARG, "need 1..8 receive buffers and a rank in [0, world)");
     const auto& L = layer->L;

@@ -60,15 +60,37 @@ class PlanInfo:
 class Plan:
     """Rank-aware tile-packing / indexing plan of one (nano-)batch (opaque, immutable)."""
 
-    def __init__(self, layer: "FusedLoRALayer", token_slot: Sequence[int]):
+    def __init__(self, layer: "FusedLoRALayer", token_slot: Sequence[int], gathered: bool = False):
         ts = np.ascontiguousarray(np.asarray(token_slot, dtype=np.int32))
         self.layer = layer
         self.tokens = int(ts.shape[0])
         self.token_slot = ts
+        self.gathered = bool(gathered)
         h = C.c_void_p()
-        call("tlora_plan_create", layer._h, self.tokens,
-             ts.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(h))
+        call("tlora_plan_create_gathered" if gathered else "tlora_plan_create", layer._h,
+             self.tokens, ts.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(h))
         self._h = h
+
+    def row_map(self) -> np.ndarray:
+        """Original token of each gathered row (identity for a plain plan)."""
+        out = np.empty(self.tokens, np.int32)
+        call("tlora_plan_row_map", self._h, out.ctypes.data_as(C.POINTER(C.c_int32)))
+        return out
+
+    def gather(self, pairs, stream=None):
+        """dst[r] = src[row_map[r]] for (src, dst) bf16 T x w tensors (tlora_gather_rows):
+        the gathered-order operands X / dY of a gathered plan."""
+        n = len(pairs)
+        if n == 0:
+            return
+        for src, dst in pairs:
+            assert src.dtype == torch.bfloat16 and dst.dtype == torch.bfloat16
+            assert src.shape == dst.shape and src.shape[0] == self.tokens
+            assert src.is_contiguous() and dst.is_contiguous()
+        srcs = (C.c_void_p * n)(*[p[0].data_ptr() for p in pairs])
+        dsts = (C.c_void_p * n)(*[p[1].data_ptr() for p in pairs])
+        widths = (C.c_int64 * n)(*[p[0].shape[1] for p in pairs])
+        call("tlora_gather_rows", self._h, n, srcs, dsts, widths, _stream_ptr(stream))
 
     def info(self) -> PlanInfo:
         i = capi.PlanInfoC()
@@ -184,8 +206,10 @@ class FusedLoRALayer:
         return A, B
 
     # ---------------------------------------------------------------- compute
-    def plan(self, token_slot: Sequence[int]) -> Plan:
-        p = Plan(self, token_slot)
+    def plan(self, token_slot: Sequence[int], gathered: bool = False) -> Plan:
+        """gathered=True: tlora_plan_create_gathered (operands in job-sorted order via
+        Plan.gather, Y / dX written back in token order by the GEMM epilogues)."""
+        p = Plan(self, token_slot, gathered)
         self._plans.add(p)
         return p
 

@@ -40,6 +40,10 @@ class LayerSetStep:
         T = wl.tokens
         self.T = T
         self.slots = wl.token_slots(shuffle=shuffle)
+        # interleaved tokens: gathered plans (job-sorted operands, one rank window per tile)
+        # unless TLORA_GATHERED=0 (plain plans: wide K-extension windows, gathers per grads)
+        import os
+        self.gathered = bool(shuffle) and os.environ.get("TLORA_GATHERED", "1") != "0"
         self.layers, self.plans = {}, {}
         self.X, self.Y, self.H, self.dY, self.dX = {}, {}, {}, {}, {}
         self.keys = [(L, name) for L in range(wl.layers) for name, _, _ in wl.projections]
@@ -56,7 +60,7 @@ class LayerSetStep:
                 lay.set_adapter(s, A, B)
             self.layers[(L, name)] = lay
             if name not in self.plans:
-                self.plans[name] = lay.plan(self.slots)
+                self.plans[name] = lay.plan(self.slots, gathered=self.gathered)
             grp = INPUT_GROUP.get(name, name)
             if grp not in self.X:
                 self.X[grp] = torch.randn(T, d, generator=g, device=dev).bfloat16()
@@ -64,6 +68,9 @@ class LayerSetStep:
                 self.Y[name] = torch.empty(T, k, dtype=y_dtype, device=dev)
                 self.dY[name] = torch.randn(T, k, generator=g, device=dev).bfloat16()
                 self.dX[name] = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+        if self.gathered:
+            self.gX = {g: torch.empty_like(t) for g, t in self.X.items()}
+            self.gdY = {n: torch.empty_like(t) for n, t in self.dY.items()}
         # H stashes: one zeroed arena; the masked low-rank launches only ever write each
         # token's window columns (zeros outside its own slot), so the rest stays zero
         R = self.layers[self.keys[0]].R  # packed rank width: same for every projection
@@ -74,9 +81,24 @@ class LayerSetStep:
         torch.cuda.synchronize(dev)
 
     def x_of(self, name):
-        return self.X[INPUT_GROUP.get(name, name)]
+        X = self.gX if self.gathered else self.X
+        return X[INPUT_GROUP.get(name, name)]
+
+    def dy_of(self, name):
+        return (self.gdY if self.gathered else self.dY)[name]
+
+    def gather_inputs(self, stream=None):
+        """Gathered plans: job-sorted copies of this step's inputs (X groups, dY), four
+        tensors per launch; the fused GEMMs write Y / dX back in token order."""
+        if not self.gathered:
+            return
+        pl = next(iter(self.plans.values()))
+        pairs = [(self.X[g], self.gX[g]) for g in self.X] + \
+                [(self.dY[n], self.gdY[n]) for n in self.dY]
+        pl.gather(pairs, stream=stream)
 
     def forward(self, stream=None):
+        self.gather_inputs(stream)
         if self.chain:
             import os
             return self.forward_chained(stream, os.environ.get("TLORA_PREFETCH_DH", "1") != "0")
@@ -103,7 +125,7 @@ class LayerSetStep:
                                       self.H[nk], zero_next=False, stream=stream)
             elif prefetch_dh:
                 lay.fused_gemm_dh(pl, self.x_of(name), self.H[(L, name)], self.Y[name], lay, pl,
-                                  self.dY[name], self._first_dh_buffer(), zero_next=False,
+                                  self.dy_of(name), self._first_dh_buffer(), zero_next=False,
                                   stream=stream)
                 self._dh_prefetched = True
             else:
@@ -127,7 +149,7 @@ class LayerSetStep:
         done = {}            # key index -> event after its grads launch (side stream)
         k0 = keys[0]
         if not getattr(self, "_dh_prefetched", False):
-            self.layers[k0].dh(self.plans[k0[1]], self.dY[k0[1]], self.dH4[0], stream=main)
+            self.layers[k0].dh(self.plans[k0[1]], self.dy_of(k0[1]), self.dH4[0], stream=main)
         self._dh_prefetched = False
         for i, (L, name) in enumerate(keys):
             lay, pl = self.layers[(L, name)], self.plans[name]
@@ -136,14 +158,14 @@ class LayerSetStep:
                 nk = keys[i + 1]
                 if i - 3 in done:  # buffer (i+1)%4 was last read by grads(i-3)
                     main.wait_event(done[i - 3])
-                lay.dx_dh(pl, self.dY[name], dH, self.dX[name], self.layers[nk], self.plans[nk[1]],
-                          self.dY[nk[1]], self.dH4[(i + 1) % 4], zero_next=False, stream=main)
+                lay.dx_dh(pl, self.dy_of(name), dH, self.dX[name], self.layers[nk], self.plans[nk[1]],
+                          self.dy_of(nk[1]), self.dH4[(i + 1) % 4], zero_next=False, stream=main)
             else:
-                lay.dx(pl, self.dY[name], dH, self.dX[name], stream=main)
+                lay.dx(pl, self.dy_of(name), dH, self.dX[name], stream=main)
             ready = torch.cuda.Event()
             ready.record(main)  # dH(i) was written by the previous launch on main
             side.wait_event(ready)
-            lay.grads(pl, self.H[(L, name)], self.dY[name], self.x_of(name), dH, beta=beta,
+            lay.grads(pl, self.H[(L, name)], self.dy_of(name), self.x_of(name), dH, beta=beta,
                       stream=side)
             if opt_inline:  # nothing later in the step reads this projection's adapters
                 lay.optimizer_step(stream=side)
@@ -161,18 +183,18 @@ class LayerSetStep:
         keys = list(reversed(self.keys))
         k0 = keys[0]
         if not getattr(self, "_dh_prefetched", False):
-            self.layers[k0].dh(self.plans[k0[1]], self.dY[k0[1]], self.dH2[0], stream=stream)
+            self.layers[k0].dh(self.plans[k0[1]], self.dy_of(k0[1]), self.dH2[0], stream=stream)
         self._dh_prefetched = False
         for i, (L, name) in enumerate(keys):
             lay, pl = self.layers[(L, name)], self.plans[name]
             dH = self.dH2[i % 2]
             if i + 1 < len(keys):
                 nk = keys[i + 1]
-                lay.dx_dh(pl, self.dY[name], dH, self.dX[name], self.layers[nk], self.plans[nk[1]],
-                          self.dY[nk[1]], self.dH2[(i + 1) % 2], zero_next=False, stream=stream)
+                lay.dx_dh(pl, self.dy_of(name), dH, self.dX[name], self.layers[nk], self.plans[nk[1]],
+                          self.dy_of(nk[1]), self.dH2[(i + 1) % 2], zero_next=False, stream=stream)
             else:
-                lay.dx(pl, self.dY[name], dH, self.dX[name], stream=stream)
-            lay.grads(pl, self.H[(L, name)], self.dY[name], self.x_of(name), dH, beta=beta,
+                lay.dx(pl, self.dy_of(name), dH, self.dX[name], stream=stream)
+            lay.grads(pl, self.H[(L, name)], self.dy_of(name), self.x_of(name), dH, beta=beta,
                       stream=stream)
             if on_layer_done is not None:
                 on_layer_done((L, name), lay)
@@ -182,7 +204,7 @@ class LayerSetStep:
             return self.backward_chained(stream, beta, on_layer_done)
         for L, name in reversed(self.keys):
             lay = self.layers[(L, name)]
-            lay.backward(self.plans[name], self.dY[name], self.x_of(name), self.H[(L, name)],
+            lay.backward(self.plans[name], self.dy_of(name), self.x_of(name), self.H[(L, name)],
                          self.dX[name], beta=beta, stream=stream)
             if on_layer_done is not None:
                 on_layer_done((L, name), lay)
@@ -233,19 +255,19 @@ class LayerSetStep:
             L, name = keys[i]
             if name in last_dx:  # dH[name] is shared by every layer of this projection
                 side.wait_event(last_dx[name])  # (its grad_a reader is earlier on `side`)
-            self.layers[keys[i]].dh(self.plans[name], self.dY[name], self.dH[name], stream=side)
+            self.layers[keys[i]].dh(self.plans[name], self.dy_of(name), self.dH[name], stream=side)
             return self._ev(side)
 
         ev_dh = launch_dh(0)
         for i, (L, name) in enumerate(keys):
             lay, pl = self.layers[(L, name)], self.plans[name]
             main.wait_event(ev_dh)
-            lay.dx(pl, self.dY[name], self.dH[name], self.dX[name], stream=main)
+            lay.dx(pl, self.dy_of(name), self.dH[name], self.dX[name], stream=main)
             last_dx[name] = self._ev(main)
             nxt = i + 1 < len(keys)
             ahead = nxt and keys[i + 1][1] != name
             ev_dh = launch_dh(i + 1) if ahead else None
-            lay.grad_b(pl, self.H[(L, name)], self.dY[name], stream=side)
+            lay.grad_b(pl, self.H[(L, name)], self.dy_of(name), stream=side)
             lay.grad_a(pl, self.x_of(name), self.dH[name], stream=side)
             ev_grads = self._ev(side)
             if nxt and not ahead:

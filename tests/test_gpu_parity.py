@@ -44,8 +44,10 @@ def bf(a):
     return O.round_bf16(np.asarray(a, np.float64))
 
 
-def gpu_run(X, W, A, B, slots, dY, beta_runs=1):
-    """Run fwd+bwd through the C-ABI on padded bf16 copies; returns numpy results."""
+def gpu_run(X, W, A, B, slots, dY, beta_runs=1, gathered=False):
+    """Run fwd+bwd through the C-ABI on padded bf16 copies; returns numpy results.
+    gathered: tlora_plan_create_gathered + tlora_gather_rows (operands in job-sorted order,
+    Y / dX stored back in token order by the epilogues; H un-gathered here for the check)."""
     T, d = X.shape
     k = W.shape[1]
     dp, kp = pad8(d), pad8(k)
@@ -61,14 +63,22 @@ def gpu_run(X, W, A, B, slots, dY, beta_runs=1):
     lay.set_base(padded(W, dp, kp))
     for s in range(len(A)):
         lay.set_adapter(s, padded(A[s], dp, ranks[s]), padded(B[s], ranks[s], kp))
-    plan = lay.plan(slots)
+    plan = lay.plan(slots, gathered=gathered)
     Xd = padded(X, T, dp)
     dYd = padded(dY, T, kp)
+    if gathered:
+        Xg, dYg = torch.empty_like(Xd), torch.empty_like(dYd)
+        plan.gather([(Xd, Xg), (dYd, dYg)])
+        Xd, dYd = Xg, dYg
     Y, H = lay.forward(plan, Xd, y_dtype=torch.float32)
     dX = None
     for i in range(beta_runs):
         dX = lay.backward(plan, dYd, Xd, H, beta=1.0 if i else 0.0)
     torch.cuda.synchronize()
+    if gathered:
+        Hn = torch.empty_like(H)
+        Hn[torch.from_numpy(plan.row_map().astype(np.int64)).to(dev)] = H
+        H = Hn
     grads = [lay.read_grad(s) for s in range(len(A))]
     out = dict(Y=Y[:, :k].double().cpu().numpy(), dX=dX[:, :d].double().cpu().numpy(),
                dA=[g[0][:d].double().cpu().numpy() for g in grads],
@@ -134,13 +144,15 @@ def golden_cases(name, n):
     return out
 
 
-@pytest.mark.parametrize("name,n", [("fused_2024.bin", 50), ("fused_101.bin", 25)])
-def test_reference_golden_instances(name, n):
+@pytest.mark.parametrize("name,n,gathered", [("fused_2024.bin", 50, False),
+                                             ("fused_101.bin", 25, False),
+                                             ("fused_2024.bin", 50, True)])
+def test_reference_golden_instances(name, n, gathered):
     for inst, A, B, slots in golden_cases(name, n):
         X, W = bf(inst.X), bf(inst.W)
         Ab, Bb = [bf(a) for a in A], [bf(b) for b in B]
         dY = bf(np.random.RandomState(inst.tokens).randn(inst.tokens, inst.k))
-        got = gpu_run(X, W, Ab, Bb, slots, dY)
+        got = gpu_run(X, W, Ab, Bb, slots, dY, gathered=gathered)
         check(got, X, W, Ab, Bb, slots, dY)
         # against the reference's own output on the original double inputs
         assert maxrel(got["Y"], inst.Y_fused) <= 2e-2
@@ -172,8 +184,8 @@ def _random_problem(T, d, k, ranks, counts=None, shuffle=True, seed=0):
     return X, W, A, B, slots, dY
 
 
-@pytest.mark.parametrize("shuffle", [False, True])
-def test_c1_full_size(shuffle):
+@pytest.mark.parametrize("shuffle,gathered", [(False, False), (True, False), (True, True)])
+def test_c1_full_size(shuffle, gathered):
     wl = config("C1")
     rs = np.random.RandomState(11)
     slots = wl.token_slots(shuffle=shuffle)
@@ -183,8 +195,54 @@ def test_c1_full_size(shuffle):
     A = [bf(rs.randn(d, r) / np.sqrt(d)) for r in wl.ranks]
     B = [bf(rs.randn(r, k) / np.sqrt(r)) for r in wl.ranks]
     dY = bf(rs.randn(T, k))
-    got = gpu_run(X, W, A, B, slots, dY)
-    check(got, X, W, A, B, slots, dY)
+    got = gpu_run(X, W, A, B, slots, dY, beta_runs=2 if gathered else 1, gathered=gathered)
+    check(got, X, W, A, B, slots, dY, scale_grads=2.0 if gathered else 1.0)
+
+
+def test_gathered_plan_matches_sorted_batch_bitwise():
+    """A gathered plan over an interleaved batch is the job-contiguous plan of the sorted
+    batch with a row map on the Y / dX stores: outputs are the sorted run's, bit for bit,
+    scattered back to token order; adapter gradients are bitwise equal."""
+    rs = np.random.RandomState(7)
+    T, d, k, ranks = 1000, 512, 384, [8, 24, 64, 128]
+    slots = rs.randint(0, len(ranks), T).astype(np.int32)
+    perm = np.argsort(slots, kind="stable")
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev).bfloat16()  # noqa: E731
+    X, dY = t(bf(rs.randn(T, d))), t(bf(rs.randn(T, k)))
+    W = t(bf(rs.randn(d, k) / np.sqrt(d)))
+    A = [t(bf(rs.randn(d, r) / np.sqrt(d))) for r in ranks]
+    B = [t(bf(rs.randn(r, k) / np.sqrt(r))) for r in ranks]
+    res = []
+    for gathered in (False, True):
+        lay = FusedLoRALayer(d, k, ranks)
+        lay.set_base(W)
+        for s in range(len(ranks)):
+            lay.set_adapter(s, A[s], B[s])
+        if gathered:
+            plan = lay.plan(slots, gathered=True)
+            assert np.array_equal(plan.row_map(), perm)
+            Xg, dYg = torch.empty_like(X), torch.empty_like(dY)
+            plan.gather([(X, Xg), (dY, dYg)])
+            assert torch.equal(Xg, X[torch.from_numpy(perm).to(dev)])
+        else:
+            plan = lay.plan(slots[perm])
+            idx = torch.from_numpy(perm).to(dev)
+            Xg, dYg = X[idx].contiguous(), dY[idx].contiguous()
+        Y, H = lay.forward(plan, Xg)
+        dX = lay.backward(plan, dYg, Xg, H)
+        torch.cuda.synchronize()
+        if not gathered:  # scatter the sorted run's outputs to token order
+            idx = torch.from_numpy(perm).to(dev)
+            Ys, dXs = torch.empty_like(Y), torch.empty_like(dX)
+            Ys[idx], dXs[idx] = Y, dX
+            Y, dX = Ys, dXs
+        res.append((Y, dX, [torch.cat([g.flatten() for g in lay.read_grad(s)])
+                            for s in range(len(ranks))]))
+        lay.close()
+    (Y0, dX0, g0), (Y1, dX1, g1) = res
+    assert torch.equal(Y0, Y1) and torch.equal(dX0, dX1)
+    assert all(torch.equal(a, b) for a, b in zip(g0, g1))
 
 
 @pytest.mark.parametrize("cell", [(1024, 2, 2048, 1), (1024, 8, 2048, 2), (1024, 16, 2048, 3),
