@@ -36,6 +36,10 @@ struct GradSmem {
 // tail of one fills with the other.
 struct GradArgs {
   GemmArgs job[2];
+  // optional static schedule (tlora::grad_schedule, built for gridDim.x CTAs): CTA b runs
+  // tiles sched_idx[sched_off[b] .. sched_off[b+1]); null -> round-robin t += gridDim.x
+  const int32_t* sched_off;
+  const int32_t* sched_idx;
 };
 
 // Tile fields: m0 = M offset, n0 = first packed rank column of the job (chunk), kb0/ke0 =
@@ -70,6 +74,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     j = t < n_first ? 0 : 1;
     return gargs.job[j].tiles[j == 0 ? t : t - n_first];
   };
+  // this CTA's tile sequence: positions [i0, i1) step di, tile = at(i)
+  const bool sched = gargs.sched_off != nullptr;
+  const int i0 = sched ? gargs.sched_off[blockIdx.x] : (int)blockIdx.x;
+  const int i1 = sched ? gargs.sched_off[blockIdx.x + 1] : n_total;
+  const int di = sched ? 1 : (int)gridDim.x;
+  auto at = [&](int i) { return sched ? gargs.sched_idx[i] : i; };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA0);
@@ -99,7 +109,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {  // TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < n_total; t += gridDim.x) {
+      for (int i = i0; i < i1; i += di) {
+        const int t = at(i);
         int j;
         const TileDesc td = tile_of(t, j);
         const CUtensorMap* tmA = j == 0 ? &tmA0 : &tmA1;
@@ -134,7 +145,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int acc_iter = 0;
-      for (int t = blockIdx.x; t < n_total; t += gridDim.x) {
+      for (int i = i0; i < i1; i += di) {
+        const int t = at(i);
         int j;
         const TileDesc td = tile_of(t, j);
         const int nkb = td.ke0 > td.kb0 ? (td.ke0 - td.kb0 + kBK - 1) / kBK : 0;
@@ -166,7 +178,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp >= 4) {  // epilogue: transposed, column-masked fp32 store
     const int ew = warp & 3;
     int acc_iter = 0;
-    for (int t = blockIdx.x; t < n_total; t += gridDim.x) {
+    for (int i = i0; i < i1; i += di) {
+      const int t = at(i);
       int j;
       const TileDesc td = tile_of(t, j);
       const GemmArgs& args = gargs.job[j];

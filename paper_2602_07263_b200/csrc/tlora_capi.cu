@@ -585,6 +585,15 @@ struct tlora_layer {
 };
 
 namespace {
+// TLORA_GRAD_LPT=0: round-robin gradient tiles instead of the LPT schedule (A/B knob).
+bool grad_lpt() {
+  static const bool on = [] {
+    const char* e = std::getenv("TLORA_GRAD_LPT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // Per-device scratch for the split-K partial planes and tlora_backward's dH. Gradient
 // launches (and tlora_backward) on one device are therefore serialised on one stream at a
 // time (the drivers in this repo do so). Growing reallocates (cudaFree synchronises); it
@@ -637,6 +646,9 @@ struct tlora_plan {
   // fused GEMM epilogues store Y / dX row i to the caller's token row_map[i].
   bool gathered = false;
   DevBuf<int32_t> row_map;
+  // LPT schedule of the combined dB+dA gradient launch for gsched_ctas CTAs (CSR)
+  int gsched_ctas = 0;
+  DevBuf<int32_t> gsched_off, gsched_idx;
 };
 
 namespace {
@@ -1072,6 +1084,18 @@ int tlora_plan_create(tlora_layer* layer, int64_t tokens, const int32_t* token_s
         TL_CUDA(cudaMemcpy(plan->perm.p, perm.data(), tokens * 4, cudaMemcpyHostToDevice));
       }
     }
+    if (!plan->interleaved && grad_lpt()) {
+      std::vector<int32_t> off, idx;
+      const int G = layer->sm_count;
+      tlora::grad_schedule(plan->P.tiles[TLORA_L_DB], plan->P.tiles[TLORA_L_DA], G, off, idx);
+      if (!idx.empty()) {
+        plan->gsched_ctas = G;
+        plan->gsched_off.alloc(off.size());
+        TL_CUDA(cudaMemcpy(plan->gsched_off.p, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+        plan->gsched_idx.alloc(idx.size());
+        TL_CUDA(cudaMemcpy(plan->gsched_idx.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice));
+      }
+    }
     plan->cnt_db.alloc(plan->P.split_count_db.size());
     TL_CUDA(cudaMemcpy(plan->cnt_db.p, plan->P.split_count_db.data(),
                        plan->P.split_count_db.size() * 4, cudaMemcpyHostToDevice));
@@ -1493,6 +1517,10 @@ void run_grads(tlora_layer* layer, const tlora_plan* plan, const void* H, const 
   constexpr int smem = tlora::GradSmem<TLORA_GRAD_STAGES>::kDynamic;
   TL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = std::min(tiles, sm_budget(layer->device, layer->sm_count, false));
+  if (on[0] && on[1] && !srt && plan->gsched_ctas == grid) {  // LPT-balanced CTA tile lists
+    g.sched_off = plan->gsched_off.p;
+    g.sched_idx = plan->gsched_idx.p;
+  }
   {
     ProfScope ps(do_b ? TLORA_L_DB : TLORA_L_DA, flops, s);  // dB+dA together: booked on dB
     if (tiles > 0) {

@@ -558,3 +558,43 @@ def test_model_projection_shapes(shape):
                                             seed=d + k)
     got = gpu_run(X, W, A, B, slots, dY)
     check(got, X, W, A, B, slots, dY)
+
+
+_LPT_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2602_07263_b200.layer import FusedLoRALayer
+rs = np.random.RandomState(3)
+T, d, k, ranks = 8192, 4096, 2048, [8, 24, 64, 128, 16]
+slots = np.sort(rs.randint(0, len(ranks), T)).astype(np.int32)
+dev = torch.device("cuda", 0)
+t = lambda a: torch.from_numpy(a.astype(np.float32)).to(dev).bfloat16()
+lay = FusedLoRALayer(d, k, ranks)
+lay.set_base(t(rs.randn(d, k) / np.sqrt(d)))
+for s, r in enumerate(ranks):
+    lay.set_adapter(s, t(rs.randn(d, r) / np.sqrt(d)), t(rs.randn(r, k) / np.sqrt(r)))
+plan = lay.plan(slots)
+X, dY = t(rs.randn(T, d)), t(rs.randn(T, k))
+Y, H = lay.forward(plan, X)
+lay.backward(plan, dY, X, H, dX=False)
+torch.cuda.synchronize()
+np.save(sys.argv[2], np.concatenate([g.float().cpu().numpy().ravel() for g in lay.packed_grads()]))
+"""
+
+
+def test_grad_lpt_schedule_is_bitwise_round_robin(tmp_path):
+    """The LPT-balanced gradient tile lists (tlora::grad_schedule) only change which CTA runs
+    a tile and when: every output element is still produced by one tile with the same
+    accumulation order, so the gradients equal the round-robin schedule's bit for bit."""
+    import os
+    import subprocess
+    script = tmp_path / "lpt.py"
+    script.write_text(_LPT_SCRIPT)
+    out = {}
+    for lpt in ("1", "0"):
+        f = tmp_path / f"g{lpt}.npy"
+        env = dict(os.environ, TLORA_GRAD_LPT=lpt)
+        subprocess.run([sys.executable, str(script), str(ROOT), str(f)], check=True, env=env,
+                       timeout=300)
+        out[lpt] = np.load(f)
+    assert out["1"].size > 0 and np.array_equal(out["1"], out["0"])
