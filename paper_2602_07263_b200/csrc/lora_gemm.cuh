@@ -64,6 +64,9 @@ struct GemmArgs {
   // EPI_BF16 / EPI_F32 (non-split): accumulator row r is stored to output row row_map[r]
   // (gathered plans: operands in job-sorted order, Y / dX in the caller's token order)
   const int32_t* row_map;
+  // 2-CTA fused GEMM: dynamic tile scheduler (self-resetting global ticket; null = static
+  // round-robin). Only read from args (the main tiles' GemmArgs) of a launch.
+  int32_t* tile_counter;
 };
 
 template <int BN, int STAGES>

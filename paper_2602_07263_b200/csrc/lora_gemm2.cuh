@@ -30,7 +30,10 @@ struct Gemm2Smem {
   static constexpr int kBBytes = 128 * kBK * 2;  // this CTA's half of B
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOffset = STAGES * kStageBytes;
-  static constexpr int kTotal = kBarOffset + (2 * STAGES + 4) * 8 + 16;
+  static constexpr int kQ = 8;  // dynamic-scheduler tile queue depth
+  // barriers: full[S], empty[S], tfull[2], tempty[2], qfull[kQ], qempty[kQ]; then the TMEM
+  // base slot (16 B) and the tile queue (kQ x int32)
+  static constexpr int kTotal = kBarOffset + (2 * STAGES + 4 + 2 * kQ) * 8 + 16 + kQ * 4;
   static constexpr int kDynamic = kTotal + 1024;
   // EPI_PEER staging: per epilogue warp two buffers of 32 rows x 64 bf16 columns, rows
   // padded to 144 B (conflict-free 16-B shared stores; each row stays one contiguous
@@ -67,7 +70,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* qfull_bar = tempty_bar + 2;
+  uint64_t* qempty_bar = qfull_bar + L::kQ;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(qempty_bar + L::kQ);
+  int32_t* tile_q = reinterpret_cast<int32_t*>(tmem_base_slot + 4);
 
   const int warp = threadIdx.x / 32;
   const uint32_t lane = threadIdx.x % 32;
@@ -95,6 +101,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 8);
     }
+    for (int q = 0; q < L::kQ; ++q) {
+      mbar_init(&qfull_bar[q], 1);
+      // leader: MMA issuer + 4 epilogue warps; peer: producer + 4 epilogue warps
+      mbar_init(&qempty_bar[q], 10);
+    }
     fence_mbar_init();
     fence_proxy_async_smem();
   }
@@ -106,13 +117,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   pdl_launch_dependents();   // persistent grid: all CTAs are resident, dependents may queue
   pdl_wait_prerequisites();  // inputs written by the previous launch are visible after this
 
+  // Tile sequence of this CTA pair. Static: cluster_id, + num_clusters, ... Dynamic
+  // (args.tile_counter): the leader's producer claims tiles from a global ticket (one tile
+  // ahead) and publishes each index into a kQ-deep queue in BOTH CTAs' shared memory
+  // (qfull: local arrive + remote arrive on the peer); every other role of both CTAs pops
+  // the same sequence and releases the slot on the leader's qempty. Index n_total ends the
+  // sequence. The ticket's last claim (value n_total + num_clusters - 1: every pair makes
+  // exactly one failing claim) resets it to 0 for the next launch, which reads it only
+  // after griddepcontrol.wait, i.e. after this grid has completed.
+  const bool dyn = args.tile_counter != nullptr;
+  uint32_t qseq = 0;
+  auto q_pop = [&](bool remote_wait) -> int {  // one thread per consumer role
+    const uint32_t slot = qseq % L::kQ, ph = (qseq / L::kQ) & 1;
+    ++qseq;
+    if (remote_wait) mbar_wait_cluster(&qfull_bar[slot], ph);
+    else mbar_wait(&qfull_bar[slot], ph);
+    const int t = *reinterpret_cast<volatile int32_t*>(&tile_q[slot]);
+    if (leader) mbar_arrive(&qempty_bar[slot]);
+    else mbar_arrive_cluster(mapa_shared(smem_u32(&qempty_bar[slot]), 0));
+    return t;
+  };
+  auto q_push = [&](int t) {  // leader producer only
+    const uint32_t slot = qseq % L::kQ, ph = (qseq / L::kQ) & 1;
+    ++qseq;
+    mbar_wait_cluster(&qempty_bar[slot], ph ^ 1);
+    tile_q[slot] = t;
+    st_shared_cluster_u32(mapa_shared(smem_u32(&tile_q[slot]), 1), (uint32_t)t);
+    mbar_arrive(&qfull_bar[slot]);
+    mbar_arrive_cluster(mapa_shared(smem_u32(&qfull_bar[slot]), 1));
+  };
+  // claim(): issue the ticket atomic only; its value is first used at the NEXT tile switch,
+  // so the producer never stalls on the atomic's round trip before issuing a tile's loads.
+  auto claim = [&]() -> int { return atomicAdd(args.tile_counter, 1); };
+  auto resolve = [&](int v) -> int {
+    if (v == n_total + num_clusters - 1) atomicExch(args.tile_counter, 0);
+    return v < n_total ? v : n_total;
+  };
+
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
       const uint32_t full0 = mapa_shared(smem_u32(full_bar), 0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cluster_id; t < n_total; t += num_clusters) {
+      int t_ahead = dyn && leader ? claim() : 0;
+      auto next_tile = [&](int cur) -> int {
+        if (!dyn) return cur < 0 ? cluster_id : cur + num_clusters;
+        if (!leader) return q_pop(true);
+        const int t = resolve(t_ahead);
+        q_push(t);
+        if (t < n_total) t_ahead = claim();  // claim the next tile while this one loads
+        return t;
+      };
+      for (int t = next_tile(-1); t < n_total; t = next_tile(t)) {
         const bool sec = t >= n_main;
         const TileDesc td = sec ? args2.tiles[t - n_main] : args.tiles[t];
         const int am = td.m0 + 128 * (int)rank;
@@ -160,7 +217,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int acc_iter = 0;
-      for (int t = cluster_id; t < n_total; t += num_clusters) {
+      auto next_tile = [&](int cur) -> int {
+        if (!dyn) return cur < 0 ? cluster_id : cur + num_clusters;
+        return q_pop(false);
+      };
+      for (int t = next_tile(-1); t < n_total; t = next_tile(t)) {
         const bool sec = t >= n_main;
         const TileDesc td = sec ? args2.tiles[t - n_main] : args.tiles[t];
         const int nkb = (td.ke0 > td.kb0 ? (td.ke0 - td.kb0 + kBK - 1) / kBK : 0) +
@@ -194,7 +255,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const int ew = warp & 3;
     const uint32_t tempty0 = mapa_shared(smem_u32(tempty_bar), 0);
     int acc_iter = 0;
-    for (int t = cluster_id; t < n_total; t += num_clusters) {
+    auto next_tile = [&](int cur) -> int {
+      if (!dyn) return cur < 0 ? cluster_id : cur + num_clusters;
+      int t = 0;
+      if (lane == 0) t = q_pop(!leader);
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    for (int t = next_tile(-1); t < n_total; t = next_tile(t)) {
       const bool sec = t >= n_main;
       const TileDesc td = sec ? args2.tiles[t - n_main] : args.tiles[t];
       const bool empty_k = !(td.ke0 > td.kb0) && (sec || !(td.ke1 > td.kb1));

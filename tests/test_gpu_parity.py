@@ -576,25 +576,29 @@ for s, r in enumerate(ranks):
 plan = lay.plan(slots)
 X, dY = t(rs.randn(T, d)), t(rs.randn(T, k))
 Y, H = lay.forward(plan, X)
-lay.backward(plan, dY, X, H, dX=False)
+dX = lay.backward(plan, dY, X, H)
 torch.cuda.synchronize()
-np.save(sys.argv[2], np.concatenate([g.float().cpu().numpy().ravel() for g in lay.packed_grads()]))
+np.save(sys.argv[2], np.concatenate([t.float().cpu().numpy().ravel()
+                                     for t in [Y, dX] + list(lay.packed_grads())]))
 """
 
 
-def test_grad_lpt_schedule_is_bitwise_round_robin(tmp_path):
-    """The LPT-balanced gradient tile lists (tlora::grad_schedule) only change which CTA runs
-    a tile and when: every output element is still produced by one tile with the same
-    accumulation order, so the gradients equal the round-robin schedule's bit for bit."""
+@pytest.mark.parametrize("knob", [("TLORA_GRAD_LPT", "1", "0"), ("TLORA_DYN_SCHED", "1", "0")])
+def test_schedules_are_bitwise_identical(tmp_path, knob):
+    """Tile schedules only change which CTA runs a tile and when; every output element is
+    still produced by one tile with the same accumulation order. LPT-balanced gradient tile
+    lists (tlora::grad_schedule) vs round-robin, and the fused GEMM's dynamic ticket
+    scheduler vs its static round-robin: Y, dX and the gradients are equal bit for bit."""
     import os
     import subprocess
-    script = tmp_path / "lpt.py"
+    var, a, b = knob
+    script = tmp_path / "sched.py"
     script.write_text(_LPT_SCRIPT)
     out = {}
-    for lpt in ("1", "0"):
-        f = tmp_path / f"g{lpt}.npy"
-        env = dict(os.environ, TLORA_GRAD_LPT=lpt)
+    for val in (a, b):
+        f = tmp_path / f"g{val}.npy"
+        env = dict(os.environ, **{var: val})
         subprocess.run([sys.executable, str(script), str(ROOT), str(f)], check=True, env=env,
                        timeout=300)
-        out[lpt] = np.load(f)
-    assert out["1"].size > 0 and np.array_equal(out["1"], out["0"])
+        out[val] = np.load(f)
+    assert out[a].size > 0 and np.array_equal(out[a], out[b])
