@@ -178,6 +178,13 @@ int tlora_plan_tiles_host(int64_t d, int64_t k, int32_t num_slots, const int32_t
                           int64_t tokens, const int32_t* token_slot, int launch, tlora_tile* out,
                           int32_t cap, int32_t* count);
 
+/* Host-only: the LPT schedule a plan uploads for its combined dB+dA gradient launch on
+ * `ctas` persistent CTAs: CTA c runs tiles idx[off[c] .. off[c+1]) of the
+ * concatenated (dB table, dA table). off has ctas + 1 entries; *count gets the tile count. */
+int tlora_plan_grad_schedule_host(int64_t d, int64_t k, int32_t num_slots, const int32_t* ranks,
+                                  int64_t tokens, const int32_t* token_slot, int32_t ctas,
+                                  int32_t* off, int32_t* idx, int32_t cap, int32_t* count);
+
 /* ---- compute (enqueue-only) ----------------------------------------------------- */
 /* Forward: Y = X·W + scatter_j((X_j·A_j)·B_j). X: T x d bf16, Y: T x k (bf16 or f32),
  * H_stash: T x R bf16 (the per-token low-rank intermediate, kept for backward). */

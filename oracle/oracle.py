@@ -43,6 +43,9 @@ def lib():
         L.orc_plan_tiles.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int32, _I, _I, C.c_int32,
                                      C.c_void_p, C.c_int64]
         L.orc_plan_tiles.restype = C.c_int64
+        L.orc_grad_schedule.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
+                                        _I, _I]
+        L.orc_grad_schedule.restype = C.c_int
         L.orc_round_bf16.argtypes = [C.c_double]
         L.orc_round_bf16.restype = C.c_double
         _lib = L
@@ -143,6 +146,18 @@ def plan_tiles(T, d, k, ranks, slots, which):
     out = np.zeros((max(1, n), 8), np.int32)
     lib().orc_plan_tiles(T, d, k, len(ranks), ranks, slots, which, out.ctypes.data, n)
     return out[:n]
+
+
+def grad_schedule(tiles_db, tiles_da, ctas):
+    """LPT CTA tile lists of one dB+dA launch (orc_grad_schedule): (off[ctas+1], idx)."""
+    db = _c(tiles_db, np.int32).reshape(-1, 8)
+    da = _c(tiles_da, np.int32).reshape(-1, 8)
+    off = np.zeros(ctas + 1, np.int32)
+    idx = np.zeros(max(1, len(db) + len(da)), np.int32)
+    if lib().orc_grad_schedule(db.ctypes.data, len(db), da.ctypes.data, len(da), ctas, off,
+                               idx) != 0:
+        raise ValueError("schedule oracle: invalid input")
+    return off, idx[: len(db) + len(da)]
 
 
 def round_bf16(a):

@@ -429,3 +429,50 @@ int64_t orc_plan_tiles(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t
   free(off);
   return sink.n;
 }
+
+/* ---- gradient-launch schedule (LPT), restated from the documented rule ------------------ */
+typedef struct {
+  int64_t cost;
+  int32_t i;
+} orc_costed;
+
+static int orc_costed_cmp(const void* a, const void* b) {
+  const orc_costed* x = (const orc_costed*)a;
+  const orc_costed* y = (const orc_costed*)b;
+  if (x->cost != y->cost) return x->cost > y->cost ? -1 : 1; /* cost descending */
+  return x->i < y->i ? -1 : (x->i > y->i); /* then index ascending (a stable sort) */
+}
+
+int orc_grad_schedule(const int32_t* tiles_db, int64_t n_db, const int32_t* tiles_da,
+                      int64_t n_da, int32_t ctas, int32_t* off, int32_t* idx) {
+  if (ctas < 1 || n_db < 0 || n_da < 0) return -1;
+  const int64_t n = n_db + n_da;
+  orc_costed* order = (orc_costed*)malloc(sizeof(orc_costed) * (n > 0 ? n : 1));
+  int64_t* load = (int64_t*)calloc(ctas, sizeof(int64_t));
+  int32_t* owner = (int32_t*)malloc(sizeof(int32_t) * (n > 0 ? n : 1));
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t* t = i < n_db ? tiles_db + 8 * i : tiles_da + 8 * (i - n_db);
+    const int64_t pad = t[7], pad64 = (pad + 63) / 64 * 64;
+    order[i].cost = (int64_t)(t[3] - t[2]) * 2 * (128 + pad64) + 4 * 128 * pad;
+    order[i].i = (int32_t)i;
+  }
+  qsort(order, (size_t)n, sizeof(orc_costed), orc_costed_cmp);
+  for (int64_t q = 0; q < n; ++q) { /* least-loaded CTA, lowest index on ties */
+    int32_t best = 0;
+    for (int32_t c = 1; c < ctas; ++c)
+      if (load[c] < load[best]) best = c;
+    owner[q] = best;
+    load[best] += order[q].cost;
+  }
+  off[0] = 0;
+  int32_t w = 0;
+  for (int32_t c = 0; c < ctas; ++c) { /* per CTA, in assignment order */
+    for (int64_t q = 0; q < n; ++q)
+      if (owner[q] == c) idx[w++] = order[q].i;
+    off[c + 1] = w;
+  }
+  free(order);
+  free(load);
+  free(owner);
+  return 0;
+}

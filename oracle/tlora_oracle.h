@@ -66,6 +66,15 @@ int orc_aimd_step(int32_t* n, int32_t* has_prev, double* t_prev, int32_t alpha, 
 int64_t orc_plan_tiles(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t* ranks,
                        const int32_t* token_slot, int32_t which, int32_t* out, int64_t cap);
 
+/* Schedule oracle: static LPT assignment of one dB+dA gradient launch's tiles (the dB table
+ * then the dA table, 8 int32 per tile as orc_plan_tiles returns them) to `ctas` CTAs.
+ * Tile cost = (ke0 - kb0) * 2 * (128 + ceil64(pad)) + 4 * 128 * pad; tiles taken by cost
+ * descending (ties: lower index first), each to the least-loaded CTA (ties: lower CTA).
+ * Writes off[ctas + 1] and idx[n_db + n_da] (CSR, CTA c runs idx[off[c] .. off[c+1])).
+ * Restates the plan's documented schedule; returns 0 or -1. */
+int orc_grad_schedule(const int32_t* tiles_db, int64_t n_db, const int32_t* tiles_da,
+                      int64_t n_da, int32_t ctas, int32_t* off, int32_t* idx);
+
 /* bf16 round-to-nearest-even of a double (via fp32), returned as a double. */
 double orc_round_bf16(double x);
 

@@ -78,6 +78,11 @@ SIGNATURES = {
     "tlora_plan_row_map": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
     "tlora_gather_rows": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p),
                                     C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_void_p]),
+    "tlora_plan_grad_schedule_host": (C.c_int, [C.c_int64, C.c_int64, C.c_int32,
+                                                C.POINTER(C.c_int32), C.c_int64,
+                                                C.POINTER(C.c_int32), C.c_int32,
+                                                C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                                C.c_int32, C.POINTER(C.c_int32)]),
     "tlora_plan_destroy": (C.c_int, [C.c_void_p]),
     "tlora_plan_get_info": (C.c_int, [C.c_void_p, C.POINTER(PlanInfoC)]),
     "tlora_plan_get_tiles": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(TileC), C.c_int32,

@@ -1289,6 +1289,24 @@ int tlora_plan_tiles_host(int64_t d, int64_t k, int32_t num_slots, const int32_t
   });
 }
 
+int tlora_plan_grad_schedule_host(int64_t d, int64_t k, int32_t num_slots, const int32_t* ranks,
+                                  int64_t tokens, const int32_t* token_slot, int32_t ctas,
+                                  int32_t* off, int32_t* idx, int32_t cap, int32_t* count) {
+  return guarded([&] {
+    require(num_slots >= 1 && ranks != nullptr && token_slot != nullptr, TLORA_ERR_ARG,
+            "null argument");
+    require(tokens >= 1, TLORA_ERR_SHAPE, "plan needs at least one token");
+    require(ctas >= 1, TLORA_ERR_ARG, "ctas must be >= 1");
+    const auto L = tlora::RegistryLayout::make(d, k, std::vector<int32_t>(ranks, ranks + num_slots));
+    const auto P = tlora::build_plan(L, tokens, token_slot);
+    std::vector<int32_t> o, x;
+    tlora::grad_schedule(P.tiles[TLORA_L_DB], P.tiles[TLORA_L_DA], ctas, o, x);
+    if (count) *count = (int32_t)x.size();
+    if (off) std::memcpy(off, o.data(), o.size() * sizeof(int32_t));
+    if (idx) std::memcpy(idx, x.data(), std::min<size_t>(cap, x.size()) * sizeof(int32_t));
+  });
+}
+
 }  // extern "C"
 
 // ==================================================================== launch bodies

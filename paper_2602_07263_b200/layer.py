@@ -313,6 +313,22 @@ def reduce_slots(recv, world, slot_rows, row0, rows, k, out, stream=None):
          int(k), _ptr(out), _stream_ptr(stream))
 
 
+def grad_schedule_host(d: int, k: int, ranks, token_slot, ctas: int):
+    """(off[ctas+1], idx): the LPT CTA tile lists of the plan's dB+dA launch (host only)."""
+    rk = (C.c_int32 * len(ranks))(*[int(r) for r in ranks])
+    ts = np.ascontiguousarray(np.asarray(token_slot, dtype=np.int32))
+    n = C.c_int32()
+    off = np.zeros(ctas + 1, np.int32)
+    I32 = C.POINTER(C.c_int32)
+    call("tlora_plan_grad_schedule_host", int(d), int(k), len(ranks), rk, int(ts.shape[0]),
+         ts.ctypes.data_as(I32), int(ctas), off.ctypes.data_as(I32), None, 0, C.byref(n))
+    idx = np.zeros(max(1, n.value), np.int32)
+    call("tlora_plan_grad_schedule_host", int(d), int(k), len(ranks), rk, int(ts.shape[0]),
+         ts.ctypes.data_as(I32), int(ctas), off.ctypes.data_as(I32), idx.ctypes.data_as(I32),
+         n.value, C.byref(n))
+    return off, idx[: n.value]
+
+
 def plan_tiles_host(d: int, k: int, ranks, token_slot, launch: int) -> np.ndarray:
     """Host-only tile table (no device), identical to what Plan uploads."""
     rk = (C.c_int32 * len(ranks))(*[int(r) for r in ranks])

@@ -23,7 +23,7 @@ from golden_io import read_records  # noqa: E402
 
 from paper_2602_07263_b200 import capi  # noqa: E402
 from paper_2602_07263_b200.layer import (AimdState, aimd_step, op_cost, partition,  # noqa: E402
-                                         plan_tiles_host)
+                                         grad_schedule_host, plan_tiles_host)
 from paper_2602_07263_b200.workload import c5_cell, config  # noqa: E402
 from conftest import has_gpu  # noqa: E402
 
@@ -101,6 +101,36 @@ def test_plan_bit_identical_to_plan_oracle(case):
         want = O.plan_tiles(len(slots), d, k, ranks, slots, launch)
         assert got.shape == want.shape, (launch, got.shape, want.shape)
         assert np.array_equal(got, want), launch
+
+
+@pytest.mark.parametrize("case", range(len(_plan_cases())))
+def test_grad_schedule_bit_identical_to_schedule_oracle(case):
+    """The LPT CTA tile lists the plan uploads for its dB+dA launch equal the oracle's
+    restatement of the rule (cost, order, tie-breaks) for 148 CTAs and a small grid; every
+    tile is scheduled exactly once."""
+    d, k, ranks, slots = _plan_cases()[case]
+    db = O.plan_tiles(len(slots), d, k, ranks, slots, capi.L_DB)
+    da = O.plan_tiles(len(slots), d, k, ranks, slots, capi.L_DA)
+    for ctas in (148, 7):
+        off, idx = grad_schedule_host(d, k, ranks, slots, ctas)
+        want_off, want_idx = O.grad_schedule(db, da, ctas)
+        assert np.array_equal(off, want_off) and np.array_equal(idx, want_idx)
+        assert np.array_equal(np.sort(idx), np.arange(len(db) + len(da)))
+
+
+def test_grad_schedule_balances_c2():
+    """On every C2 projection the busiest CTA carries <= 1.15x the mean bytes (round-robin
+    over the largest-first list: 1.31-1.53x)."""
+    c2 = config("C2")
+    slots = c2.token_slots()
+    for _, d, k in c2.projections:
+        tiles = np.concatenate([plan_tiles_host(d, k, c2.ranks, slots, capi.L_DB),
+                                plan_tiles_host(d, k, c2.ranks, slots, capi.L_DA)])
+        cost = ((tiles[:, 3] - tiles[:, 2]).astype(np.int64) * 2 * (128 + (tiles[:, 7] + 63) // 64 * 64)
+                + 4 * 128 * tiles[:, 7].astype(np.int64))
+        off, idx = grad_schedule_host(d, k, c2.ranks, slots, 148)
+        load = np.array([cost[idx[off[c]:off[c + 1]]].sum() for c in range(148)])
+        assert load.max() <= 1.15 * load.mean()
 
 
 def test_plan_covers_every_owned_column():
