@@ -104,6 +104,13 @@ int tlora_copy_to_device(void* dst, int dst_dtype, const void* src_host, int src
 int tlora_copy_to_host(void* dst_host, int dst_dtype, const void* src, int src_dtype,
                        int64_t count, void* stream);
 int tlora_stream_sync(void* stream);
+/* Enqueue-only helpers for copy-engine collectives over peer-mapped (NVLink) memory:
+ * cudaMemcpyAsync(cudaMemcpyDefault); a 32-bit flag write ordered after all prior work
+ * of the stream (cuStreamWriteValue32, fenced); a wait until *addr >= value
+ * (cuStreamWaitValue32 GEQ). No SM is used by any of the three. */
+int tlora_copy_async(void* dst, const void* src, size_t bytes, void* stream);
+int tlora_stream_write_u32(void* stream, void* addr, uint32_t value);
+int tlora_stream_wait_u32(void* stream, void* addr, uint32_t value);
 
 /* ---- layer: one adapted projection (frozen base W + adapter registry) --------- */
 /* ranks[num_slots]: registry layout in reference adapter order (std::map by job_id,

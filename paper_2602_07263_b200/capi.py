@@ -54,6 +54,9 @@ SIGNATURES = {
     "tlora_copy_to_host": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int64,
                                      C.c_void_p]),
     "tlora_stream_sync": (C.c_int, [C.c_void_p]),
+    "tlora_copy_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "tlora_stream_write_u32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32]),
+    "tlora_stream_wait_u32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32]),
     "tlora_layer_create": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int32,
                                      C.POINTER(C.c_int32), C.POINTER(C.c_void_p)]),
     "tlora_layer_destroy": (C.c_int, [C.c_void_p]),

@@ -800,6 +800,49 @@ int tlora_stream_sync(void* stream) {
   return guarded([&] { TL_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream))); });
 }
 
+// Stream memory operations (executed by the GPU front end, no SM): the copy-engine
+// all-gather's completion flags in peer-mapped memory.
+namespace {
+using StreamValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+StreamValueFn stream_value_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  require(cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
+              q == cudaDriverEntryPointSuccess && p != nullptr,
+          TLORA_ERR_CUDA, std::string(name) + " unavailable");
+  return reinterpret_cast<StreamValueFn>(p);
+}
+}  // namespace
+
+int tlora_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  return guarded([&] {
+    if (bytes == 0) return;
+    require(dst != nullptr && src != nullptr, TLORA_ERR_ARG, "null pointer");
+    TL_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault,
+                            reinterpret_cast<cudaStream_t>(stream)));
+  });
+}
+
+int tlora_stream_write_u32(void* stream, void* addr, uint32_t value) {
+  return guarded([&] {
+    static StreamValueFn fn = stream_value_fn("cuStreamWriteValue32");
+    require(addr != nullptr, TLORA_ERR_ARG, "null address");
+    const CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr),
+                          value, 0 /* CU_STREAM_WRITE_VALUE_DEFAULT: fenced after prior work */);
+    require(r == CUDA_SUCCESS, TLORA_ERR_CUDA, "cuStreamWriteValue32 failed (" + std::to_string((int)r) + ")");
+  });
+}
+
+int tlora_stream_wait_u32(void* stream, void* addr, uint32_t value) {
+  return guarded([&] {
+    static StreamValueFn fn = stream_value_fn("cuStreamWaitValue32");
+    require(addr != nullptr, TLORA_ERR_ARG, "null address");
+    const CUresult r = fn(reinterpret_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(addr),
+                          value, 0 /* CU_STREAM_WAIT_VALUE_GEQ */);
+    require(r == CUDA_SUCCESS, TLORA_ERR_CUDA, "cuStreamWaitValue32 failed (" + std::to_string((int)r) + ")");
+  });
+}
+
 int tlora_layer_create(int device, int64_t d, int64_t k, int32_t num_slots, const int32_t* ranks,
                        tlora_layer** out) {
   return guarded([&] {

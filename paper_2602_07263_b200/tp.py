@@ -27,12 +27,15 @@ norms and activations are outside the path); the collective pattern is the real 
 """
 from __future__ import annotations
 
+import ctypes as _C
+import os
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
+from .capi import call as _call
 from .layer import AimdState, FusedLoRALayer, aimd_step, partition, reduce_slots
 from .workload import INPUT_GROUP, Workload
 
@@ -185,7 +188,108 @@ class TPLayerSetStep:
                 buf = symm_mem.empty(P, T // P, k, dtype=bf, device=self.dev)
                 self.recv[name] = buf
                 self.recv_hdl[name] = symm_mem.rendezvous(buf, grp)
+        # Copy-engine all-gather (TLORA_TP_CE_AG, default on at P > 1). NCCL's all-gather
+        # kernels need SMs that the persistent fused GEMMs hold for their whole launch (at
+        # TP4 a nano-batch's boundary traffic took ~6 ms, as long as its compute). Here the
+        # gathered buffers live in symmetric (peer-mapped) memory; each rank pushes its
+        # shard rows into every peer's buffer with cudaMemcpyAsync on the comm stream (copy
+        # engines over NVLink, no SM), then raises its flag in each peer's flag array
+        # (cuStreamWriteValue32, fenced after the copies). The consumer's compute stream
+        # waits for every peer's flag to reach the gather's epoch (cuStreamWaitValue32).
+        # Epochs advance identically on all ranks (same gather sequence). Buffer reuse is
+        # ordered by the step structure: a rank pushes into a buffer only after it consumed
+        # a later flag of that peer, raised after the peer's last read of the buffer.
+        self.ce_ag = P > 1 and os.environ.get("TLORA_TP_CE_AG", "1") != "0"
+        self.ag_hdl = {}
+        if self.ce_ag:
+            import torch.distributed._symmetric_memory as symm_mem
+            grp = group if group is not None else dist.group.WORLD
+
+            def symm(key, like):
+                buf = symm_mem.empty(*like.shape, dtype=like.dtype, device=self.dev)
+                self.ag_hdl[key] = symm_mem.rendezvous(buf, grp)
+                return buf
+
+            for g in self.groups:
+                self.X_full[g] = symm(("X", g), self.X_full[g])
+            for name in list(self.H_full):
+                self.H_full[name] = symm(("H", name), self.H_full[name])
+            for name in list(self.dY_full):
+                self.dY_full[name] = symm(("dY", name), self.dY_full[name])
+            # reduce-scatter by push: receive slots [P][T/P][width] (slot = source rank);
+            # every rank copies its partial rows of owner q's shard into q's slot, then the
+            # owner sums the P slots in fixed order (reduce_slots, deterministic)
+            self.rs_recv = {}
+            for g in self.groups:
+                w = self.dX_shard[g].shape[1]
+                self.rs_recv[("rsX", g)] = symm(("rsX", g), torch.empty(P, T // P, w, dtype=bf))
+            for name in list(self.dH_shard):
+                w = self.dH_shard[name].shape[1]
+                self.rs_recv[("rsH", name)] = symm(("rsH", name), torch.empty(P, T // P, w, dtype=bf))
+            self.flags = symm_mem.empty(P, dtype=torch.int32, device=self.dev)
+            self.flags.zero_()
+            self.flag_hdl = symm_mem.rendezvous(self.flags, grp)
+            self._epoch = 0
+            torch.cuda.synchronize(self.dev)
+            dist.barrier(group=grp)  # every rank's flags are zero before any push
         torch.cuda.synchronize(self.dev)
+
+    def _ag_ce(self, stream, items, b) -> int:
+        """Push this rank's rows of nano-batch b into every rank's gathered buffers (the
+        all_gather_into_tensor layout: rank r's shard at rows b.t0 + r * b.tokens / P),
+        then raise this rank's flag on every peer. Returns the epoch to wait for."""
+        P, r = self.world, self.rank
+        nr = b.tokens // P
+        sp = _C.c_void_p(stream.cuda_stream)
+        for key, full, shard in items:
+            row_bytes = full.shape[1] * full.element_size()
+            off, nbytes = (b.t0 + r * nr) * row_bytes, nr * row_bytes
+            ptrs = self.ag_hdl[key].buffer_ptrs
+            for j in range(P):  # peers first in ring order from the next rank, self last
+                q = (r + 1 + j) % P
+                _call("tlora_copy_async", _C.c_void_p(int(ptrs[q]) + off),
+                      _C.c_void_p(shard.data_ptr()), _C.c_size_t(nbytes), sp)
+        self._epoch += 1
+        for q in range(P):
+            if q != r:
+                _call("tlora_stream_write_u32", sp,
+                      _C.c_void_p(int(self.flag_hdl.buffer_ptrs[q]) + 4 * r), self._epoch)
+        return self._epoch
+
+    def _rs_ce(self, stream, items, b):
+        """Reduce-scatter of nano-batch b by copy-engine push: for each (key, partial rows
+        [b.tokens x w], output shard rows [b.tokens / P x w]) this rank copies the chunk
+        owned by rank q into q's receive slot `rank`, raises its flags, waits for every
+        peer's, and sums its own P slots (reduce_slots) into the output, all on `stream`."""
+        P, r = self.world, self.rank
+        nr, slot_rows, row0 = b.tokens // P, self.T // P, b.t0 // P
+        sp = _C.c_void_p(stream.cuda_stream)
+        for key, part, out in items:
+            w = part.shape[1]
+            row_bytes = w * part.element_size()
+            ptrs = self.ag_hdl[key].buffer_ptrs
+            dst_off = (r * slot_rows + row0) * row_bytes
+            for j in range(P):
+                q = (r + 1 + j) % P
+                _call("tlora_copy_async", _C.c_void_p(int(ptrs[q]) + dst_off),
+                      _C.c_void_p(part.data_ptr() + q * nr * row_bytes),
+                      _C.c_size_t(nr * row_bytes), sp)
+        self._epoch += 1
+        for q in range(P):
+            if q != r:
+                _call("tlora_stream_write_u32", sp,
+                      _C.c_void_p(int(self.flag_hdl.buffer_ptrs[q]) + 4 * r), self._epoch)
+        self._ag_wait(stream, self._epoch)
+        for key, part, out in items:
+            recv = self.rs_recv[key]
+            reduce_slots(recv, P, slot_rows, row0, nr, recv.shape[2], out, stream=stream)
+
+    def _ag_wait(self, stream, epoch):
+        sp = _C.c_void_p(stream.cuda_stream)
+        base = self.flags.data_ptr()
+        for q in range(self.world):
+            if q != self.rank:
+                _call("tlora_stream_wait_u32", sp, _C.c_void_p(base + 4 * q), epoch)
 
     # -------------------------------------------------------------- plans per N
     def plans(self, n: int):
@@ -278,21 +382,31 @@ class TPLayerSetStep:
             b = nb[i]
             M.wait_event(ev)
             self._mark(M, "comm_ag_f", i, 0)
+            epoch = None
             with torch.cuda.stream(M):
-                for g in self.groups:
-                    self._ag(self._rows(self.X_full[g], b), self._srows(self.X_shard[g], b))
-                for p in cols:
-                    self._ag(self._rows(self.H_full[p], b), self._srows(self.H_shard[p], b))
+                if self.ce_ag:
+                    items = ([(("X", g), self.X_full[g], self._srows(self.X_shard[g], b))
+                              for g in self.groups] +
+                             [(("H", p), self.H_full[p], self._srows(self.H_shard[p], b))
+                              for p in cols])
+                    epoch = self._ag_ce(M, items, b)
+                else:
+                    for g in self.groups:
+                        self._ag(self._rows(self.X_full[g], b), self._srows(self.X_shard[g], b))
+                    for p in cols:
+                        self._ag(self._rows(self.H_full[p], b), self._srows(self.H_shard[p], b))
             self._mark(M, "comm_ag_f", i, 1)
             ev2 = torch.cuda.Event()
             ev2.record(M)
-            return ev2
+            return ev2, epoch
 
         ev_g = gather(0, shrink(0))
         for i in range(len(nb)):
             ev_next = gather(i + 1, shrink(i + 1)) if i + 1 < len(nb) else None
             b = nb[i]
-            C.wait_event(ev_g)
+            C.wait_event(ev_g[0])
+            if ev_g[1] is not None:
+                self._ag_wait(C, ev_g[1])
             self._mark(C, "comp_f", i, 0)
             for p in cols:
                 self.layers[p].fused_gemm(plans[i][p][0], self._rows(self.X_full[INPUT_GROUP[p]], b),
@@ -349,13 +463,18 @@ class TPLayerSetStep:
             b = nb[i]
             M.wait_event(start)
             self._mark(M, "comm_ag_b", i, 0)
+            epoch = None
             with torch.cuda.stream(M):
-                for p in rows:
-                    self._ag(self._rows(self.dY_full[p], b), self._srows(self.dY_shard[p], b))
+                if self.ce_ag:
+                    epoch = self._ag_ce(M, [(("dY", p), self.dY_full[p],
+                                             self._srows(self.dY_shard[p], b)) for p in rows], b)
+                else:
+                    for p in rows:
+                        self._ag(self._rows(self.dY_full[p], b), self._srows(self.dY_shard[p], b))
             self._mark(M, "comm_ag_b", i, 1)
             ev = torch.cuda.Event()
             ev.record(M)
-            return ev
+            return ev, epoch
 
         def grad_a_cols(i, ev):
             b = nb[i]
@@ -371,7 +490,9 @@ class TPLayerSetStep:
             ev_dy_next = gather_dy(i + 1) if i + 1 < len(nb) else None
             b = nb[i]
             beta = 1.0 if i else 0.0
-            C.wait_event(ev_dy)
+            C.wait_event(ev_dy[0])
+            if ev_dy[1] is not None:
+                self._ag_wait(C, ev_dy[1])
             self._mark(C, "comp_b", i, 0)
             # Chained schedule (as runner.LayerSetStep): each dX launch also computes the
             # NEXT projection's dH as extra tiles (tlora_backward_dx_dh), so only the first
@@ -416,10 +537,16 @@ class TPLayerSetStep:
             M.wait_event(ev_c)
             self._mark(M, "comm_rs_b", i, 0)
             with torch.cuda.stream(M):
-                for g in self.groups:
-                    self._rs(self._srows(self.dX_shard[g], b), self._rows(self.dX_part[g], b))
-                for p in cols:
-                    self._rs(self._srows(self.dH_shard[p], b), self._rows(self.dH_part[p], b))
+                if self.ce_ag:
+                    self._rs_ce(M, [(("rsX", g), self._rows(self.dX_part[g], b),
+                                     self._srows(self.dX_shard[g], b)) for g in self.groups] +
+                                [(("rsH", p), self._rows(self.dH_part[p], b),
+                                  self._srows(self.dH_shard[p], b)) for p in cols], b)
+                else:
+                    for g in self.groups:
+                        self._rs(self._srows(self.dX_shard[g], b), self._rows(self.dX_part[g], b))
+                    for p in cols:
+                        self._rs(self._srows(self.dH_shard[p], b), self._rows(self.dH_part[p], b))
             self._mark(M, "comm_rs_b", i, 1)
             ev_r = torch.cuda.Event()
             ev_r.record(M)
