@@ -221,6 +221,18 @@ def run_ours(args, rank, world, local_rank):
     pending = []
 
     bucket_at_end = os.environ.get("TLORA_DP_BUCKET", "per_layer") == "end"
+    # DP gradient all-reduce by copy-engine push (paper_2602_07263_b200/dp.py), opt-in with
+    # TLORA_DP_CE=1 (A/B on C2: +1.4% at DP2, -1.5% at DP4, where every rank pushes its
+    # full gradients to 3 peers; NCCL's ring stays the default). Skipped when its
+    # double-buffered receive slots would exceed 24 GB per GPU.
+    push_ar = None
+    if world > 1 and not bucket_at_end and os.environ.get("TLORA_DP_CE", "0") == "1":
+        sizes = {key: sum(g.numel() for g in lay.packed_grads()) for key, lay in step.layers.items()}
+        if 2 * world * 4 * sum(sizes.values()) <= (24 << 30):
+            from paper_2602_07263_b200.dp import PushAllReduce
+            push_ar = PushAllReduce(world, rank, local_rank)
+            for key, n in sizes.items():
+                push_ar.register(key, n)
 
     def allreduce_grads(name, layer, ready=None):
         if bucket_at_end:
@@ -234,7 +246,11 @@ def run_ours(args, rank, world, local_rank):
         with torch.cuda.stream(comm_stream):
             comm_stream.wait_event(ev)
             dAT, dB = layer.packed_grads()
-            works = [dist.all_reduce(dAT, async_op=True), dist.all_reduce(dB, async_op=True)]
+            if push_ar is not None:
+                push_ar.allreduce(name, [dAT, dB], comm_stream)
+                works = []
+            else:
+                works = [dist.all_reduce(dAT, async_op=True), dist.all_reduce(dB, async_op=True)]
             pending.extend(works)
             if opt_inline:  # this projection's AdamW right after its all-reduce, overlapping
                 for w in works:  # the rest of the backward (comm stream waits, host does not)
@@ -256,6 +272,8 @@ def run_ours(args, rank, world, local_rank):
 
     def bwd():
         cb = allreduce_grads if world > 1 else None
+        if push_ar is not None:
+            push_ar.next_step()
         if args.overlap != 0:
             step.backward_overlapped(stream, on_layer_done=cb)
         else:
@@ -506,6 +524,9 @@ def run_ours(args, rank, world, local_rank):
                    "projections": wl.projections, "token_order": ("shuffled" + (" (gathered plan)" if step.gathered else " (plain plan)"))
                    if args.shuffle else "job-contiguous",
                    "parallelism": f"dp{world}", "lowrank_side_stream_sms": args.overlap,
+                   "dp_allreduce": (None if world == 1 else
+                                    "copy-engine push + stream flags" if push_ar is not None
+                                    else "nccl"),
                    "dp_sm_reserve": os.environ.get("TLORA_SM_RESERVE") if world > 1 else None,
                    "nccl_max_nchannels": os.environ.get("NCCL_MAX_NCHANNELS") if world > 1 else None,
                    "cuda_graph": used_graph, "chained_lowrank": step.chain,
