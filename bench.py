@@ -222,13 +222,12 @@ def run_ours(args, rank, world, local_rank):
 
     bucket_at_end = os.environ.get("TLORA_DP_BUCKET", "per_layer") == "end"
     # DP gradient all-reduce by copy-engine push (paper_2602_07263_b200/dp.py), opt-in with
-    # TLORA_DP_CE=1 (A/B on C2: +1.4% at DP2, -1.5% at DP4, where every rank pushes its
-    # full gradients to 3 peers; NCCL's ring stays the default). Skipped when its
-    # double-buffered receive slots would exceed 24 GB per GPU.
+    # TLORA_DP_CE=1 (NCCL's ring stays the default; A/B in profiles/r1c_summary.md).
+    # Skipped when its double-buffered slots would exceed 24 GB per GPU.
     push_ar = None
     if world > 1 and not bucket_at_end and os.environ.get("TLORA_DP_CE", "0") == "1":
         sizes = {key: sum(g.numel() for g in lay.packed_grads()) for key, lay in step.layers.items()}
-        if 2 * world * 4 * sum(sizes.values()) <= (24 << 30):
+        if 2 * 2 * 4 * sum(sizes.values()) <= (24 << 30):
             from paper_2602_07263_b200.dp import PushAllReduce
             push_ar = PushAllReduce(world, rank, local_rank)
             for key, n in sizes.items():
