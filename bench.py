@@ -779,6 +779,13 @@ def main():
             os.environ.setdefault("MASTER_PORT", "29555")
             os.environ.setdefault("RANK", str(rank))
             os.environ.setdefault("WORLD_SIZE", str(world))
+            # The image sets NCCL_DEBUG=VERSION, whose only effect is a "NCCL version ..."
+            # banner on stdout ahead of the JSON line: drop that level. Other levels keep
+            # their log, sent to a per-process file (an explicit NCCL_DEBUG_FILE wins).
+            if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+                del os.environ["NCCL_DEBUG"]
+            elif os.environ.get("NCCL_DEBUG"):
+                os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/tlora_nccl.%h.%p.log")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out = run_tp(args, rank, world, local_rank) if args.tp else run_ours(args, rank, world, local_rank)
     if rank == 0:

@@ -110,9 +110,15 @@ def main():
         bad.append("reduce_scatter")
     if tp == 1 and not torch.equal(rsd.cpu(), x.cpu()):
         bad.append("reduce_scatter (tp=1 identity)")
+    # NCCL reduces bf16 in bf16: every partial sum of the ring/tree is rounded (half an ulp,
+    # 2^-9 relative), so after world-1 additions and the final store the error is bounded by
+    # world * 2^-9 * sum_p |x_p| (x2 margin below). Exact for world = 2 (one rounding).
     ar_ref = sum(xs[p].float() for p in range(world))
-    if not torch.allclose(ar.cpu().float(), ar_ref, rtol=1e-2, atol=1e-2):
-        bad.append("all_reduce")
+    ar_bound = world * 2.0 ** -8 * sum(xs[p].float().abs() for p in range(world)) + 1e-6
+    ar_err = (ar.cpu().float() - ar_ref).abs()
+    if not bool((ar_err <= ar_bound).all()):
+        bad.append(f"all_reduce max|d|={ar_err.max().item():.3e} "
+                   f"worst ratio={(ar_err / ar_bound).max().item():.2f}")
     capi.call("tlora_comm_destroy", h)
     lay.close()
     ok = torch.tensor([0 if bad else 1])
