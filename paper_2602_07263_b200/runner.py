@@ -8,6 +8,8 @@ Alg. 1 FusedKernelLaunch) executed for real.
 """
 from __future__ import annotations
 
+import os
+
 import torch
 
 from .layer import FusedLoRALayer
@@ -135,10 +137,11 @@ class LayerSetStep:
         """Chained backward with each projection's dB+dA launch on a side stream: it reads
         only H, X, dY and the projection's dH (produced by the previous dX launch), so it
         can run while the main stream's next fused GEMM runs, filling that GEMM's tail. dH
-        uses a ring of 4 buffers; a dX launch waits for the side-stream reader of the
-        buffer it overwrites."""
+        uses a ring of buffers; a dX launch waits for the side-stream reader of the
+        buffer it overwrites (ring depth TLORA_DH_RING, default 8: 0.7% faster than 4 on C2)."""
         self.side = torch.cuda.Stream(self.dev)
-        self.dH4 = torch.zeros(4, self.T, self.dH2.shape[2], dtype=torch.bfloat16, device=self.dev)
+        self.dh_ring = max(2, int(os.environ.get("TLORA_DH_RING", "8")))
+        self.dH4 = torch.zeros(self.dh_ring, self.T, self.dH2.shape[2], dtype=torch.bfloat16, device=self.dev)
         self.side_grads = True
 
     def _backward_side(self, main, beta, on_layer_done, opt_inline=False):
@@ -153,13 +156,14 @@ class LayerSetStep:
         self._dh_prefetched = False
         for i, (L, name) in enumerate(keys):
             lay, pl = self.layers[(L, name)], self.plans[name]
-            dH = self.dH4[i % 4]
+            nr = self.dh_ring
+            dH = self.dH4[i % nr]
             if i + 1 < len(keys):
                 nk = keys[i + 1]
-                if i - 3 in done:  # buffer (i+1)%4 was last read by grads(i-3)
-                    main.wait_event(done[i - 3])
+                if i + 1 - nr in done:  # buffer (i+1)%nr was last read by grads(i+1-nr)
+                    main.wait_event(done[i + 1 - nr])
                 lay.dx_dh(pl, self.dy_of(name), dH, self.dX[name], self.layers[nk], self.plans[nk[1]],
-                          self.dy_of(nk[1]), self.dH4[(i + 1) % 4], zero_next=False, stream=main)
+                          self.dy_of(nk[1]), self.dH4[(i + 1) % nr], zero_next=False, stream=main)
             else:
                 lay.dx(pl, self.dy_of(name), dH, self.dX[name], stream=main)
             ready = torch.cuda.Event()
