@@ -438,10 +438,12 @@ def test_cuda_graph_replay_matches_eager():
 
 
 @pytest.mark.parametrize("tokens", [(256, 256, 256), (300, 77, 513)])
-def test_chained_lowrank_tiles_are_bit_identical(tokens):
+def test_chained_lowrank_tiles_are_bit_identical(tokens, monkeypatch):
     """Chained schedule (next projection's shrink / dH as extra CTA-pair tiles of the fused
     GEMM launch: tlora_forward_gemm_shrink / tlora_backward_dx_dh) vs one launch per op:
-    Y, dX, H stashes and adapter gradients bitwise equal, ragged token counts included."""
+    Y, dX, H stashes and adapter gradients bitwise equal, ragged token counts included.
+    The side-stream variant runs with dH ring depths 2 (a wait before every dX launch) and
+    8 (no waits over these 6 projections)."""
     from paper_2602_07263_b200.runner import LayerSetStep
     from paper_2602_07263_b200.workload import Job, Workload
 
@@ -449,10 +451,12 @@ def test_chained_lowrank_tiles_are_bit_identical(tokens):
                   [Job("a", 8, 2, tokens[0]), Job("b", 200, 3, tokens[1]),
                    Job("c", 16, 1, tokens[2])], layers=2)
     out = []
-    for chain, side in ((False, False), (True, False), (True, True)):
+    for chain, side, ring in ((False, False, 0), (True, False, 0), (True, True, 2), (True, True, 8)):
         st = LayerSetStep(wl, device=0, seed=7, chain=chain)
         if side:  # dB+dA launches on a side stream (runner.enable_side_grads)
+            monkeypatch.setenv("TLORA_DH_RING", str(ring))
             st.enable_side_grads()
+            assert st.dh_ring == ring
         st.forward()
         st.backward()
         torch.cuda.synchronize()
