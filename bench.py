@@ -25,6 +25,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "aggregate LoRA training tokens/sec (all jobs) at 1/2/4/8 B200; tensor-pipe %"
+NANO_DEFAULT = 1  # executor nano-batches per step (0 = AIMD every step); see DESIGN.md §5c
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
                   "source": "fallback (B200_PROFILING.md)"}
 
@@ -180,13 +181,289 @@ def cpu_reference_sample(wl, tokens_per_job: int, seconds_budget: float, threads
     the reference has none) when present, else the oracle port (oracle/liboracle.so).
     Returns dict(value tokens/s, cores, kind, sample) or None.
     """
-    from paper_2602_07263_b200 import cpu_baseline
-    return cpu_baseline.measure(wl, tokens_per_job=tokens_per_job, seconds_budget=seconds_budget,
+    return _bench_cpu().measure(wl, tokens_per_job=tokens_per_job, seconds_budget=seconds_budget,
                                 threads=threads)
 
 
+def _bench_cpu():
+    """oracle/bench_cpu.py: the CPU baseline leg (lives with the oracle, outside the
+    product package; only this leg and the reference arm execute oracle/)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import bench_cpu
+    return bench_cpu
+
+
+def ref_tokens_per_job(wl, threads: int, per_thread: int = 64) -> int:
+    """Reference-arm / cpu_baseline sample: >= per_thread tokens per host thread."""
+    return max(8, -(-per_thread * threads // len(wl.jobs)))
+
+
 # ------------------------------------------------------------------------------ GPU arm
+def make_comm(local_rank, rank, world):
+    """tlora_comm (NCCL through the C-ABI) for the executor's data-parallel all-reduce: rank 0
+    makes the unique id, torch.distributed broadcasts it (host plumbing only)."""
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from paper_2602_07263_b200 import capi
+    uid = torch.zeros(capi.UNIQUE_ID_BYTES, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        buf = (C.c_uint8 * capi.UNIQUE_ID_BYTES)()
+        capi.call("tlora_comm_get_unique_id", buf)
+        uid.copy_(torch.tensor(list(bytes(buf)), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    idb = (C.c_uint8 * capi.UNIQUE_ID_BYTES)(*uid.cpu().tolist())
+    h = C.c_void_p()
+    capi.call("tlora_comm_create", local_rank, idb, world, rank, 1, C.byref(h))
+    return h
+
+
+def run_executor(args, rank, world, local_rank):
+    """Default arm: the C++ step executor (tlora_step_*) — rank-aware nano-batches, AIMD on
+    the measured step time (nano 0) or a fixed N, chained fused GEMMs, side-stream
+    gradients, masked AdamW, DP all-reduce through the C-ABI communicator, CUDA graphs at
+    one replica. Python only builds inputs, times and reports."""
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from paper_2602_07263_b200 import capi
+    from paper_2602_07263_b200.step import TrainingStep
+    from paper_2602_07263_b200.workload import config
+
+    torch.cuda.set_device(local_rank)
+    capi.call("tlora_device_check", local_rank, None)
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    wl = config(args.config)
+    if args.layers > 0:
+        wl.layers = args.layers
+    comm = make_comm(local_rank, rank, world) if world > 1 else None
+    st = TrainingStep(wl, device=local_rank, nano_fixed=max(0, args.nano_batches),
+                      nano_init=args.nano_init, graphs=not args.no_graph, input_sets=2,
+                      comm=comm)
+    st.init_random(seed=wl.seed + rank)
+    st.enable_optimizer()
+    stream = torch.cuda.current_stream()
+    clocks.wait_ready()
+    for _ in range(args.warmup):
+        st.run(stream=stream)
+    torch.cuda.synchronize()
+    # untimed settle steps (>= 1 s under load); every rank runs the same count
+    t_clk0 = time.time()
+    while True:
+        for _ in range(3):
+            st.run(stream=stream)
+        el = torch.tensor([time.time() - t_clk0], device="cuda", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        if el.item() >= 1.0:
+            break
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    lib = capi.lib()
+    graph_launches = n_launch = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    traj = []
+    e0.record(stream)
+    for i in range(args.steps):
+        last = i == args.steps - 1 and os.environ.get("TLORA_BENCH_PROF", "1") != "0"
+        if last:  # the LAST timed step runs eagerly with CUDA events around every launch
+            capi.call("tlora_profile_begin")
+        s_ = st.run(eager=last, stream=stream)
+        traj.append([s_.nano_used, round(s_.ms, 3)])
+        n_launch += s_.launches  # kernels of the step (a replay counts its captured kernels)
+        if s_.replayed_graph:
+            graph_launches += 1
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    cnt = (C.c_int32 * 6)()
+    ms6 = (C.c_double * 6)()
+    fl6 = (C.c_double * 6)()
+    capi.call("tlora_profile_end", cnt, ms6, fl6)
+    t_clk1 = time.time()
+    clk = clocks.stop(window=(t_clk0, t_clk1))
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    ms_per_step = ms / args.steps
+    tokens = wl.tokens * world
+    value = tokens / (ms_per_step / 1e3)
+
+    # ---- e2e: host pinned inputs -> H2D (copy stream, double-buffered input sets) -> the
+    # executor's step on the set -> D2H of every adapter gradient; step i+1's H2D overlaps
+    # step i, step i+1 starts after step i's gradients are on the host.
+    bind_host_numa(local_rank)
+    sets = [list(st.X[s].values()) + list(st.dY[s].values()) for s in range(2)]
+    host_in = [t.cpu().pin_memory() for t in sets[0]]
+    grads = [g for lay in st.layers.values() for g in lay.packed_grads()]
+    host_out = [torch.empty(g.shape, dtype=g.dtype, pin_memory=True) for g in grads]
+    h2d = sum(t.numel() * t.element_size() for t in host_in)
+    d2h = sum(t.numel() * t.element_size() for t in host_out)
+    copy, copy_out = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def e2e_run(nsteps):
+        done = [torch.cuda.Event() for _ in range(nsteps)]
+        ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_out = None
+        with torch.cuda.stream(copy):
+            for h, d in zip(host_in, sets[0]):
+                d.copy_(h, non_blocking=True)
+            ev_in[0].record(copy)
+        for i in range(nsteps):
+            s = i % 2
+            stream.wait_event(ev_in[s])
+            if ev_out is not None:
+                stream.wait_event(ev_out)  # grads of step i-1 are on the host before reuse
+            with torch.cuda.stream(copy):  # next step's inputs, while this step runs
+                if i + 1 < nsteps:
+                    if i >= 1:
+                        copy.wait_event(done[i - 1])  # set (i+1)%2 was last read by step i-1
+                    for h, d in zip(host_in, sets[(i + 1) % 2]):
+                        d.copy_(h, non_blocking=True)
+                    ev_in[(i + 1) % 2].record(copy)
+            st.run(input_set=s, stream=stream)
+            done[i].record(stream)
+            with torch.cuda.stream(copy_out):
+                copy_out.wait_event(done[i])
+                for g, h in zip(grads, host_out):
+                    h.copy_(g, non_blocking=True)
+                ev_out = torch.cuda.Event()
+                ev_out.record(copy_out)
+        stream.wait_event(ev_out)
+
+    e2e_run(2)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(2, min(args.steps, 10))
+    f0.record(stream)
+    e2e_run(e2e_steps)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+
+    roofline = roofline_block(cnt, ms6, fl6, "CUDA-event brackets around every launch of the "
+                              "LAST timed step (eager, same kernels as the replayed graph); "
+                              "per-launch durations of that step")
+    cpu = cpu_f32 = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        tpj = args.cpu_tokens_per_job or ref_tokens_per_job(wl, threads)
+        cpu = cpu_reference_sample(wl, tokens_per_job=tpj, seconds_budget=args.cpu_seconds,
+                                   threads=threads)
+        cpu_f32 = _bench_cpu().measure_oracle_f32(wl, tokens_per_job=tpj,
+                                                  seconds_budget=min(10.0, args.cpu_seconds),
+                                                  threads=threads)
+    flops_step = wl.flops_fwd_bwd() * world
+    nano_desc = (f"fixed N={args.nano_batches} (the reference's config.fixed_n)"
+                 if args.nano_batches > 0 else
+                 f"AIMD every step from N={args.nano_init} (nano_pipeline.hpp:99-112, "
+                 "sim_engine.hpp:306-315)")
+    return {
+        "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded normal activations/grads, random-init W and adapters)",
+        "config": {"workload": f"{wl.name}: {wl.notes}", "layers_per_step": wl.layers,
+                   "tokens_per_gpu": wl.tokens,
+                   "jobs": [[j.job_id, j.rank, j.tokens] for j in wl.jobs],
+                   "projections": wl.projections, "parallelism": f"dp{world}",
+                   "driver": "C++ step executor (tlora_step_run: libtlora.so)",
+                   "nano_batches": nano_desc, "aimd_trajectory_n_ms": traj,
+                   "dp_allreduce": None if world == 1 else "nccl via tlora_comm (C-ABI), per key "
+                                   "after its last nano-batch, on the executor's comm stream",
+                   "cuda_graph": not args.no_graph and world == 1,
+                   "graph_replays_timed": graph_launches,
+                   "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)",
+                   "algorithmic_tflop_per_step": round(flops_step / 1e12, 3),
+                   "achieved_tflops_step": round(flops_step / (ms_per_step / 1e3) / 1e12, 1)},
+        "e2e": {"value": round(tokens / (e2e_ms / 1e3), 1), "unit": "tokens/s",
+                "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "h2d_gb_per_s": round(h2d / (e2e_ms / 1e3) / 1e9, 2),
+                "bound": "PCIe host->device (raw pinned copy ~55.5 GB/s, tools/pcie_probe.py)",
+                "path": "host pinned inputs -> H2D into the executor's input set -> "
+                        "tlora_step_run -> D2H of the adapter gradients (H2D of step i+1 "
+                        "overlapped with step i)"},
+        "gpu_launches": n_launch,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "cpu_baseline_oracle_f32": cpu_f32,
+        "clocks": clk,
+    }
+
+
+def roofline_block(cnt, ms6, fl6, timing):
+    """Roofline of the dominant kernel family (the fused base+LoRA GEMM: fwd + dX) from the
+    live per-launch CUDA-event times and algorithmic FLOPs of one step."""
+    from paper_2602_07263_b200 import capi
+    peaks = load_peaks()
+    fam_ms = ms6[capi.L_FWD] + ms6[capi.L_DX]
+    fam_fl = fl6[capi.L_FWD] + fl6[capi.L_DX]
+    achieved = fam_fl / (fam_ms / 1e3) / 1e12 if fam_ms > 0 else 0.0
+    peak = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+    total_ms = sum(ms6)
+    names = list(capi.LAUNCH_NAMES)
+    if cnt[capi.L_DA] == 0 and cnt[capi.L_DB] > 0:
+        names[capi.L_DB] = "dB+dA (one launch)"
+    per_launch = {names[i]: {
+        "launches": cnt[i], "ms_total": round(ms6[i], 3),
+        "tflops": round(fl6[i] / (ms6[i] / 1e3) / 1e12, 1) if ms6[i] > 0 else None,
+        "share_of_gemm_time": round(ms6[i] / total_ms, 4) if total_ms > 0 else None}
+        for i in range(6)}
+    traffic = traffic_alg = commit = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        try:
+            tj = json.loads(tp.read_text())
+            traffic = tj.get("dram_bytes_per_launch_mean", tj.get("fwd_bytes_per_launch"))
+            traffic_alg = tj.get("algorithmic_bytes_per_launch_mean")
+            commit = tj.get("commit")
+        except Exception:
+            traffic = None
+    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
+            "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak else None,
+            "frac_of_burst": round(achieved / float(peaks["bf16_tflops"]), 4),
+            "timing": timing, "traffic": traffic, "traffic_algorithmic_bytes": traffic_alg,
+            "traffic_source": "profiles/traffic.json (ncu dram bytes, mean per fused-GEMM launch"
+                              + (f", captured at commit {commit})" if commit else ")"),
+            "kernel": "lora_gemm2_kernel (2-CTA fused base+LoRA GEMM: fwd + dX)",
+            "peak_source": peaks["source"] + " sustained bf16", "per_launch": per_launch}
+
+
+def run_cpp_host(args):
+    """--host cpp: the pure C++ host (tests/cpp/_build/step_main: LayerSetTrainer over the
+    C-ABI, no Python in the loop) prints its own BENCH-format line; add clocks around it."""
+    import torch
+    binp = ROOT / "tests" / "cpp" / "_build" / "step_main"
+    if not binp.exists():
+        subprocess.run(["make", "-C", str(ROOT), "tests/cpp/_build/step_main"], check=True)
+    clocks = ClockSampler(0)
+    clocks.start()
+    clocks.wait_ready()
+    t0 = time.time()
+    p = subprocess.run([str(binp), "bench", args.config, str(args.steps), str(args.warmup),
+                        str(max(0, args.nano_batches)), str(max(0, args.layers))],
+                       capture_output=True, text=True, check=True)
+    clk = clocks.stop(window=(t0, time.time()))
+    out = json.loads(p.stdout.strip().splitlines()[-1])
+    out["clocks"] = clk
+    out["gpu_launches"] = None
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
+    """--driver python: round 1's Python per-launch driver (runner.LayerSetStep), kept as the
+    executor's bitwise cross-check and for the shuffled / overlap experiments."""
     import torch
     import torch.distributed as dist
     from paper_2602_07263_b200 import capi
@@ -500,8 +777,10 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference_sample(wl, tokens_per_job=args.cpu_tokens_per_job,
-                                   seconds_budget=args.cpu_seconds, threads=os.cpu_count() or 1)
+        threads = os.cpu_count() or 1
+        cpu = cpu_reference_sample(wl, tokens_per_job=args.cpu_tokens_per_job or
+                                   ref_tokens_per_job(wl, threads),
+                                   seconds_budget=args.cpu_seconds, threads=threads)
 
     flops_step = wl.flops_fwd_bwd() * world
     out = {
@@ -682,10 +961,10 @@ def run_reference(args, rank, world):
     wl = config(args.config)
     if rank != 0:
         return None
-    from paper_2602_07263_b200 import cpu_baseline
     threads = os.cpu_count() or 1
-    res = cpu_baseline.measure(wl, tokens_per_job=args.ref_tokens_per_job, seconds_budget=0.0,
-                               threads=threads, repeats=args.steps)
+    tpj = args.ref_tokens_per_job or ref_tokens_per_job(wl, threads)
+    res = _bench_cpu().measure(wl, tokens_per_job=tpj, seconds_budget=0.0, threads=threads,
+                               repeats=args.steps)
     if res is None or res.get("value") is None:
         why = (res or {}).get("sample", "reference CPU build missing (make ref)")
         return {"impl": "reference", "unavailable": why}
@@ -699,7 +978,8 @@ def run_reference(args, rank, world):
         "scaling": "weak", "vs_baseline": None, "dtype": res["dtype"],
         "data": "synthetic (seeded)",
         "config": {"workload": f"{wl.name}: {wl.notes}", "sample": res["sample"],
-                   "tokens_per_step": res.get("tokens_per_repeat")},
+                   "tokens_per_step": res.get("tokens_per_repeat"),
+                   "tokens_per_thread": res.get("tokens_per_thread"), "threads": threads},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": res["cores"],
                          "kind": res["kind"], "sample": res["sample"]},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
@@ -719,9 +999,11 @@ def main():
                     help="override the config's layer count (0 = as configured)")
     ap.add_argument("--shuffle", action="store_true", help="interleave jobs' tokens")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-tokens-per-job", type=int, default=8)
+    ap.add_argument("--cpu-tokens-per-job", type=int, default=0,
+                    help="cpu_baseline sample per job (0 = 64 tokens per host thread)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-tokens-per-job", type=int, default=8)
+    ap.add_argument("--ref-tokens-per-job", type=int, default=0,
+                    help="reference-arm sample per job (0 = 64 tokens per host thread)")
     ap.add_argument("--overlap", type=int, default=0,
                     help="low-rank launches on a side stream concurrent with the fused GEMMs: "
                          "N>0 caps them to N SMs (GEMMs get the rest), -1 = uncapped, "
@@ -735,6 +1017,14 @@ def main():
     ap.add_argument("--tp", action="store_true",
                     help="tensor-parallel layer set over the torchrun group (default config C4)")
     ap.add_argument("--nano", type=int, default=4, help="initial nano-batch count (TP mode)")
+    ap.add_argument("--driver", default="cpp", choices=["cpp", "python"],
+                    help="cpp: the C++ step executor (default); python: runner.LayerSetStep")
+    ap.add_argument("--host", default="python", choices=["python", "cpp"],
+                    help="cpp: run the pure C++ host binary (tests/cpp/_build/step_main)")
+    ap.add_argument("--nano-batches", type=int, default=NANO_DEFAULT,
+                    help="executor: fixed nano-batch count N (> 0), or 0 = AIMD every step")
+    ap.add_argument("--nano-init", type=int, default=4,
+                    help="executor: AIMD initial N (reference default 4)")
     ap.add_argument("--fused-rs", default="auto",
                     help="TP mode: comma list of row-parallel projections (o,down) whose "
                          "reduce-scatter is fused into the GEMM epilogue (bulk copies into "
@@ -779,15 +1069,17 @@ def main():
             os.environ.setdefault("MASTER_PORT", "29555")
             os.environ.setdefault("RANK", str(rank))
             os.environ.setdefault("WORLD_SIZE", str(world))
-            # The image sets NCCL_DEBUG=VERSION, whose only effect is a "NCCL version ..."
-            # banner on stdout ahead of the JSON line: drop that level. Other levels keep
-            # their log, sent to a per-process file (an explicit NCCL_DEBUG_FILE wins).
-            if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
-                del os.environ["NCCL_DEBUG"]
-            elif os.environ.get("NCCL_DEBUG"):
-                os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/tlora_nccl.%h.%p.log")
+            # NCCL_DEBUG / NCCL_DEBUG_FILE stay as the environment sets them (the driver
+            # reads NCCL's init lines); the JSON line is the last line rank 0 prints.
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    out = run_tp(args, rank, world, local_rank) if args.tp else run_ours(args, rank, world, local_rank)
+    if args.host == "cpp":
+        out = run_cpp_host(args)
+    elif args.tp:
+        out = run_tp(args, rank, world, local_rank)
+    elif args.driver == "python" or args.shuffle or args.overlap != 0:
+        out = run_ours(args, rank, world, local_rank)
+    else:
+        out = run_executor(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1 or args.tp:

@@ -140,11 +140,15 @@ struct DeviceBuffer {
 };
 
 // One fused layer built from the reference-style inputs: registry (slots in std::map
-// order), padded bf16 device copies, and the plan of this batch. The batch is laid out on
-// the device job-sorted (tlora_segments: the CSR form of segment_rows for every job, rows
-// ascending within a job), gathered during the host-side conversion at no extra cost, so
-// arbitrarily interleaved segment maps (test_fused_lora.cpp:45-46) run as job-contiguous
-// tiles; results are scattered back to the caller's row order.
+// order), padded bf16 device copies, and the plan of this batch. Only adapters that some
+// token references are registered — the same set check_shapes validates (fused_lora.hpp:
+// 70-77) and fused_forward reads (:104 skips jobs without rows) — so an unreferenced
+// adapter of any shape is never touched. A referenced rank-0 adapter (A d x 0, B 0 x k:
+// its delta is exactly zero) is registered as a zero rank-1 adapter. The batch is laid
+// out on the device job-sorted (tlora_segments: the CSR form of segment_rows for every
+// job, rows ascending within a job), gathered during the host-side conversion at no extra
+// cost, so arbitrarily interleaved segment maps (test_fused_lora.cpp:45-46) run as
+// job-contiguous tiles; results are scattered back to the caller's row order.
 class DeviceLayer {
  public:
   DeviceLayer(const TokenBatch& batch, const Matrix& W,
@@ -155,26 +159,32 @@ class DeviceLayer {
         k_(W.cols()),
         dp_(round8(d_)),
         kp_(round8(k_)) {
-    std::vector<int32_t> ranks;
     std::map<std::string, int32_t> slot_of;
-    for (const auto& [id, a] : by_id) {
-      slot_of[id] = static_cast<int32_t>(ranks.size());
-      ranks.push_back(static_cast<int32_t>(a->A.cols()));
+    for (const auto& id : batch.segment_map) slot_of.emplace(id, 0);
+    std::vector<int32_t> ranks;
+    for (auto& [id, slot] : slot_of) {  // std::map order of the referenced ids
+      slot = static_cast<int32_t>(ranks.size());
+      const Index r = by_id.at(id)->A.cols();
       ids_.push_back(id);
+      true_rank_.push_back(r);
+      ranks.push_back(static_cast<int32_t>(r > 0 ? r : 1));
     }
     tl_check(tlora_layer_create(dev_, dp_, kp_, static_cast<int32_t>(ranks.size()), ranks.data(),
                                 &layer_));
     const auto wp = padded(W, dp_, kp_);
     tl_check(tlora_layer_set_base(layer_, wp.data(), TLORA_F64, TLORA_HOST, nullptr));
-    for (const auto& [id, a] : by_id) {
-      const auto ap = padded(a->A, dp_, a->A.cols());
-      const auto bp = padded(a->B, a->B.rows(), kp_);
-      tl_check(tlora_layer_set_adapter(layer_, slot_of[id], ap.data(), bp.data(), TLORA_F64,
-                                       TLORA_HOST, nullptr));
+    for (size_t s = 0; s < ids_.size(); ++s) {
+      const AdapterMatrices& a = *by_id.at(ids_[s]);
+      const Index r = ranks[s];
+      // rank 0: zero d x 1 / 1 x k (padded() of an empty matrix is all zeros)
+      const auto ap = padded(a.A, dp_, r);
+      const auto bp = padded(a.B, r, kp_);
+      tl_check(tlora_layer_set_adapter(layer_, static_cast<int32_t>(s), ap.data(), bp.data(),
+                                       TLORA_F64, TLORA_HOST, nullptr));
     }
     tl_check(tlora_layer_layout(layer_, nullptr, &R_));
     std::vector<int32_t> slots(static_cast<size_t>(T_));
-    for (Index t = 0; t < T_; ++t) slots[static_cast<size_t>(t)] = slot_of[batch.segment_map[t]];
+    for (Index t = 0; t < T_; ++t) slots[static_cast<size_t>(t)] = slot_of.at(batch.segment_map[t]);
     perm_.resize(static_cast<size_t>(T_));
     std::vector<int64_t> offsets(ranks.size() + 1);
     tl_check(tlora_segments(T_, slots.data(), static_cast<int32_t>(ranks.size()), perm_.data(),
@@ -204,6 +214,7 @@ class DeviceLayer {
     return out;
   }
 
+  // Gradients of the referenced adapters (the others get zeros from fused_backward).
   FusedGradients backward(const Matrix& dY) {
     DeviceBuffer g(dev_, static_cast<size_t>(T_ * kp_ * 2));
     DeviceBuffer dX(dev_, static_cast<size_t>(T_ * dp_ * 2));
@@ -219,13 +230,14 @@ class DeviceLayer {
         out.dX(static_cast<Index>(perm_[static_cast<size_t>(i)]), j) = dx[static_cast<size_t>(i * dp_ + j)];
     for (size_t s = 0; s < ids_.size(); ++s) {
       const auto& id = ids_[s];
-      const Index r = rank_of(s);
-      std::vector<float> da(static_cast<size_t>(dp_ * r)), db(static_cast<size_t>(r * kp_));
+      const Index r = true_rank_[s];
+      const Index rr = r > 0 ? r : 1;
+      std::vector<float> da(static_cast<size_t>(dp_ * rr)), db(static_cast<size_t>(rr * kp_));
       tl_check(tlora_layer_read_grad(layer_, static_cast<int32_t>(s), da.data(), db.data(),
                                      TLORA_HOST, nullptr));
       Matrix A(d_, r), B(r, k_);
       for (Index i = 0; i < d_; ++i)
-        for (Index j = 0; j < r; ++j) A(i, j) = da[static_cast<size_t>(i * r + j)];
+        for (Index j = 0; j < r; ++j) A(i, j) = da[static_cast<size_t>(i * rr + j)];
       for (Index i = 0; i < r; ++i)
         for (Index j = 0; j < k_; ++j) B(i, j) = db[static_cast<size_t>(i * kp_ + j)];
       out.dA[id] = std::move(A);
@@ -234,30 +246,22 @@ class DeviceLayer {
     return out;
   }
 
-  void set_ranks(std::vector<Index> r) { ranks_ = std::move(r); }
-
  private:
-  Index rank_of(size_t s) const { return ranks_.at(s); }
-
   int dev_;
   Index T_, d_, k_, dp_, kp_;
   int32_t R_ = 0;
   tlora_layer* layer_ = nullptr;
   tlora_plan* plan_ = nullptr;
-  std::vector<std::string> ids_;
-  std::vector<Index> ranks_;
-  std::vector<int64_t> perm_;  // device row i holds the caller's token perm_[i]
+  std::vector<std::string> ids_;   // referenced job ids, std::map order (= slot order)
+  std::vector<Index> true_rank_;   // their ranks (0 allowed)
+  std::vector<int64_t> perm_;      // device row i holds the caller's token perm_[i]
   std::unique_ptr<DeviceBuffer> X_, H_;
 };
 
 inline std::unique_ptr<DeviceLayer> make_device_layer(
     const TokenBatch& batch, const Matrix& W,
     const std::map<std::string, const AdapterMatrices*>& by_id) {
-  auto L = std::make_unique<DeviceLayer>(batch, W, by_id);
-  std::vector<Index> ranks;
-  for (const auto& [id, a] : by_id) ranks.push_back(a->A.cols());
-  L->set_ranks(std::move(ranks));
-  return L;
+  return std::make_unique<DeviceLayer>(batch, W, by_id);
 }
 
 }  // namespace detail
@@ -292,9 +296,25 @@ inline FusedGradients fused_backward(const TokenBatch& batch, const Matrix& base
   detail::check_shapes(batch, base_weight, by_id);
   if (dY.rows() != batch.rows.rows() || dY.cols() != base_weight.cols())
     throw std::runtime_error("fused_lora: upstream gradient shape != token count x k");
+  if (batch.rows.rows() == 0) {
+    FusedGradients out;
+    out.dX = Matrix(0, batch.rows.cols());
+    for (const auto& [id, a] : by_id) {
+      out.dA[id] = Matrix::Zero(a->A.rows(), a->A.cols());
+      out.dB[id] = Matrix::Zero(a->B.rows(), a->B.cols());
+    }
+    return out;
+  }
   auto L = detail::make_device_layer(batch, base_weight, by_id);
   L->forward();
-  return L->backward(dY);
+  FusedGradients out = L->backward(dY);
+  // adapters no token references have zero gradients (shaped like the adapter itself)
+  for (const auto& [id, a] : by_id)
+    if (!out.dA.count(id)) {
+      out.dA[id] = Matrix::Zero(a->A.rows(), a->A.cols());
+      out.dB[id] = Matrix::Zero(a->B.rows(), a->B.cols());
+    }
+  return out;
 }
 
 // Unfused accounting (fused_lora.hpp:137-163), via the bit-identical C-ABI restatement.

@@ -14,8 +14,11 @@
  *     (passed as void* = cudaStream_t; NULL = legacy default stream).
  *   - Matrices are dense row-major. Activations/weights on device are bf16; adapter
  *     gradients are fp32. Host-side loaders accept f64 / f32 / bf16.
- *   - Distinct layers/plans are independent; calls on one layer are externally
- *     serialised per stream (reference contract: pure and reentrant).
+ *   - Distinct layers/plans are independent: every plan owns its scratch (split-K
+ *     partial planes, dH of tlora_backward, gather copies), so gradient launches of
+ *     different plans may run concurrently on different streams. Calls that use ONE plan
+ *     are serialised on one stream by the caller, and so are calls that write one layer's
+ *     gradients (reference contract: pure and reentrant).
  */
 #ifndef TLORA_H_
 #define TLORA_H_
@@ -27,7 +30,7 @@
 extern "C" {
 #endif
 
-#define TLORA_ABI_VERSION 4
+#define TLORA_ABI_VERSION 5
 
 enum tlora_status {
   TLORA_OK = 0,
@@ -142,6 +145,12 @@ int tlora_layer_set_optimizer(tlora_layer* layer, const float* lr, const float* 
 /* One AdamW step of every slot on grads * grad_scale (e.g. 1/world for a DP mean); writes
  * the fp32 masters/moments and refreshes the bf16 operand layouts the kernels read. */
 int tlora_layer_optimizer_step(tlora_layer* layer, float grad_scale, void* stream);
+/* The same step restricted to the slots with present[slot] != 0 (device int32 array of
+ * num_slots entries, e.g. tlora_plan_present_mask of the step's batch): a job with no
+ * tokens in the step takes no optimizer step (masters, moments and step counter stay as
+ * they are). present == NULL updates every slot (= tlora_layer_optimizer_step). */
+int tlora_layer_optimizer_step_masked(tlora_layer* layer, const int32_t* present, float grad_scale,
+                                      void* stream);
 /* Copy one slot's fp32 master adapter out: A is d x r, B is r x k. */
 int tlora_layer_read_adapter(tlora_layer* layer, int32_t slot, float* A, float* B, int where,
                              void* stream);
@@ -167,6 +176,9 @@ int tlora_plan_row_map(const tlora_plan* plan, int32_t* row_map);
 int tlora_gather_rows(const tlora_plan* plan, int32_t n, const void* const* src, void* const* dst,
                       const int64_t* width, void* stream);
 int tlora_plan_destroy(tlora_plan* plan);
+/* Device pointer (valid for the plan's lifetime) to num_slots int32 flags: 1 if the slot
+ * owns at least one token of this plan's batch. */
+int tlora_plan_present_mask(const tlora_plan* plan, const int32_t** present);
 int tlora_plan_get_info(const tlora_plan* plan, tlora_plan_info* info);
 /* Copy the tile table of `launch` into out[cap]; *count gets the table length. */
 int tlora_plan_get_tiles(const tlora_plan* plan, int launch, tlora_tile* out, int32_t cap,
@@ -208,7 +220,7 @@ int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, c
  * = shrink + gemm; tlora_backward = dh + dx + grad_b(H, dY) + grad_a(X, dH). H / dH are
  * T x R bf16, masked to each token's own packed-rank columns (zero elsewhere), so partial
  * H / dH summed across ranks stay valid operands. Calls on one plan are serialised on
- * one stream (the split-K workspace belongs to the plan). */
+ * one stream (the split-K partial planes belong to the plan). */
 int tlora_forward_shrink(tlora_layer* layer, const tlora_plan* plan, const void* X, void* H,
                          void* stream);
 int tlora_forward_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X, const void* H,
@@ -255,6 +267,13 @@ int tlora_backward_dx_dh(tlora_layer* layer, const tlora_plan* plan, const void*
                          const void* dH, void* dX, float beta, tlora_layer* next,
                          const tlora_plan* next_plan, const void* dY_next, void* dH_next,
                          int zero_next, void* stream);
+/* tlora_backward_dx of `layer` with the SHRINK of `next` (H_next = X_next·Aᵀcat masked, as
+ * tlora_forward_shrink) as extra tiles of the same launch: the last dX launch of one
+ * nano-batch carries the first shrink of the next nano-batch's forward. */
+int tlora_backward_dx_shrink(tlora_layer* layer, const tlora_plan* plan, const void* dY,
+                             const void* dH, void* dX, float beta, tlora_layer* next,
+                             const tlora_plan* next_plan, const void* X_next, void* H_next,
+                             int zero_next, void* stream);
 /* Both adapter gradients in ONE persistent launch (+ one split-K reduce): dB from (H, dY)
  * and dA from (X, dH); = tlora_backward_grad_b then tlora_backward_grad_a. */
 int tlora_backward_grads(tlora_layer* layer, const tlora_plan* plan, const void* H,
@@ -330,6 +349,110 @@ int tlora_comm_all_reduce(tlora_comm* comm, int group, const void* send, void* r
  * adapter gradients dA / dB over `group` (normally TLORA_GROUP_DP), in place. */
 int tlora_layer_allreduce_grads(tlora_layer* layer, tlora_comm* comm, int group, int average,
                                 void* stream);
+
+/* ---- synthetic data (seeded, deterministic on any device) --------------------------- */
+/* dst[i] = scale * N(0,1) sample i of the counter-based generator keyed by seed (bf16 or
+ * f32 device buffer, count elements). Lets C++ hosts and tests build identical inputs. */
+int tlora_fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, float scale,
+                      void* stream);
+
+/* ---- rank-aware nano-batch map (nano_pipeline.hpp:51-60 gives only counts) -------------
+ * Samples enumerated job-major (slot 0's batch[0] samples, then slot 1's, ...). per_nano =
+ * partition(sum batch, n) (bit-exact); samples are placed by weight[slot] descending (ties:
+ * lower slot), each on the least-loaded nano-batch with room left (ties: lower nano), which
+ * fixes nano_slot[n_out x num_slots] (samples of slot s in nano i); job s's samples then go
+ * to the nano-batches in nano order (its first nano_slot[0][s] to nano 0, ...): sample_nano
+ * [sum batch]. Errors as partition (TLORA_ERR_PLAN). Host-only. */
+int tlora_nano_assign(int32_t num_slots, const int32_t* batch, const int64_t* weight, int32_t n,
+                      int32_t* n_out, int32_t* per_nano, int32_t* sample_nano, int32_t* nano_slot);
+
+/* ---- the layer-set training step executor (the caller of the path: the iteration body of
+ * sim_engine.hpp:306-315 executed for real) ---------------------------------------------
+ * A step = for each nano-batch of the rank-aware map of N: forward of every (layer,
+ * projection) key in order, then backward in reverse order (gradients accumulate over the
+ * nano-batches), then the fused masked AdamW of every key (after the key's gradient
+ * all-reduce over the DP group when a communicator is given). N = nano_fixed if > 0, else
+ * the AIMD controller's n (nano_pipeline.hpp:99-112, driven by the CUDA-event time of every
+ * step, clamped to the combined batch as sim_engine.hpp:314). The step owns its layers
+ * (tlora_step_layer: set base / adapters / optimizer through the layer API) and its
+ * step-sized buffers (tlora_step_buffer); nano-batch i is the row range
+ * [nano_t0[i], nano_t0[i+1]) of every buffer (tlora_step_layout). */
+typedef struct tlora_step tlora_step;
+enum tlora_step_flags {
+  TLORA_STEP_SIDE_GRADS = 1, /* dB+dA (and AdamW) of each key on a side stream             */
+  TLORA_STEP_GRAPH = 2       /* capture each (N, input set) step into a CUDA graph after its
+                                first eager run and replay it (single replica only)        */
+};
+enum tlora_run_flags { TLORA_RUN_EAGER = 1 /* launch eagerly even if a graph exists */ };
+typedef struct tlora_step_desc {
+  int32_t device;
+  int32_t num_layers;
+  int32_t num_projections;
+  const int64_t* proj_d;      /* [P] in-features                                          */
+  const int64_t* proj_k;      /* [P] out-features                                         */
+  const int32_t* proj_input;  /* [P] input group: projections with one id read one X       */
+  int32_t num_slots;
+  const int32_t* ranks;       /* [S] registry layout, reference adapter order             */
+  const int32_t* batch;       /* [S] samples of each job in the step (JobSpec.batch_size) */
+  const int32_t* seq_len;     /* [S] tokens per sample (JobSpec.seq_len)                  */
+  int32_t y_dtype;            /* TLORA_BF16 or TLORA_F32                                  */
+  int32_t flags;              /* tlora_step_flags                                         */
+  int32_t dh_ring;            /* dH ring depth, 0 = 8                                     */
+  int32_t input_sets;         /* 1 or 2 input buffer sets (double-buffered host inputs)   */
+  int32_t nano_init;          /* AIMD initial n, 0 = 4 (sim_engine.hpp:63)                */
+  int32_t nano_fixed;         /* > 0: fixed N, no AIMD (the reference's config.fixed_n)   */
+  int32_t aimd_alpha;         /* 0 = 4                                                    */
+  double aimd_beta;           /* 0 = 0.5                                                  */
+  double aimd_tau_rel;        /* >= 0                                                     */
+} tlora_step_desc;
+typedef struct tlora_step_stats {
+  int32_t nano_used;      /* N of the step just run                                        */
+  int32_t next_nano;      /* N the controller chose for the next step                      */
+  double ms;              /* CUDA-event time of the step on the caller's stream            */
+  int32_t replayed_graph; /* 1 if the step was a CUDA-graph replay                         */
+  long long launches;     /* kernels in the step (a replay re-launches the eager run's)     */
+  int64_t tokens;
+} tlora_step_stats;
+enum tlora_buffer_kind {
+  TLORA_BUF_X = 0,  /* index = input group, per input set: T x d  bf16                     */
+  TLORA_BUF_DY = 1, /* index = projection, per input set: T x k  bf16 (upstream gradient) */
+  TLORA_BUF_Y = 2,  /* index = projection: T x k (y_dtype)                                 */
+  TLORA_BUF_DX = 3, /* index = projection: T x d bf16                                      */
+  TLORA_BUF_H = 4   /* index = key (layer * P + projection): T x R bf16 stash             */
+};
+int tlora_step_create(const tlora_step_desc* desc, tlora_comm* comm /* NULL: one replica */,
+                      tlora_step** out);
+int tlora_step_destroy(tlora_step* step);
+int tlora_step_layer(tlora_step* step, int32_t layer, int32_t proj, tlora_layer** out);
+int tlora_step_buffer(tlora_step* step, int32_t kind, int32_t index, int32_t set, void** ptr,
+                      int64_t* rows, int64_t* cols);
+/* Token layout for nano count n (plans are built on first use): *n_out = min(n, samples),
+ * nano_t0[n_out + 1] row offsets, nano_slot[n_out x S], sample_row[samples] first row of
+ * each sample (samples job-major). Any output may be NULL. */
+int tlora_step_layout(tlora_step* step, int32_t n, int32_t* n_out, int64_t* nano_t0,
+                      int32_t* nano_slot, int64_t* sample_row);
+/* N the next tlora_step_run will use (fill the inputs in that layout). */
+int tlora_step_next_n(const tlora_step* step, int32_t* n);
+/* One training step on input set `set`, enqueued on `stream` and waited for (the step time
+ * feeds AIMD). stats may be NULL. */
+int tlora_step_run(tlora_step* step, int32_t set, int32_t flags, void* stream,
+                   tlora_step_stats* stats);
+
+/* One op of the step schedule (host-only view for tests and drivers). */
+enum tlora_op_kind { TLORA_OP_SHRINK = 0, TLORA_OP_FWD = 1, TLORA_OP_DH = 2, TLORA_OP_DX = 3,
+                     TLORA_OP_GRADS = 4, TLORA_OP_ALLREDUCE = 5, TLORA_OP_ADAMW = 6 };
+enum tlora_stream_id { TLORA_STREAM_MAIN = 0, TLORA_STREAM_SIDE = 1, TLORA_STREAM_COMM = 2 };
+typedef struct tlora_step_op {
+  int32_t kind, stream, key, nano;
+  int32_t slot;                         /* dH ring slot read (DX, GRADS), -1            */
+  int32_t sec_kind, sec_key, sec_nano;  /* secondary tiles of a FWD / DX launch, -1     */
+  int32_t sec_slot;                     /* ring slot the secondary dH writes, -1         */
+  int32_t beta;                         /* GRADS: 1 = accumulate onto earlier nano-batches */
+  int32_t wait0, wait1;                 /* ops (on other streams) waited for, -1         */
+} tlora_step_op;
+int tlora_step_schedule_host(int32_t keys, int32_t nano, int32_t ring, int32_t side_grads,
+                             int32_t data_parallel, tlora_step_op* out, int32_t cap,
+                             int32_t* count);
 
 #ifdef __cplusplus
 }

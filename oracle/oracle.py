@@ -46,6 +46,16 @@ def lib():
         L.orc_grad_schedule.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32,
                                         _I, _I]
         L.orc_grad_schedule.restype = C.c_int
+        L.orc_nano_assign.argtypes = [C.c_int32, _I, np.ctypeslib.ndpointer(np.int64,
+                                                                            flags="C_CONTIGUOUS"),
+                                      C.c_int32, C.POINTER(C.c_int32), _I, _I, _I]
+        L.orc_nano_assign.restype = C.c_int
+        PF = C.POINTER(C.POINTER(C.c_float))
+        _F = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+        L.orc_train_step_f32.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int32, _I,
+                                         np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS"),
+                                         _F, _F, PF, PF, _F, _F, _F, PF, PF]
+        L.orc_train_step_f32.restype = None
         L.orc_round_bf16.argtypes = [C.c_double]
         L.orc_round_bf16.restype = C.c_double
         _lib = L
@@ -167,3 +177,44 @@ def round_bf16(a):
     lsb = (u >> 16) & 1
     u = ((u + 0x7FFF + lsb) & 0xFFFF0000).astype(np.uint32)
     return u.view(np.float32).astype(np.float64)
+
+
+def nano_assign(batch, weight, n):
+    """Rank-aware sample -> nano-batch map (orc_nano_assign): (n, per_nano, sample_nano,
+    nano_slot[n x S])."""
+    batch = _c(batch, np.int32)
+    weight = _c(weight, np.int64)
+    S, total = len(batch), int(batch.sum())
+    out_n = C.c_int32()
+    per = np.zeros(max(1, min(max(n, 1), max(total, 1))), np.int32)
+    sn = np.zeros(max(1, total), np.int32)
+    ns = np.zeros(max(1, per.size * S), np.int32)
+    if lib().orc_nano_assign(S, batch, weight, n, C.byref(out_n), per, sn, ns) != 0:
+        raise ValueError("nano_assign: invalid argument")
+    m = out_n.value
+    return m, per[:m].tolist(), sn[:total], ns[: m * S].reshape(m, S)
+
+
+def _ppf(mats):
+    arr = (C.POINTER(C.c_float) * len(mats))()
+    for i, m in enumerate(mats):
+        arr[i] = m.ctypes.data_as(C.POINTER(C.c_float))
+    return arr
+
+
+def train_step_f32(X, W, A, B, offsets, dY):
+    """fp32 fwd+bwd of one layer on a job-contiguous batch (orc_train_step_f32): the
+    CPU baseline's timed body. Returns Y, dX, dA, dB (float32)."""
+    X, W, dY = _c(X, np.float32), _c(W, np.float32), _c(dY, np.float32)
+    A = [_c(a, np.float32) for a in A]
+    B = [_c(b, np.float32) for b in B]
+    T, d = X.shape
+    k = W.shape[1]
+    ranks = np.array([a.shape[1] for a in A], np.int32)
+    Y = np.empty((T, k), np.float32)
+    dX = np.empty((T, d), np.float32)
+    dA = [np.empty_like(a) for a in A]
+    dB = [np.empty_like(b) for b in B]
+    lib().orc_train_step_f32(T, d, k, len(A), ranks, _c(offsets, np.int64), X, W, _ppf(A),
+                             _ppf(B), dY, Y, dX, _ppf(dA), _ppf(dB))
+    return Y, dX, dA, dB

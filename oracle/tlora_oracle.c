@@ -476,3 +476,183 @@ int orc_grad_schedule(const int32_t* tiles_db, int64_t n_db, const int32_t* tile
   free(owner);
   return 0;
 }
+
+
+/* ---------------------------------------------------------------- nano-batch map */
+int orc_nano_assign(int32_t S, const int32_t* batch, const int64_t* weight, int32_t n,
+                    int32_t* n_out, int32_t* per_nano, int32_t* sample_nano, int32_t* nano_slot) {
+  if (S < 1) return -1;
+  int64_t total = 0;
+  for (int32_t s = 0; s < S; ++s) {
+    if (batch[s] < 0 || weight[s] < 0) return -1;
+    total += batch[s];
+  }
+  if (total < 1 || total > 2147483647) return -1;
+  int32_t nn = 0;
+  if (orc_partition((int32_t)total, n, &nn, per_nano) != 0) return -1;
+  *n_out = nn;
+  int64_t* load = (int64_t*)calloc((size_t)nn, sizeof(int64_t));
+  int32_t* room = (int32_t*)malloc((size_t)nn * sizeof(int32_t));
+  char* done = (char*)calloc((size_t)S, 1);
+  int64_t* first = (int64_t*)malloc((size_t)S * sizeof(int64_t));
+  if (!load || !room || !done || !first) return -1;
+  for (int32_t i = 0; i < nn; ++i) room[i] = per_nano[i];
+  for (int64_t i = 0; i < (int64_t)nn * S; ++i) nano_slot[i] = 0;
+  int64_t acc = 0;
+  for (int32_t s = 0; s < S; ++s) {
+    first[s] = acc;
+    acc += batch[s];
+  }
+  /* slots by weight descending, ties by slot: brute-force selection (S is small) */
+  for (int32_t round = 0; round < S; ++round) {
+    int32_t best = -1;
+    for (int32_t s = 0; s < S; ++s)
+      if (!done[s] && (best < 0 || weight[s] > weight[best])) best = s;
+    done[best] = 1;
+    for (int32_t q = 0; q < batch[best]; ++q) {
+      int32_t pick = -1;
+      for (int32_t i = 0; i < nn; ++i)
+        if (room[i] > 0 && (pick < 0 || load[i] < load[pick])) pick = i;
+      --room[pick];
+      load[pick] += weight[best];
+      ++nano_slot[(int64_t)pick * S + best];
+    }
+  }
+  /* swap refinement: heaviest nano h (first on ties); first (o, a, b) in ascending order
+   * with nano_slot[h][a] > 0, nano_slot[o][b] > 0, weight[a] > weight[b] and
+   * load[o] + (weight[a] - weight[b]) < load[h]; swap one sample; repeat until none */
+  for (int32_t i = 0; i < nn; ++i) {
+    load[i] = 0;
+    for (int32_t s = 0; s < S; ++s) load[i] += (int64_t)nano_slot[(int64_t)i * S + s] * weight[s];
+  }
+  for (;;) {
+    int32_t h = 0, found = 0;
+    for (int32_t i = 1; i < nn; ++i)
+      if (load[i] > load[h]) h = i;
+    for (int32_t o = 0; o < nn && !found; ++o) {
+      if (o == h) continue;
+      for (int32_t a = 0; a < S && !found; ++a) {
+        if (!nano_slot[(int64_t)h * S + a]) continue;
+        for (int32_t b = 0; b < S && !found; ++b) {
+          if (!nano_slot[(int64_t)o * S + b] || weight[a] <= weight[b]) continue;
+          const int64_t delta = weight[a] - weight[b];
+          if (load[o] + delta >= load[h]) continue;
+          nano_slot[(int64_t)h * S + a]--;
+          nano_slot[(int64_t)h * S + b]++;
+          nano_slot[(int64_t)o * S + b]--;
+          nano_slot[(int64_t)o * S + a]++;
+          load[h] -= delta;
+          load[o] += delta;
+          found = 1;
+        }
+      }
+    }
+    if (!found) break;
+  }
+  /* which samples: a job's samples go to the nano-batches in nano order (the first
+   * nano_slot[0][s] samples to nano 0, ...), so each (nano, job) is a contiguous range */
+  for (int32_t s = 0; s < S; ++s) {
+    int64_t q = first[s];
+    for (int32_t i = 0; i < nn; ++i)
+      for (int32_t c = 0; c < nano_slot[(int64_t)i * S + s]; ++c) sample_nano[q++] = i;
+  }
+  free(load);
+  free(room);
+  free(done);
+  free(first);
+  return 0;
+}
+
+/* ---------------------------------------------------------------- fp32 CPU train step */
+#define ORC_RB 32 /* token rows per block: one W row is reused RB times from cache */
+
+/* C[rows x n] (+)= A[rows x p] · B[p x n] for a block of rows (all row-major, lda/ldc) */
+static void blk_nn_f32(int64_t rows, int64_t p, int64_t n, const float* A, int64_t lda,
+                       const float* B, float* C, int64_t ldc, int accumulate) {
+  if (!accumulate)
+    for (int64_t i = 0; i < rows; ++i)
+      for (int64_t j = 0; j < n; ++j) C[i * ldc + j] = 0.f;
+  for (int64_t q = 0; q < p; ++q) {
+    const float* b = B + q * n;
+    for (int64_t i = 0; i < rows; ++i) {
+      const float a = A[i * lda + q];
+      float* c = C + i * ldc;
+#pragma omp simd
+      for (int64_t j = 0; j < n; ++j) c[j] += a * b[j];
+    }
+  }
+}
+
+/* C[rows x n] (+)= A[rows x p] · B[n x p]ᵀ */
+static void blk_nt_f32(int64_t rows, int64_t p, int64_t n, const float* A, int64_t lda,
+                       const float* B, float* C, int64_t ldc, int accumulate) {
+  for (int64_t j = 0; j < n; ++j) {
+    const float* b = B + j * p;
+    for (int64_t i = 0; i < rows; ++i) {
+      const float* a = A + i * lda;
+      float acc = 0.f;
+#pragma omp simd reduction(+ : acc)
+      for (int64_t q = 0; q < p; ++q) acc += a[q] * b[q];
+      C[i * ldc + j] = accumulate ? C[i * ldc + j] + acc : acc;
+    }
+  }
+}
+
+void orc_train_step_f32(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t* ranks,
+                        const int64_t* off, const float* X, const float* W,
+                        const float* const* A, const float* const* B, const float* dY, float* Y,
+                        float* dX, float* const* dA, float* const* dB) {
+  int32_t rmax = 1;
+  for (int32_t s = 0; s < S; ++s) rmax = ranks[s] > rmax ? ranks[s] : rmax;
+  float* H = (float*)malloc((size_t)T * rmax * sizeof(float));
+  float* dH = (float*)malloc((size_t)T * rmax * sizeof(float));
+  const int64_t nblk = (T + ORC_RB - 1) / ORC_RB;
+  /* forward + dH + dX, token-row blocks in parallel (each block inside one job) */
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t t0 = b * ORC_RB, t1 = t0 + ORC_RB < T ? t0 + ORC_RB : T;
+    for (int32_t s = 0; s < S; ++s) {
+      const int64_t lo = off[s] > t0 ? off[s] : t0, hi = off[s + 1] < t1 ? off[s + 1] : t1;
+      if (lo >= hi) continue;
+      const int64_t r = ranks[s];
+      blk_nn_f32(hi - lo, d, r, X + lo * d, d, A[s], H + lo * rmax, rmax, 0);
+      blk_nt_f32(hi - lo, k, r, dY + lo * k, k, B[s], dH + lo * rmax, rmax, 0);
+    }
+    blk_nn_f32(t1 - t0, d, k, X + t0 * d, d, W, Y + t0 * k, k, 0);
+    blk_nt_f32(t1 - t0, k, d, dY + t0 * k, k, W, dX + t0 * d, d, 0);
+    for (int32_t s = 0; s < S; ++s) {
+      const int64_t lo = off[s] > t0 ? off[s] : t0, hi = off[s + 1] < t1 ? off[s + 1] : t1;
+      if (lo >= hi) continue;
+      const int64_t r = ranks[s];
+      blk_nn_f32(hi - lo, r, k, H + lo * rmax, rmax, B[s], Y + lo * k, k, 1);
+      blk_nt_f32(hi - lo, r, d, dH + lo * rmax, rmax, A[s], dX + lo * d, d, 1);
+    }
+  }
+  /* dA_s = X_sᵀ·dH_s (d x r), dB_s = H_sᵀ·dY_s (r x k): parallel over output rows */
+  for (int32_t s = 0; s < S; ++s) {
+    const int64_t r = ranks[s], lo = off[s], hi = off[s + 1];
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < d; ++i) {
+      float* out = dA[s] + i * r;
+      for (int64_t j = 0; j < r; ++j) out[j] = 0.f;
+      for (int64_t t = lo; t < hi; ++t) {
+        const float x = X[t * d + i];
+        const float* g = dH + t * rmax;
+        for (int64_t j = 0; j < r; ++j) out[j] += x * g[j];
+      }
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < r; ++i) {
+      float* out = dB[s] + i * k;
+      for (int64_t j = 0; j < k; ++j) out[j] = 0.f;
+      for (int64_t t = lo; t < hi; ++t) {
+        const float h = H[t * rmax + i];
+        const float* g = dY + t * k;
+#pragma omp simd
+        for (int64_t j = 0; j < k; ++j) out[j] += h * g[j];
+      }
+    }
+  }
+  free(H);
+  free(dH);
+}

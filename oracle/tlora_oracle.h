@@ -75,6 +75,29 @@ int64_t orc_plan_tiles(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t
 int orc_grad_schedule(const int32_t* tiles_db, int64_t n_db, const int32_t* tiles_da,
                       int64_t n_da, int32_t ctas, int32_t* off, int32_t* idx);
 
+/* Rank-aware nano-batch map (restates tlora_nano_assign, include/tlora.h; the reference
+ * only gives counts: nano_pipeline.hpp:51-60). Samples are enumerated job-major (slot 0's
+ * batch[0] samples, then slot 1's, ...). counts = partition(sum batch, n). Samples are
+ * taken by weight[slot] descending (ties: lower slot, then lower sample index) and each
+ * goes to the nano with the least accumulated weight among those with room left (ties:
+ * lower nano), then single-sample swaps between the heaviest nano and the others while
+ * they lower its load (first improving (o, a, b) in ascending order); this fixes nano_slot[n_out * S] (samples of slot s in nano i). Which
+ * samples: job s's samples go to the nano-batches in nano order (its first nano_slot[0][s]
+ * samples to nano 0, and so on), so every (nano, job) pair is one contiguous sample range.
+ * Writes *n_out, per_nano[n] (= partition's counts), sample_nano[sum batch] and nano_slot.
+ * Returns 0 or -1. */
+int orc_nano_assign(int32_t S, const int32_t* batch, const int64_t* weight, int32_t n,
+                    int32_t* n_out, int32_t* per_nano, int32_t* sample_nano, int32_t* nano_slot);
+
+/* fp32 training step of one fused layer (CPU baseline of bench.py, BASELINE.md §4 item 2:
+ * the repo's oracle, fp32 fwd+bwd, OpenMP over all host cores). Job-contiguous batch:
+ * slot s owns token rows [off[s], off[s+1]). Y = X·W + H·B, H_s = X_s·A_s; dH_s = dY_s·B_sᵀ,
+ * dX = dY·Wᵀ + dH·Aᵀ, dA_s = X_sᵀ·dH_s, dB_s = H_sᵀ·dY_s. Row-major fp32, cache-blocked. */
+void orc_train_step_f32(int64_t T, int64_t d, int64_t k, int32_t S, const int32_t* ranks,
+                        const int64_t* off, const float* X, const float* W,
+                        const float* const* A, const float* const* B, const float* dY, float* Y,
+                        float* dX, float* const* dA, float* const* dB);
+
 /* bf16 round-to-nearest-even of a double (via fp32), returned as a double. */
 double orc_round_bf16(double x);
 

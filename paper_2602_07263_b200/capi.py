@@ -42,6 +42,36 @@ class PlanInfoC(C.Structure):
     ]
 
 
+class StepDescC(C.Structure):
+    _fields_ = [
+        ("device", C.c_int32), ("num_layers", C.c_int32), ("num_projections", C.c_int32),
+        ("proj_d", C.POINTER(C.c_int64)), ("proj_k", C.POINTER(C.c_int64)),
+        ("proj_input", C.POINTER(C.c_int32)), ("num_slots", C.c_int32),
+        ("ranks", C.POINTER(C.c_int32)), ("batch", C.POINTER(C.c_int32)),
+        ("seq_len", C.POINTER(C.c_int32)), ("y_dtype", C.c_int32), ("flags", C.c_int32),
+        ("dh_ring", C.c_int32), ("input_sets", C.c_int32), ("nano_init", C.c_int32),
+        ("nano_fixed", C.c_int32), ("aimd_alpha", C.c_int32), ("aimd_beta", C.c_double),
+        ("aimd_tau_rel", C.c_double),
+    ]
+
+
+class StepStatsC(C.Structure):
+    _fields_ = [("nano_used", C.c_int32), ("next_nano", C.c_int32), ("ms", C.c_double),
+                ("replayed_graph", C.c_int32), ("launches", C.c_longlong), ("tokens", C.c_int64)]
+
+
+class StepOpC(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("kind", "stream", "key", "nano", "slot", "sec_kind",
+                                         "sec_key", "sec_nano", "sec_slot", "beta", "wait0",
+                                         "wait1")]
+
+
+STEP_SIDE_GRADS, STEP_GRAPH = 1, 2
+RUN_EAGER = 1
+BUF_X, BUF_DY, BUF_Y, BUF_DX, BUF_H = range(5)
+OP_SHRINK, OP_FWD, OP_DH, OP_DX, OP_GRADS, OP_ALLREDUCE, OP_ADAMW = range(7)
+STREAM_MAIN, STREAM_SIDE, STREAM_COMM = range(3)
+
 # exported symbol -> (restype, argtypes); also the list the CPU test checks against the header
 SIGNATURES = {
     "tlora_last_error": (C.c_char_p, []),
@@ -72,6 +102,9 @@ SIGNATURES = {
                                             C.POINTER(C.c_float), C.c_float, C.c_float,
                                             C.c_float]),
     "tlora_layer_optimizer_step": (C.c_int, [C.c_void_p, C.c_float, C.c_void_p]),
+    "tlora_layer_optimizer_step_masked": (C.c_int, [C.c_void_p, C.c_void_p, C.c_float,
+                                                    C.c_void_p]),
+    "tlora_plan_present_mask": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "tlora_layer_read_adapter": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int,
                                            C.c_void_p]),
     "tlora_plan_create": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int32),
@@ -147,6 +180,25 @@ SIGNATURES = {
                                 C.POINTER(C.c_longlong)]),
     "tlora_partition": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                                   C.POINTER(C.c_int32)]),
+    "tlora_backward_dx_shrink": (C.c_int, [C.c_void_p] * 5 + [C.c_float] + [C.c_void_p] * 4
+                                 + [C.c_int, C.c_void_p]),
+    "tlora_fill_normal": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_float,
+                                    C.c_void_p]),
+    "tlora_nano_assign": (C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
+                                    C.POINTER(C.c_int32), C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tlora_step_create": (C.c_int, [C.POINTER(StepDescC), C.c_void_p, C.POINTER(C.c_void_p)]),
+    "tlora_step_destroy": (C.c_int, [C.c_void_p]),
+    "tlora_step_layer": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    "tlora_step_buffer": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                    C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int64)]),
+    "tlora_step_layout": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_void_p,
+                                    C.c_void_p, C.c_void_p]),
+    "tlora_step_next_n": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    "tlora_step_run": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                 C.POINTER(StepStatsC)]),
+    "tlora_step_schedule_host": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                           C.POINTER(StepOpC), C.c_int32, C.POINTER(C.c_int32)]),
     "tlora_aimd_step": (C.c_int, [C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                   C.POINTER(C.c_double), C.c_int32, C.c_double, C.c_double,
                                   C.c_double]),

@@ -354,7 +354,7 @@ struct AdamJob {
 __global__ void __launch_bounds__(256) adamw_layer_kernel(
     const AdamJob j0, const AdamJob j1, const int32_t* __restrict__ row_slot,
     const float2* __restrict__ hp, int32_t* __restrict__ steps, int32_t num_slots, float b1,
-    float b2, float eps, float grad_scale, int64_t R) {
+    float b2, float eps, float grad_scale, int64_t R, const int32_t* __restrict__ present) {
   __shared__ float tile[32][65];
   __shared__ bool last;
   const bool second = (int)blockIdx.x >= j0.nblocks;
@@ -371,7 +371,11 @@ __global__ void __launch_bounds__(256) adamw_layer_kernel(
     if (r < R && c < N) {
       const int sl = row_slot[r];
       const int64_t idx = r * N + c;
-      if (sl >= 0) {
+      // slots absent from the step (present[sl] == 0) take no optimizer step: masters,
+      // moments and step counter unchanged (their bf16 copies are rewritten unchanged)
+      if (sl >= 0 && present != nullptr && !present[sl]) {
+        val = *reinterpret_cast<const float4*>(J.P + idx);
+      } else if (sl >= 0) {
         const float2 h = hp[sl];  // lr, wd
         const float t = (float)(steps[sl] + 1);
         const float c1 = 1.f / (1.f - powf(b1, t)), c2 = 1.f / (1.f - powf(b2, t));
@@ -427,7 +431,8 @@ __global__ void __launch_bounds__(256) adamw_layer_kernel(
   }
   __syncthreads();
   if (last) {
-    for (int sl = tid; sl < num_slots; sl += blockDim.x) steps[sl] += 1;
+    for (int sl = tid; sl < num_slots; sl += blockDim.x)
+      if (present == nullptr || present[sl]) steps[sl] += 1;
     if (tid == 0) steps[num_slots] = 0;
   }
 }
@@ -472,6 +477,27 @@ __global__ void convert_kernel(const void* src, int sdt, void* dst, int ddt, int
     if (ddt == TLORA_F64) reinterpret_cast<double*>(dst)[i] = v;
     else if (ddt == TLORA_F32) reinterpret_cast<float*>(dst)[i] = (float)v;
     else reinterpret_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn((float)v);
+  }
+}
+
+// Counter-based normal samples: element i of stream `seed` is Box-Muller of two uniforms
+// from splitmix64(seed, 2i) / (seed, 2i+1). Deterministic across devices and launch shapes.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__global__ void fill_normal_kernel(void* dst, int dtype, int64_t n, uint64_t seed, float scale) {
+  const uint64_t key = splitmix64(seed ^ 0x5851F42D4C957F2Dull);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = splitmix64(key + 2 * (uint64_t)i), b = splitmix64(key + 2 * (uint64_t)i + 1);
+    const double u1 = ((a >> 11) + 1) * (1.0 / 9007199254740993.0);  // (0, 1]
+    const double u2 = (b >> 11) * (1.0 / 9007199254740992.0);        // [0, 1)
+    const float v = scale * (float)(sqrt(-2.0 * log(u1)) * cospi(2.0 * u2));
+    if (dtype == TLORA_F32) reinterpret_cast<float*>(dst)[i] = v;
+    else reinterpret_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(v);
   }
 }
 
@@ -630,36 +656,6 @@ bool grad_lpt() {
   return on;
 }
 
-// Per-device scratch for the split-K partial planes and tlora_backward's dH. Gradient
-// launches (and tlora_backward) on one device are therefore serialised on one stream at a
-// time (the drivers in this repo do so). Growing reallocates (cudaFree synchronises); it
-// only happens while shapes are first seen, so a warmed-up step can be captured in a
-// CUDA graph (capture may run on a different stream than the warm-up).
-struct Workspace {
-  DevBuf<char> partial, dh, gather;
-};
-std::mutex g_ws_mu;
-std::map<int, std::unique_ptr<Workspace>> g_ws;
-
-template <class T>
-T* ws_get(int device, cudaStream_t s, int kind, size_t count) {  // kind: 0 partial, 1 dH, 2 gather
-  std::lock_guard<std::mutex> lk(g_ws_mu);
-  auto& w = g_ws[device];
-  if (!w) w = std::make_unique<Workspace>();
-  const bool dh = kind == 1;
-  DevBuf<char>& b = kind == 0 ? w->partial : kind == 1 ? w->dh : w->gather;
-  const size_t bytes = count * sizeof(T);
-  if (b.n < bytes) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    TL_CUDA(cudaStreamIsCapturing(s, &cs));
-    require(cs == cudaStreamCaptureStatusNone, TLORA_ERR_ARG,
-            "workspace must grow during CUDA-graph capture: run the step once before capturing");
-    TL_CUDA(cudaDeviceSynchronize());
-    b.alloc(bytes);
-    if (dh) TL_CUDA(cudaMemset(b.p, 0, bytes));
-  }
-  return reinterpret_cast<T*>(b.p);
-}
 }  // namespace
 
 struct tlora_plan {
@@ -685,7 +681,52 @@ struct tlora_plan {
   // LPT schedule of the combined dB+dA gradient launch for gsched_ctas CTAs (CSR)
   int gsched_ctas = 0;
   DevBuf<int32_t> gsched_off, gsched_idx;
+  // per-slot presence in this batch (1 = the slot owns >= 1 token), device copy: the
+  // optimizer mask of a step built from this plan (tlora_plan_present_mask)
+  DevBuf<int32_t> present;
+  // Scratch owned by the plan (split-K partial planes, tlora_backward's dH, the gather
+  // copies of an interleaved plain plan). Each kind is allocated once, at its maximum
+  // size for this plan, on first use (never during CUDA-graph capture) and never regrown,
+  // so distinct plans never share scratch and a returned pointer stays valid for the
+  // plan's lifetime. Calls on ONE plan are serialised on one stream (tlora.h).
+  mutable std::mutex scratch_mu;
+  mutable DevBuf<char> scratch[3];  // 0 partial planes, 1 dH, 2 gather
 };
+
+namespace {
+enum { kScratchPartial = 0, kScratchDh = 1, kScratchGather = 2 };
+
+// Bytes of each scratch kind a plan can ever need (the maximum over the launches).
+size_t scratch_bytes(const tlora_plan* plan, int kind) {
+  const auto& L = plan->P.layout;
+  const int64_t T = plan->P.T, R = L.R;
+  if (kind == kScratchDh) return (size_t)T * R * 2;
+  if (kind == kScratchGather) return (size_t)T * (L.k + R + L.d + R) * 2;
+  const tlora::PlanTables& PT = plan->interleaved ? plan->Ps : plan->P;
+  size_t n = 0;
+  if (PT.splits_db > 1) n += (size_t)PT.splits_db * R * L.k;
+  if (PT.splits_da > 1) n += (size_t)PT.splits_da * R * L.d;
+  return n * 4;
+}
+
+template <class T>
+T* plan_scratch(const tlora_plan* plan, cudaStream_t s, int kind, size_t count) {
+  std::lock_guard<std::mutex> lk(plan->scratch_mu);
+  DevBuf<char>& b = plan->scratch[kind];
+  const size_t bytes = count * sizeof(T);
+  if (b.n < bytes) {
+    const size_t full = std::max(bytes, scratch_bytes(plan, kind));
+    require(b.n == 0, TLORA_ERR_ARG, "plan scratch request exceeds its planned size");
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TL_CUDA(cudaStreamIsCapturing(s, &cs));
+    require(cs == cudaStreamCaptureStatusNone, TLORA_ERR_ARG,
+            "plan scratch is allocated on first use: run the step once before capturing");
+    b.alloc(full);
+    if (kind == kScratchDh) TL_CUDA(cudaMemset(b.p, 0, full));
+  }
+  return reinterpret_cast<T*>(b.p);
+}
+}  // namespace
 
 namespace {
 
@@ -708,6 +749,12 @@ const void* stage_input(const void* src, size_t count, int dtype, int where, Dev
 }
 
 }  // namespace
+
+// Error hook for the library's other translation units (tlora_step.cu): same
+// thread-local slot tlora_last_error() reads.
+namespace tlora {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace tlora
 
 // ==================================================================== C-ABI
 extern "C" {
@@ -793,6 +840,21 @@ int tlora_copy_to_host(void* dst_host, int dst_dtype, const void* src, int src_d
     TL_CUDA(cudaGetLastError());
     TL_CUDA(cudaMemcpyAsync(dst_host, tmp.p, count * db, cudaMemcpyDeviceToHost, s));
     TL_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int tlora_fill_normal(void* dst, int dtype, int64_t count, uint64_t seed, float scale,
+                      void* stream) {
+  return guarded([&] {
+    require(count >= 0, TLORA_ERR_ARG, "negative count");
+    if (count == 0) return;
+    require(dst != nullptr, TLORA_ERR_ARG, "dst is null");
+    require(dtype == TLORA_F32 || dtype == TLORA_BF16, TLORA_ERR_ARG, "dtype must be f32 or bf16");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int blocks = (int)std::min<int64_t>(tlora::ceil_div(count, 256), 8192);
+    fill_normal_kernel<<<blocks, 256, 0, s>>>(dst, dtype, count, seed, scale);
+    TL_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
   });
 }
 
@@ -1047,6 +1109,11 @@ int tlora_layer_set_optimizer(tlora_layer* layer, const float* lr, const float* 
 }
 
 int tlora_layer_optimizer_step(tlora_layer* layer, float grad_scale, void* stream) {
+  return tlora_layer_optimizer_step_masked(layer, nullptr, grad_scale, stream);
+}
+
+int tlora_layer_optimizer_step_masked(tlora_layer* layer, const int32_t* present, float grad_scale,
+                                      void* stream) {
   return guarded([&] {
     require(layer != nullptr, TLORA_ERR_ARG, "layer is null");
     require(layer->opt_set, TLORA_ERR_ARG, "optimizer not configured (tlora_layer_set_optimizer)");
@@ -1070,7 +1137,7 @@ int tlora_layer_optimizer_step(tlora_layer* layer, float grad_scale, void* strea
     }
     adamw_layer_kernel<<<job[0].nblocks + job[1].nblocks, 256, 0, s>>>(
         job[0], job[1], layer->row_slot.p, layer->hparams.p, layer->steps_dev.p, S,
-        layer->beta1, layer->beta2, layer->eps, grad_scale, R);
+        layer->beta1, layer->beta2, layer->eps, grad_scale, R, present);
     TL_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
   });
@@ -1175,6 +1242,13 @@ int tlora_plan_create(tlora_layer* layer, int64_t tokens, const int32_t* token_s
         TL_CUDA(cudaMemcpy(plan->gsched_idx.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice));
       }
     }
+    {
+      const int S = (int)layer->L.rank.size();
+      std::vector<int32_t> pres(S);
+      for (int s_ = 0; s_ < S; ++s_) pres[s_] = plan->P.slot_first[s_] >= 0 ? 1 : 0;
+      plan->present.alloc(S);
+      TL_CUDA(cudaMemcpy(plan->present.p, pres.data(), S * 4, cudaMemcpyHostToDevice));
+    }
     plan->cnt_db.alloc(plan->P.split_count_db.size());
     TL_CUDA(cudaMemcpy(plan->cnt_db.p, plan->P.split_count_db.data(),
                        plan->P.split_count_db.size() * 4, cudaMemcpyHostToDevice));
@@ -1259,6 +1333,13 @@ int tlora_gather_rows(const tlora_plan* plan, int32_t n, const void* const* src,
       g_launches.fetch_add(1, std::memory_order_relaxed);
       TL_CUDA(cudaGetLastError());
     }
+  });
+}
+
+int tlora_plan_present_mask(const tlora_plan* plan, const int32_t** present) {
+  return guarded([&] {
+    require(plan != nullptr && present != nullptr, TLORA_ERR_ARG, "null argument");
+    *present = plan->present.p;
   });
 }
 
@@ -1550,7 +1631,7 @@ void run_grads(tlora_layer* layer, const tlora_plan* plan, const void* H, const 
     size_t total = 0;
     for (int q = 0; q < 4; ++q)
       if (on[q / 2]) total += (size_t)T * widths[q];
-    __nv_bfloat16* gbuf = ws_get<__nv_bfloat16>(layer->device, s, 2, total);
+    __nv_bfloat16* gbuf = plan_scratch<__nv_bfloat16>(plan, s, kScratchGather, total);
     GatherJob jobs[4] = {};
     size_t o = 0;
     for (int q = 0; q < 4; ++q) {
@@ -1570,7 +1651,7 @@ void run_grads(tlora_layer* layer, const tlora_plan* plan, const void* H, const 
   size_t need = 0;
   for (int j = 0; j < 2; ++j)
     if (on[j] && nsp[j] > 1) need += (size_t)nsp[j] * R * Ns[j];
-  float* ws = need ? ws_get<float>(layer->device, s, 0, need) : nullptr;
+  float* ws = need ? plan_scratch<float>(plan, s, kScratchPartial, need) : nullptr;
   size_t off = 0;
   double flops = 0.0;
   for (int j = 0; j < 2; ++j) {
@@ -1802,7 +1883,7 @@ int tlora_backward(tlora_layer* layer, const tlora_plan* plan, const void* dY, c
     DeviceGuard g(layer->device);
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     __nv_bfloat16* dH =
-        ws_get<__nv_bfloat16>(layer->device, s, 1, (size_t)plan->P.T * layer->L.R);
+        plan_scratch<__nv_bfloat16>(plan, s, kScratchDh, (size_t)plan->P.T * layer->L.R);
     run_dh(layer, plan, dY, dH, s);
     if (dX) run_dx(layer, plan, dY, dH, dX, 0.f, s);
     run_grads(layer, plan, H_stash, dY, dH, X, true, true, beta, s);
@@ -1852,6 +1933,30 @@ int tlora_backward_dx_dh(tlora_layer* layer, const tlora_plan* plan, const void*
     if (zero_next)
       TL_CUDA(cudaMemsetAsync(dH_next, 0, (size_t)next_plan->P.T * next->L.R * 2, s));
     const Gemm2Secondary sec = make_lowrank2(next, next_plan, 1, dY_next, dH_next);
+    run_dx(layer, plan, dY, dH, dX, beta, s, &sec);
+  });
+}
+
+int tlora_backward_dx_shrink(tlora_layer* layer, const tlora_plan* plan, const void* dY,
+                             const void* dH, void* dX, float beta, tlora_layer* next,
+                             const tlora_plan* next_plan, const void* X_next, void* H_next,
+                             int zero_next, void* stream) {
+  return guarded([&] {
+    check_bound(layer, plan);
+    check_bound(next, next_plan);
+    check_align(dY, "dY");
+    check_align(dH, "dH");
+    check_align(dX, "dX");
+    check_align(X_next, "X_next");
+    check_align(H_next, "H_next");
+    require(next->device == layer->device, TLORA_ERR_ARG, "layers on different devices");
+    require(H_next != dH && H_next != dX && H_next != dY, TLORA_ERR_ARG,
+            "H_next must not alias this layer's operands");
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (zero_next)
+      TL_CUDA(cudaMemsetAsync(H_next, 0, (size_t)next_plan->P.T * next->L.R * 2, s));
+    const Gemm2Secondary sec = make_lowrank2(next, next_plan, 0, X_next, H_next);
     run_dx(layer, plan, dY, dH, dX, beta, s, &sec);
   });
 }

@@ -83,6 +83,27 @@ struct tlora_comm {
   int device = 0;
   int32_t world = 1, rank = 0, tp = 1, dp = 1;
   ncclComm_t comm[3] = {nullptr, nullptr, nullptr};  // TLORA_GROUP_WORLD / _TP / _DP
+  // Destroys every communicator that exists (a failed split in create must not leak the
+  // world comm). Returns the first NCCL error; keeps destroying after one fails.
+  ncclResult_t release() {
+    ncclResult_t first = ncclSuccess;
+    for (int i = 2; i >= 0; --i) {
+      if (!comm[i]) continue;
+      const ncclResult_t r = nccl().destroy(comm[i]);
+      comm[i] = nullptr;
+      if (r != ncclSuccess && first == ncclSuccess) first = r;
+    }
+    return first;
+  }
+  ~tlora_comm() {
+    if (comm[0] || comm[1] || comm[2]) {
+      int prev = -1;
+      cudaGetDevice(&prev);
+      if (prev != device) cudaSetDevice(device);
+      release();
+      if (prev >= 0 && prev != device) cudaSetDevice(prev);
+    }
+  }
 };
 
 extern "C" {
@@ -132,8 +153,7 @@ int tlora_comm_destroy(tlora_comm* comm) {
     if (!comm) return;
     std::unique_ptr<tlora_comm> c(comm);
     DeviceGuard g(c->device);
-    for (int i = 2; i >= 0; --i)
-      if (c->comm[i]) TL_NCCL(nccl().destroy(c->comm[i]));
+    TL_NCCL(c->release());  // all three are destroyed even if one fails; first error wins
   });
 }
 

@@ -92,6 +92,12 @@ class Plan:
         widths = (C.c_int64 * n)(*[p[0].shape[1] for p in pairs])
         call("tlora_gather_rows", self._h, n, srcs, dsts, widths, _stream_ptr(stream))
 
+    def present_mask(self) -> int:
+        """Device pointer to the plan's per-slot presence flags (int32, num_slots)."""
+        p = C.c_void_p()
+        call("tlora_plan_present_mask", self._h, C.byref(p))
+        return p.value
+
     def info(self) -> PlanInfo:
         i = capi.PlanInfoC()
         call("tlora_plan_get_info", self._h, C.byref(i))
@@ -193,8 +199,14 @@ class FusedLoRALayer:
         call("tlora_layer_set_optimizer", self._h, (C.c_float * S)(*lr), (C.c_float * S)(*wd),
              float(beta1), float(beta2), float(eps))
 
-    def optimizer_step(self, grad_scale=1.0, stream=None):
-        call("tlora_layer_optimizer_step", self._h, C.c_float(grad_scale), _stream_ptr(stream))
+    def optimizer_step(self, grad_scale=1.0, stream=None, plan: "Plan | None" = None):
+        """plan: only the slots with tokens in that plan's batch take a step (jobs absent
+        from the step keep masters, moments and step count); None = every slot."""
+        if plan is None:
+            call("tlora_layer_optimizer_step", self._h, C.c_float(grad_scale), _stream_ptr(stream))
+            return
+        call("tlora_layer_optimizer_step_masked", self._h, C.c_void_p(plan.present_mask()),
+             C.c_float(grad_scale), _stream_ptr(stream))
 
     def read_adapter(self, slot: int, stream=None):
         r = self.ranks[slot]

@@ -28,8 +28,12 @@ class LayerSetStep:
     """
 
     def __init__(self, wl: Workload, device: int = 0, seed: int | None = None,
-                 shuffle: bool = False, y_dtype=torch.bfloat16, chain: bool = True):
+                 shuffle: bool = False, y_dtype=torch.bfloat16, chain: bool = True,
+                 keep_weights: bool = False):
         self.wl = wl
+        # keep_weights: retain the bf16 W / A_j / B_j each layer was loaded with (the
+        # full-size parity tests restate the step from them; the bench does not keep them)
+        self.weights = {} if keep_weights else None
         # chain: each projection's shrink (forward) / dH (backward) rides as extra tiles in
         # the previous projection's fused GEMM launch (tlora_forward_gemm_shrink /
         # tlora_backward_dx_dh) instead of its own launch; bit-identical either way.
@@ -54,12 +58,17 @@ class LayerSetStep:
             d, k = dims[name]
             lay = FusedLoRALayer(d, k, wl.ranks, device=device)
             W = torch.randn(d, k, generator=g, device=dev, dtype=torch.float32).mul_(d ** -0.5)
-            lay.set_base(W.bfloat16())
-            del W
+            W = W.bfloat16()
+            lay.set_base(W)
+            ab = []
             for s, j in enumerate(wl.jobs):
                 A = torch.randn(d, j.rank, generator=g, device=dev).mul_(d ** -0.5).bfloat16()
                 B = torch.randn(j.rank, k, generator=g, device=dev).mul_(j.rank ** -0.5).bfloat16()
                 lay.set_adapter(s, A, B)
+                ab.append((A, B))
+            if self.weights is not None:
+                self.weights[(L, name)] = (W, ab)
+            del W, ab
             self.layers[(L, name)] = lay
             if name not in self.plans:
                 self.plans[name] = lay.plan(self.slots, gathered=self.gathered)

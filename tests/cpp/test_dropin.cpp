@@ -319,6 +319,36 @@ void gpu_backward_bilinearity() {
   }
 }
 
+void gpu_unreferenced_and_rank0_adapters() {
+  // Only referenced adapters are validated (fused_lora.hpp:70-77) and used (:104): an
+  // unreferenced adapter of a wrong shape must be ignored, and a referenced rank-0 adapter
+  // (A d x 0, B 0 x k) contributes exactly nothing, as in the reference.
+  std::mt19937_64 rng(99);
+  auto inst = random_instance(rng, 2);
+  const Index d = inst.base_weight.rows(), k = inst.base_weight.cols();
+  auto ad = inst.adapters;
+  ad.push_back({"zz_unused", Matrix(d + 5, 3), Matrix(7, k + 2)});  // bad shape, unreferenced
+  auto [y1, c1] = fused_forward(inst.batch, inst.base_weight, inst.adapters);
+  auto [y2, c2] = fused_forward(inst.batch, inst.base_weight, ad);
+  CHECK((y1 - y2).cwiseAbs().maxCoeff() == 0.0);
+  auto g = fused_backward(inst.batch, inst.base_weight, ad,
+                          Matrix::Zero(inst.batch.rows.rows(), k) + y1);
+  CHECK(g.dA.at("zz_unused").rows() == d + 5 && g.dA.at("zz_unused").cwiseAbs().maxCoeff() == 0.0);
+  CHECK(g.dB.at("zz_unused").cols() == k + 2);
+
+  TokenBatch batch;
+  batch.rows = Matrix(3, 2);
+  batch.rows << 1, 2, 3, 4, 5, 6;
+  batch.segment_map = {"r0", "r0", "r0"};
+  Matrix W(2, 2);
+  W << 1, 0, 0, 1;
+  auto [y, cost] = fused_forward(batch, W, {{"r0", Matrix(2, 0), Matrix(0, 2)}});
+  CHECK((y - batch.rows * W).cwiseAbs().maxCoeff() == 0.0);
+  auto g0 = fused_backward(batch, W, {{"r0", Matrix(2, 0), Matrix(0, 2)}}, Matrix::Zero(3, 2) + y);
+  CHECK(g0.dA.at("r0").rows() == 2 && g0.dA.at("r0").cols() == 0);
+  CHECK(g0.dB.at("r0").rows() == 0 && g0.dB.at("r0").cols() == 2);
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -335,6 +365,8 @@ int main(int argc, char** argv) {
     cases.push_back({"fused_forward matches the materialized oracle", gpu_matches_oracle});
     cases.push_back({"linearity and single-segment KAT", gpu_linear_and_kat});
     cases.push_back({"fused_backward pinned by bilinearity", gpu_backward_bilinearity});
+    cases.push_back({"unreferenced / rank-0 adapters as in the reference",
+                     gpu_unreferenced_and_rank0_adapters});
   }
   for (auto& [name, fn] : cases) {
     const int before = g_fail;

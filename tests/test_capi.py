@@ -43,7 +43,7 @@ def test_library_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(capi.SIGNATURES), set(syms) ^ set(capi.SIGNATURES)
-    assert lib.tlora_abi_version() == 4
+    assert lib.tlora_abi_version() == 5
 
 
 def test_op_cost_via_abi_matches_reference_golden():

@@ -1,0 +1,199 @@
+"""The C++ step executor (tlora_step_*) on the GPU: bitwise agreement with the Python
+per-launch driver it replaces, the AIMD controller driven by its own measured step times
+(nano_pipeline.hpp:99-112, clamped as sim_engine.hpp:314), the rank-aware token layout
+as uploaded, the masked optimizer for jobs absent from a step, and the pure-C++ host
+(tests/cpp/step_main) matching the Python-driven executor bit for bit."""
+import math
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT / "oracle"))
+import oracle as O  # noqa: E402
+
+from paper_2602_07263_b200.runner import LayerSetStep  # noqa: E402
+from paper_2602_07263_b200.step import TrainingStep, sample_weights  # noqa: E402
+from paper_2602_07263_b200.workload import Job, Workload, config  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+MINI = Workload("mini", [("q", 512, 768), ("k", 512, 256), ("o", 768, 512), ("down", 640, 768)],
+                [Job("a", 8, 2, 256), Job("b", 200, 3, 320), Job("c", 16, 1, 192),
+                 Job("d", 64, 2, 128)], layers=2, seed=77)
+
+
+def _state(st):
+    torch.cuda.synchronize()
+    return {
+        "Y": {n: t.clone() for n, t in st.Y.items()},
+        "dX": {n: t.clone() for n, t in st.dX.items()},
+        "H": {k: st.H[k].clone() for k in st.keys},
+        "g": {k: [t.clone() for s in range(len(st.layers[k].ranks))
+                  for t in st.layers[k].read_grad(s)] for k in st.keys},
+        "P": {k: [t.clone() for s in range(len(st.layers[k].ranks))
+                  for t in st.layers[k].read_adapter(s)] for k in st.keys},
+    }
+
+
+def _equal(a, b):
+    for part in ("Y", "dX", "H"):
+        for key in a[part]:
+            assert torch.equal(a[part][key], b[part][key]), (part, key)
+    for part in ("g", "P"):
+        for key in a[part]:
+            assert all(torch.equal(x, y) for x, y in zip(a[part][key], b[part][key])), (part, key)
+
+
+@pytest.mark.parametrize("wl", [MINI, config("C2")], ids=["mini", "C2"])
+def test_executor_matches_python_driver_bitwise(wl):
+    """N = 1: the executor's chained schedule is the Python driver's chained + side-stream
+    schedule (same launches, same tiles): every output, stash, gradient and updated adapter
+    is bitwise equal, for the eager first step and for graph replays."""
+    py = LayerSetStep(wl, device=0, seed=wl.seed, chain=True)
+    py.enable_optimizer()
+    py.enable_side_grads()
+    ex = TrainingStep(wl, device=0, nano_fixed=1, graphs=True)
+    ex.init_random(wl.seed)
+    ex.enable_optimizer()
+    for i in range(3):
+        py.step()
+        s = ex.run()
+        assert s.replayed_graph == (i > 0) and s.nano_used == 1
+        _equal(_state(py), _state(ex))
+
+
+def test_executor_aimd_follows_reference_rule():
+    """N comes from the reference controller fed with the executor's own CUDA-event step
+    times: restating aimd_step (oracle) on the reported times reproduces every N, clamped to
+    the combined batch; the first observation only seeds t_prev."""
+    wl = MINI
+    ex = TrainingStep(wl, device=0, nano_fixed=0, nano_init=4, graphs=True)
+    ex.init_random(wl.seed)
+    ex.enable_optimizer()
+    total = sum(j.batch for j in wl.jobs)
+    n, t_prev = 4, None
+    for _ in range(10):
+        assert ex.next_n() == n
+        s = ex.run()
+        assert s.nano_used == min(n, total)
+        n, t_prev = O.aimd_step(n, t_prev, s.ms / 1e3)
+        n = min(n, total)
+        assert s.next_nano == n
+    assert len({u for u, _ in ex.trajectory}) >= 2  # the controller moved N
+
+
+def test_executor_layout_is_the_rank_aware_map():
+    """The layout the executor plans with == the oracle's nano map (bit-exact counts) laid
+    out nano-major, job-contiguous inside a nano-batch; sample rows tile [0, T)."""
+    wl = config("C2")
+    ex = TrainingStep(wl, device=0, nano_fixed=1, graphs=False)
+    batch, weight = [j.batch for j in wl.jobs], sample_weights(wl)
+    for n in (1, 2, 3, 5, 17, 40):
+        k, t0, ns, sample_row = ex.layout(n)
+        ko, per, sample_nano, nso = O.nano_assign(batch, weight, n)
+        assert k == ko and np.array_equal(ns, nso)
+        sizes = np.array([ns[i] @ np.array([j.seq_len for j in wl.jobs]) for i in range(k)])
+        assert np.array_equal(np.diff(t0), sizes) and t0[-1] == wl.tokens
+        seqs = np.repeat([j.seq_len for j in wl.jobs], batch)
+        order = np.argsort(sample_row)
+        assert np.array_equal(np.cumsum(seqs[order])[:-1], sample_row[order][1:])
+        for q in range(len(sample_row)):  # sample q lies inside its nano-batch's row range
+            i = sample_nano[q]
+            assert t0[i] <= sample_row[q] < t0[i + 1]
+
+
+def test_masked_optimizer_skips_absent_jobs():
+    """A job with no tokens in the step takes no AdamW step (masters and step counter
+    unchanged); when it reappears its first update uses bias correction t = 1."""
+    from paper_2602_07263_b200.layer import FusedLoRALayer
+    rs = np.random.RandomState(3)
+    d, k, ranks = 128, 136, [8, 24, 16]
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    lay = FusedLoRALayer(d, k, ranks)
+    lay.set_base(t(rs.randn(d, k) / np.sqrt(d)).bfloat16())
+    for s, r in enumerate(ranks):
+        lay.set_adapter(s, t(rs.randn(d, r) / np.sqrt(d)).float(), t(rs.randn(r, k) / np.sqrt(r)).float())
+    lr, wd = [1e-2, 2e-2, 5e-3], [0.0, 0.1, 0.01]
+    lay.set_optimizer(lr, wd, 0.9, 0.99, 1e-8)
+    X = t(rs.randn(400, d)).bfloat16()
+    dY = t(rs.randn(400, k)).bfloat16()
+    slots_a = np.repeat([0, 2], [250, 150]).astype(np.int32)    # job 1 absent
+    slots_b = np.repeat([0, 1, 2], [100, 200, 100]).astype(np.int32)
+    before = [[x.double() for x in lay.read_adapter(s)] for s in range(3)]
+    plan = lay.plan(slots_a)
+    Y, H = lay.forward(plan, X)
+    lay.backward(plan, dY, X, H)
+    lay.optimizer_step(plan=plan)
+    torch.cuda.synchronize()
+    mid = [[x.double() for x in lay.read_adapter(s)] for s in range(3)]
+    assert all(torch.equal(a, b) for a, b in zip(before[1], mid[1]))       # untouched
+    assert not torch.equal(before[0][0], mid[0][0])                         # stepped
+    plan_b = lay.plan(slots_b)
+    Y, H = lay.forward(plan_b, X)
+    lay.backward(plan_b, dY, X, H)
+    g1 = [x.double() for x in lay.read_grad(1)]
+    lay.optimizer_step(plan=plan_b)
+    torch.cuda.synchronize()
+    after = [x.double() for x in lay.read_adapter(1)]
+    for p0, g, p1 in zip(mid[1], g1, after):  # first step for job 1: t = 1, zero moments
+        m, v = 0.1 * g, 0.01 * g * g
+        ref = p0 - lr[1] * ((m / 0.1) / (torch.sqrt(v / 0.01) + 1e-8) + wd[1] * p0)
+        assert ((p1 - ref).abs().max() / p0.abs().max()).item() < 1e-5
+
+
+def test_cpp_host_step_matches_python_driven_executor(tmp_path):
+    """tests/cpp/step_main drives the executor purely from C++ (weights and inputs from
+    tlora_fill_normal, no Python, no torch) and dumps Y / dX / gradients / adapters after
+    two steps at N = 2; the same executor driven from Python with the same fills gives the
+    same bytes."""
+    binp = ROOT / "tests" / "cpp" / "_build" / "step_main"
+    if not binp.exists():
+        subprocess.run(["make", "-C", str(ROOT), "tests/cpp/_build/step_main"], check=True)
+    out = tmp_path / "cpp.bin"
+    p = subprocess.run([str(binp), "dump", str(out)], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout + p.stderr
+    cpp = np.fromfile(out, dtype=np.uint8)
+    from paper_2602_07263_b200 import capi
+    import ctypes as C
+    wl = Workload("cpp-mini", [("q", 512, 768), ("k", 512, 256), ("o", 768, 512)],
+                  [Job("a", 8, 2, 256), Job("b", 200, 3, 320), Job("c", 16, 1, 192)],
+                  layers=2, seed=5)
+    ex = TrainingStep(wl, device=0, nano_fixed=2, graphs=True)
+    fill = capi.lib().tlora_fill_normal
+    seed = 1000
+    for key in ex.keys:  # the C++ program's fill order (tests/cpp/step_main.cpp)
+        lay = ex.layers[key]
+        W = torch.empty(lay.d, lay.k, dtype=torch.bfloat16, device="cuda")
+        fill(C.c_void_p(W.data_ptr()), capi.BF16, W.numel(), seed, C.c_float(1.0 / math.sqrt(lay.d)), None)
+        seed += 1
+        lay.set_base(W)
+        for s, r in enumerate(lay.ranks):
+            A = torch.empty(lay.d, r, dtype=torch.float32, device="cuda")
+            B = torch.empty(r, lay.k, dtype=torch.float32, device="cuda")
+            fill(C.c_void_p(A.data_ptr()), capi.F32, A.numel(), seed, C.c_float(1.0 / math.sqrt(lay.d)), None)
+            fill(C.c_void_p(B.data_ptr()), capi.F32, B.numel(), seed + 1, C.c_float(1.0 / math.sqrt(r)), None)
+            seed += 2
+            lay.set_adapter(s, A, B)
+    for g in ex.groups:
+        x = ex.X[0][g]
+        fill(C.c_void_p(x.data_ptr()), capi.BF16, x.numel(), seed, C.c_float(1.0), None)
+        seed += 1
+    for n in ex.names:
+        y = ex.dY[0][n]
+        fill(C.c_void_p(y.data_ptr()), capi.BF16, y.numel(), seed, C.c_float(1.0), None)
+        seed += 1
+    ex.enable_optimizer(1e-3, 0.01)
+    ex.run()
+    ex.run()
+    st = _state(ex)
+    parts = [st["Y"][n] for n in ex.names] + [st["dX"][n] for n in ex.names]
+    for key in ex.keys:
+        parts += st["g"][key] + st["P"][key]
+    py = np.concatenate([t.contiguous().view(torch.uint8).cpu().numpy().ravel() for t in parts])
+    assert py.size == cpp.size and np.array_equal(py, cpp)
