@@ -13,9 +13,15 @@ ORACLE   := oracle/liboracle.so
 
 CPPTEST  := tests/cpp/_build/test_dropin
 STEPMAIN := tests/cpp/_build/step_main
+COSTMAIN := tests/cpp/_build/cost_main
 CUDA_HOME ?= /usr/local/cuda
 
-all: $(LIB) $(ORACLE) $(CPPTEST) $(STEPMAIN)
+all: $(LIB) $(ORACLE) $(CPPTEST) $(STEPMAIN) $(COSTMAIN)
+
+# measured B200 cost model (include/lora_fleet/hardware.hpp) from C++; host-only
+$(COSTMAIN): tests/cpp/cost_main.cpp include/lora_fleet/hardware.hpp
+	mkdir -p tests/cpp/_build
+	$(CXX) -std=c++20 -O2 -Iinclude -o $@ tests/cpp/cost_main.cpp
 
 # pure C++ host of the training step executor (LayerSetTrainer over the C-ABI)
 $(STEPMAIN): tests/cpp/step_main.cpp include/lora_fleet/*.hpp include/tlora.h $(LIB)
@@ -53,6 +59,6 @@ ref:
 	$(MAKE) -C oracle ref
 
 clean:
-	rm -f $(LIB) $(ORACLE) $(CPPTEST) $(STEPMAIN) $(CAPI_O) $(STEP_O) build_ptxas.log
+	rm -f $(LIB) $(ORACLE) $(CPPTEST) $(STEPMAIN) $(COSTMAIN) $(CAPI_O) $(STEP_O) build_ptxas.log
 
 .PHONY: all clean ref

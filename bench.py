@@ -294,6 +294,24 @@ def run_executor(args, rank, world, local_rank):
     tokens = wl.tokens * world
     value = tokens / (ms_per_step / 1e3)
 
+    # ---- the AIMD-driven executor on the same workload (after the timed region): N chosen
+    # every step by the reference's controller from the measured step time
+    aimd = None
+    if args.aimd_steps > 0 and args.nano_batches > 0:
+        st.set_controller(0, args.nano_init)
+        at = []
+        for _ in range(args.aimd_steps):
+            s_ = st.run(stream=stream)
+            at.append([s_.nano_used, round(s_.ms, 3)])
+        tot = sum(m for _, m in at)
+        aimd = {"steps": len(at), "trajectory_n_ms": at,
+                "tokens_per_s": round(wl.tokens * len(at) / (tot / 1e3), 1),
+                "note": "AIMD every step from N=%d (nano_pipeline.hpp:99-112, clamped as "
+                        "sim_engine.hpp:314); first visit of each N is eager, then its graph "
+                        "replays" % args.nano_init}
+        st.set_controller(args.nano_batches)
+        st.run(stream=stream)
+
     # ---- e2e: host pinned inputs -> H2D (copy stream, double-buffered input sets) -> the
     # executor's step on the set -> D2H of every adapter gradient; step i+1's H2D overlaps
     # step i, step i+1 starts after step i's gradients are on the host.
@@ -396,6 +414,7 @@ def run_executor(args, rank, world, local_rank):
                         "overlapped with step i)"},
         "gpu_launches": n_launch,
         "roofline": roofline,
+        "aimd": aimd,
         "cpu_baseline": cpu,
         "cpu_baseline_oracle_f32": cpu_f32,
         "clocks": clk,
@@ -1030,7 +1049,8 @@ def main():
                          "reduce-scatter is fused into the GEMM epilogue (bulk copies into "
                          "the owner's receive slot over NVLink); the rest use NCCL on the "
                          "comm stream. auto = o,down when TP > 1; none = NCCL for all")
-    ap.add_argument("--aimd-steps", type=int, default=8, help="AIMD exploration steps (TP mode)")
+    ap.add_argument("--aimd-steps", type=int, default=12,
+                    help="AIMD steps: TP mode exploration; executor: the untimed AIMD phase")
     ap.add_argument("--dp-reserve-sms", type=int, default=0,
                     help="DP (N>1): SMs kept free of the persistent grids for the concurrent "
                          "NCCL all-reduce (NCCL gets half as many channels); 0 = defaults "

@@ -380,8 +380,10 @@ int tlora_nano_assign(int32_t num_slots, const int32_t* batch, const int64_t* we
 typedef struct tlora_step tlora_step;
 enum tlora_step_flags {
   TLORA_STEP_SIDE_GRADS = 1, /* dB+dA (and AdamW) of each key on a side stream             */
-  TLORA_STEP_GRAPH = 2       /* capture each (N, input set) step into a CUDA graph after its
+  TLORA_STEP_GRAPH = 2,      /* capture each (N, input set) step into a CUDA graph after its
                                 first eager run and replay it (single replica only)        */
+  TLORA_STEP_EARLY_GRADS = 4 /* a key's dB+dA waits only for the launch that produced its dH,
+                                so it may overlap the key's own dX launch                   */
 };
 enum tlora_run_flags { TLORA_RUN_EAGER = 1 /* launch eagerly even if a graph exists */ };
 typedef struct tlora_step_desc {
@@ -431,6 +433,11 @@ int tlora_step_buffer(tlora_step* step, int32_t kind, int32_t index, int32_t set
  * each sample (samples job-major). Any output may be NULL. */
 int tlora_step_layout(tlora_step* step, int32_t n, int32_t* n_out, int64_t* nano_t0,
                       int32_t* nano_slot, int64_t* sample_row);
+/* Switch the nano-batch controller: nano_fixed > 0 pins N; 0 = AIMD from nano_init (0 = 4)
+ * with a fresh AimdState (alpha 0 = 4, beta 0 = 0.5). Layouts, plans and graphs of N values
+ * seen before are kept. */
+int tlora_step_set_controller(tlora_step* step, int32_t nano_fixed, int32_t nano_init,
+                              int32_t aimd_alpha, double aimd_beta, double aimd_tau_rel);
 /* N the next tlora_step_run will use (fill the inputs in that layout). */
 int tlora_step_next_n(const tlora_step* step, int32_t* n);
 /* One training step on input set `set`, enqueued on `stream` and waited for (the step time
@@ -450,6 +457,8 @@ typedef struct tlora_step_op {
   int32_t beta;                         /* GRADS: 1 = accumulate onto earlier nano-batches */
   int32_t wait0, wait1;                 /* ops (on other streams) waited for, -1         */
 } tlora_step_op;
+/* side_grads: 0 = gradients on the main stream, 1 = side stream, 2 = side stream with
+ * TLORA_STEP_EARLY_GRADS. */
 int tlora_step_schedule_host(int32_t keys, int32_t nano, int32_t ring, int32_t side_grads,
                              int32_t data_parallel, tlora_step_op* out, int32_t cap,
                              int32_t* count);

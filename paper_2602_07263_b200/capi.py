@@ -66,7 +66,7 @@ class StepOpC(C.Structure):
                                          "wait1")]
 
 
-STEP_SIDE_GRADS, STEP_GRAPH = 1, 2
+STEP_SIDE_GRADS, STEP_GRAPH, STEP_EARLY_GRADS = 1, 2, 4
 RUN_EAGER = 1
 BUF_X, BUF_DY, BUF_Y, BUF_DX, BUF_H = range(5)
 OP_SHRINK, OP_FWD, OP_DH, OP_DX, OP_GRADS, OP_ALLREDUCE, OP_ADAMW = range(7)
@@ -195,6 +195,8 @@ SIGNATURES = {
     "tlora_step_layout": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_void_p,
                                     C.c_void_p, C.c_void_p]),
     "tlora_step_next_n": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    "tlora_step_set_controller": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                            C.c_double, C.c_double]),
     "tlora_step_run": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                  C.POINTER(StepStatsC)]),
     "tlora_step_schedule_host": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,

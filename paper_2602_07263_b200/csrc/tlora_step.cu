@@ -100,7 +100,10 @@ struct Op {
   int32_t wait0, wait1;                    // op indices waited on (other streams), -1
 };
 
-std::vector<Op> build_schedule(int32_t keys, int32_t n, int32_t ring, bool side, bool dp) {
+// early: a GRADS op waits only for the launch that produced its dH (it may then overlap the
+// key's own dX launch) instead of for the key's dX launch.
+std::vector<Op> build_schedule(int32_t keys, int32_t n, int32_t ring, bool side, bool dp,
+                               bool early = false) {
   need(keys >= 1 && n >= 1 && ring >= 2, TLORA_ERR_ARG, "schedule: bad sizes");
   std::vector<Op> ops;
   std::vector<int32_t> grads_op;  // global backward index -> GRADS op index
@@ -113,7 +116,7 @@ std::vector<Op> build_schedule(int32_t keys, int32_t n, int32_t ring, bool side,
     const int32_t prev = g - ring;
     return prev >= 0 ? grads_op[prev] : -1;
   };
-  int32_t g = 0;
+  int32_t g = 0, dh_producer = -1;
   for (int32_t i = 0; i < n; ++i) {
     if (i == 0)
       push({TLORA_OP_SHRINK, TLORA_STREAM_MAIN, 0, 0, -1, -1, -1, -1, -1, 0, -1, -1});
@@ -130,7 +133,7 @@ std::vector<Op> build_schedule(int32_t keys, int32_t n, int32_t ring, bool side,
         o.sec_slot = g % ring;
         o.wait0 = ring_wait(g);
       }
-      push(o);
+      dh_producer = push(o);
     }
     for (int32_t j = 0; j < keys; ++j) {
       const int32_t key = keys - 1 - j, gi = g + j;
@@ -147,8 +150,10 @@ std::vector<Op> build_schedule(int32_t keys, int32_t n, int32_t ring, bool side,
         o.sec_nano = i + 1;
       }
       const int32_t dx = push(o);
+      const int32_t after = early ? dh_producer : dx;
+      dh_producer = dx;
       const int32_t gr = push({TLORA_OP_GRADS, gstream, key, i, gi % ring, -1, -1, -1, -1,
-                               i > 0 ? 1 : 0, gstream == TLORA_STREAM_MAIN ? -1 : dx, -1});
+                               i > 0 ? 1 : 0, gstream == TLORA_STREAM_MAIN ? -1 : after, -1});
       grads_op.push_back(gr);
       if (i + 1 == n) {
         if (dp) {
@@ -304,7 +309,8 @@ Layout& tlora_step::layout(int32_t n) {
       chk(tlora_plan_create(lay(key(0, p)), (int64_t)slots.size(), slots.data(),
                             &lo->plans[(size_t)i][(size_t)p]));
   }
-  lo->ops = build_schedule(L * P, m.n, ring, (desc.flags & TLORA_STEP_SIDE_GRADS) != 0, comm != nullptr);
+  lo->ops = build_schedule(L * P, m.n, ring, (desc.flags & TLORA_STEP_SIDE_GRADS) != 0,
+                           comm != nullptr, (desc.flags & TLORA_STEP_EARLY_GRADS) != 0);
   lo->needs_event.assign(lo->ops.size(), 0);
   for (const auto& o : lo->ops)
     for (int32_t w : {o.wait0, o.wait1})
@@ -406,7 +412,8 @@ int tlora_step_schedule_host(int32_t keys, int32_t nano, int32_t ring, int32_t s
                              int32_t data_parallel, tlora_step_op* out, int32_t cap,
                              int32_t* count) {
   return step_guard([&] {
-    const auto ops = build_schedule(keys, nano, ring, side_grads != 0, data_parallel != 0);
+    const auto ops = build_schedule(keys, nano, ring, side_grads != 0, data_parallel != 0,
+                                    side_grads == 2);
     if (count) *count = (int32_t)ops.size();
     if (out)
       for (size_t i = 0; i < ops.size() && (int32_t)i < cap; ++i) {
@@ -618,6 +625,26 @@ int tlora_step_layout(tlora_step* step, int32_t n, int32_t* n_out, int64_t* nano
     if (nano_t0) std::memcpy(nano_t0, lo.t0.data(), lo.t0.size() * 8);
     if (nano_slot) std::memcpy(nano_slot, lo.map.nano_slot.data(), lo.map.nano_slot.size() * 4);
     if (sample_row) std::memcpy(sample_row, lo.sample_row.data(), lo.sample_row.size() * 8);
+  });
+}
+
+int tlora_step_set_controller(tlora_step* step, int32_t nano_fixed, int32_t nano_init,
+                              int32_t aimd_alpha, double aimd_beta, double aimd_tau_rel) {
+  return step_guard([&] {
+    need(step != nullptr, TLORA_ERR_ARG, "step is null");
+    need(nano_fixed >= 0 && nano_init >= 0, TLORA_ERR_ARG, "negative nano count");
+    const int32_t alpha = aimd_alpha ? aimd_alpha : 4;
+    const double beta = aimd_beta != 0.0 ? aimd_beta : 0.5;
+    if (alpha < 1 || beta <= 0.0 || beta >= 1.0 || aimd_tau_rel < 0.0)
+      throw std::invalid_argument("AimdState: invalid controller parameters");
+    step->desc.nano_fixed = nano_fixed;
+    step->desc.nano_init = nano_init;
+    step->desc.aimd_alpha = alpha;
+    step->desc.aimd_beta = beta;
+    step->desc.aimd_tau_rel = aimd_tau_rel;
+    step->aimd_n = std::min(std::max(1, nano_init > 0 ? nano_init : 4), step->total_samples);
+    step->has_prev = 0;  // the first observation seeds t_prev again (nano_pipeline.hpp:99-112)
+    step->t_prev = 0.0;
   });
 }
 

@@ -106,7 +106,7 @@ class TrainingStep:
     def __init__(self, wl: Workload, device: int = 0, nano_fixed: int = 1, nano_init: int = 4,
                  side_grads: bool = True, graphs: bool = True, dh_ring: int = 8,
                  input_sets: int = 1, comm=None, y_dtype=torch.bfloat16, aimd_alpha: int = 4,
-                 aimd_beta: float = 0.5, aimd_tau_rel: float = 0.0):
+                 aimd_beta: float = 0.5, aimd_tau_rel: float = 0.0, early_grads: bool | None = None):
         self.wl, self.device = wl, int(device)
         self.dev = torch.device("cuda", self.device)
         self.names = [p[0] for p in wl.projections]
@@ -125,7 +125,11 @@ class TrainingStep:
             batch=(C.c_int32 * S)(*[j.batch for j in wl.jobs]),
             seq=(C.c_int32 * S)(*[j.seq_len for j in wl.jobs]))
         a = self._arrs
-        flags = (capi.STEP_SIDE_GRADS if side_grads else 0) | (capi.STEP_GRAPH if graphs else 0)
+        if early_grads is None:  # A/B knob
+            import os
+            early_grads = os.environ.get("TLORA_EARLY_GRADS", "0") == "1"
+        flags = ((capi.STEP_SIDE_GRADS if side_grads else 0) | (capi.STEP_GRAPH if graphs else 0)
+                 | (capi.STEP_EARLY_GRADS if early_grads and side_grads else 0))
         desc = capi.StepDescC(self.device, wl.layers, P, a["d"], a["k"], a["inp"], S, a["ranks"],
                               a["batch"], a["seq"], capi.BF16 if y_dtype == torch.bfloat16 else capi.F32,
                               flags, dh_ring, input_sets, nano_init, nano_fixed, aimd_alpha,
@@ -214,6 +218,12 @@ class TrainingStep:
         self.trajectory.append((s.nano_used, s.ms))
         return s
 
+    def set_controller(self, nano_fixed: int = 0, nano_init: int = 4, alpha: int = 4,
+                       beta: float = 0.5, tau_rel: float = 0.0):
+        """nano_fixed > 0 pins N; 0 = AIMD from nano_init with a fresh controller state."""
+        call("tlora_step_set_controller", self._h, int(nano_fixed), int(nano_init), int(alpha),
+             float(beta), float(tau_rel))
+
     def next_n(self) -> int:
         n = C.c_int32()
         call("tlora_step_next_n", self._h, C.byref(n))
@@ -244,7 +254,7 @@ class TrainingStep:
             pass
 
 
-def schedule_host(keys: int, nano: int, ring: int = 8, side_grads: bool = True,
+def schedule_host(keys: int, nano: int, ring: int = 8, side_grads: bool | int = True,
                   data_parallel: bool = False):
     """The executor's op list for (keys, nano-batches) (host-only, no device)."""
     n = C.c_int32()

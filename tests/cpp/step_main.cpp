@@ -90,12 +90,12 @@ Config make_config(const std::string& name, int layers_override) {
 // Weights and inputs from the library's seeded generator, in a fixed order (the Python side
 // of the dump test repeats it): per key W, then per slot A, B; then X per group, dY per
 // projection.
-void fill(LayerSetTrainer& tr, const Config& c, uint64_t seed, float lr) {
+void fill(LayerSetTrainer& tr, const Config& c, uint64_t seed, double lr) {
   const int P = (int)c.projections.size();
   const int S = (int)c.jobs.size();
   std::vector<float> lrs, wd;
   for (int s = 0; s < S; ++s) {
-    lrs.push_back(lr * (1.0f + 0.25f * (s % 4)));
+    lrs.push_back((float)(lr * (1.0 + 0.25 * (s % 4))));  // as the Python drivers compute it
     wd.push_back(0.01f);
   }
   void* tmp = nullptr;
@@ -153,7 +153,7 @@ int dump(const char* path) {
   TrainerOptions opt;
   opt.nano_fixed = 2;
   LayerSetTrainer tr(set, opt, c.input_group);
-  fill(tr, c, 1000, 1e-3f);
+  fill(tr, c, 1000, 1e-3);
   tr.step();
   tr.step();
   std::vector<uint8_t> out;
@@ -203,7 +203,7 @@ int bench(int argc, char** argv) {
   TrainerOptions opt;
   opt.nano_fixed = nano;
   LayerSetTrainer tr(set, opt, c.input_group);
-  fill(tr, c, 2602, 1e-4f);
+  fill(tr, c, 2602, 1e-4);
   cudaStream_t s;
   if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return 1;
   for (int i = 0; i < warmup; ++i) tr.step(0, s);

@@ -21,6 +21,7 @@
 #include "lora_fleet/fused_lora.hpp"
 #include "lora_fleet/nano_pipeline.hpp"
 #include "lora_fleet/ssm_plan.hpp"
+#include "lora_fleet/trainer.hpp"
 
 using namespace lora_fleet;
 
@@ -349,6 +350,69 @@ void gpu_unreferenced_and_rank0_adapters() {
   CHECK(g0.dB.at("r0").rows() == 0 && g0.dB.at("r0").cols() == 2);
 }
 
+void gpu_persistent_fused_layer() {
+  // The persistent FusedLayer (W uploaded once, plan per batch, device buffers) computes the
+  // same Y as the per-call reference drop-in on the same job-sorted batch, and repeated
+  // calls with resident weights need no re-upload.
+  std::mt19937_64 rng(123);
+  std::normal_distribution<double> val;
+  const int T = 300, d = 96, k = 80;
+  const std::vector<int> ranks = {4, 16, 8};
+  const std::vector<int> counts = {120, 100, 80};
+  Matrix W(d, k);
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < k; ++j) W(i, j) = val(rng) / 10;
+  std::vector<AdapterMatrices> ad;
+  for (size_t s = 0; s < ranks.size(); ++s) {
+    Matrix A(d, ranks[s]), B(ranks[s], k);
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < ranks[s]; ++j) A(i, j) = val(rng) / 10;
+    for (int i = 0; i < ranks[s]; ++i)
+      for (int j = 0; j < k; ++j) B(i, j) = val(rng) / 10;
+    ad.push_back({"job" + std::to_string(s), A, B});
+  }
+  TokenBatch batch;
+  batch.rows = Matrix(T, d);
+  for (int t = 0; t < T; ++t)
+    for (int j = 0; j < d; ++j) batch.rows(t, j) = val(rng);
+  std::vector<int32_t> slots;
+  for (size_t s = 0; s < counts.size(); ++s)
+    for (int c = 0; c < counts[s]; ++c) {
+      slots.push_back((int32_t)s);
+      batch.segment_map.push_back("job" + std::to_string(s));
+    }
+  auto [yref, cost] = fused_forward(batch, W, ad);
+  FusedLayer lay(detail::device_index(), d, k, ranks);
+  std::vector<double> wrow(d * k);
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < k; ++j) wrow[i * k + j] = W(i, j);
+  lay.set_base(wrow.data(), TLORA_F64, TLORA_HOST);
+  for (size_t s = 0; s < ranks.size(); ++s) {
+    std::vector<double> a(d * ranks[s]), b(ranks[s] * k);
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < ranks[s]; ++j) a[i * ranks[s] + j] = ad[s].A(i, j);
+    for (int i = 0; i < ranks[s]; ++i)
+      for (int j = 0; j < k; ++j) b[i * k + j] = ad[s].B(i, j);
+    lay.set_adapter((int)s, a.data(), b.data(), TLORA_F64, TLORA_HOST);
+  }
+  tlora_plan* plan = lay.plan(slots);
+  detail::DeviceBuffer X(detail::device_index(), (size_t)T * d * 2), Y(detail::device_index(), (size_t)T * k * 4),
+      H(detail::device_index(), (size_t)T * lay.rank_pad_total() * 2);
+  std::vector<double> xrow(T * d);
+  for (int t = 0; t < T; ++t)
+    for (int j = 0; j < d; ++j) xrow[t * d + j] = batch.rows(t, j);
+  detail::tl_check(tlora_copy_to_device(X.p, TLORA_BF16, xrow.data(), TLORA_F64, T * d, nullptr));
+  for (int rep = 0; rep < 2; ++rep) {
+    lay.forward(plan, X.p, Y.p, TLORA_F32, H.p);
+    std::vector<double> y(T * k);
+    detail::tl_check(tlora_copy_to_host(y.data(), TLORA_F64, Y.p, TLORA_F32, T * k, nullptr));
+    double diff = 0.0;
+    for (int t = 0; t < T; ++t)
+      for (int j = 0; j < k; ++j) diff = std::max(diff, std::fabs(y[t * k + j] - yref(t, j)));
+    CHECK(diff == 0.0);
+  }
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -367,6 +431,7 @@ int main(int argc, char** argv) {
     cases.push_back({"fused_backward pinned by bilinearity", gpu_backward_bilinearity});
     cases.push_back({"unreferenced / rank-0 adapters as in the reference",
                      gpu_unreferenced_and_rank0_adapters});
+    cases.push_back({"persistent FusedLayer == per-call fused_forward", gpu_persistent_fused_layer});
   }
   for (auto& [name, fn] : cases) {
     const int before = g_fail;

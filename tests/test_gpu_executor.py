@@ -92,6 +92,7 @@ def test_executor_layout_is_the_rank_aware_map():
     out nano-major, job-contiguous inside a nano-batch; sample rows tile [0, T)."""
     wl = config("C2")
     ex = TrainingStep(wl, device=0, nano_fixed=1, graphs=False)
+    ex.init_random(wl.seed)  # plans need loaded adapters
     batch, weight = [j.batch for j in wl.jobs], sample_weights(wl)
     for n in (1, 2, 3, 5, 17, 40):
         k, t0, ns, sample_row = ex.layout(n)
@@ -195,5 +196,29 @@ def test_cpp_host_step_matches_python_driven_executor(tmp_path):
     parts = [st["Y"][n] for n in ex.names] + [st["dX"][n] for n in ex.names]
     for key in ex.keys:
         parts += st["g"][key] + st["P"][key]
-    py = np.concatenate([t.contiguous().view(torch.uint8).cpu().numpy().ravel() for t in parts])
-    assert py.size == cpp.size and np.array_equal(py, cpp)
+    chunks = [t.contiguous().view(torch.uint8).cpu().numpy().ravel() for t in parts]
+    py = np.concatenate(chunks)
+    assert py.size == cpp.size
+    off, bad = 0, []
+    for i, c in enumerate(chunks):  # name the first differing parts (diagnostics)
+        if not np.array_equal(c, cpp[off:off + c.size]):
+            bad.append(i)
+        off += c.size
+    assert not bad, f"differing parts (Y x{len(ex.names)}, dX x{len(ex.names)}, then grads/adapters per key): {bad[:10]}"
+
+
+def test_executor_data_parallel_multi_gpu():
+    """tests/step_dp_check.py under torchrun on every visible GPU (>= 2)."""
+    import socket
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (run via gpurun --gpus 2)")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    n = min(torch.cuda.device_count(), 4)
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), str(ROOT / "tests" / "step_dp_check.py")],
+                       capture_output=True, text=True, timeout=600)
+    print(p.stdout[-3000:])
+    assert p.returncode == 0 and "STEP_DP_CHECK PASS" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]

@@ -81,7 +81,7 @@ def test_nano_assign_balances_lora_work_better_than_job_order():
             assert lpt <= max(order), (name, n)
 
 
-def _check_schedule(ops, keys, n, ring, side, dp):
+def _check_schedule(ops, keys, n, ring, side, dp, early=False):
     idx = {}
     for i, o in enumerate(ops):
         idx.setdefault((o["kind"], o["key"], o["nano"]), []).append(i)
@@ -131,7 +131,8 @@ def _check_schedule(ops, keys, n, ring, side, dp):
             last_reader[o["slot"]] = i
             if side:
                 dx = idx[(capi.OP_DX, o["key"], o["nano"])][0]
-                assert o["wait0"] == dx
+                # after the key's dX launch, or (early) after the launch that wrote its dH
+                assert o["wait0"] == (written[(o["key"], o["nano"])][1] if early else dx)
     # main-stream fused launches: exactly 2 x keys x n, plus the step's first shrink
     main = [o for o in ops if o["stream"] == capi.STREAM_MAIN and o["kind"] != capi.OP_GRADS
             and o["kind"] != capi.OP_ADAMW]
@@ -142,10 +143,10 @@ def _check_schedule(ops, keys, n, ring, side, dp):
 @pytest.mark.parametrize("n", [1, 2, 3])
 def test_schedule_invariants(keys, n):
     for ring in (2, 3, 8):
-        for side in (True, False):
+        for side in (2, 1, 0):
             for dp in (False, True):
                 ops = schedule_host(keys, n, ring, side, dp)
-                _check_schedule(ops, keys, n, ring, side, dp)
+                _check_schedule(ops, keys, n, ring, bool(side), dp, early=side == 2)
 
 
 # ---------------------------------------------------------------- gloo world-2 dataflow

@@ -56,19 +56,25 @@ def measure(d, k, ranks, tokens_per_job, reps=10):
     for _ in range(3):
         step()
     torch.cuda.synchronize()
-    capi.call("tlora_profile_begin")
+    # step time WITHOUT the per-launch event brackets (they add a fixed cost per launch)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
         step()
     e1.record()
     torch.cuda.synchronize()
+    step_ms = e0.elapsed_time(e1) / reps
+    # component times: every launch bracketed by CUDA events
+    capi.call("tlora_profile_begin")
+    for _ in range(reps):
+        step()
+    torch.cuda.synchronize()
     cnt, ms6, fl6 = (C.c_int32 * 6)(), (C.c_double * 6)(), (C.c_double * 6)()
     capi.call("tlora_profile_end", cnt, ms6, fl6)
     rt = sum(r * tokens_per_job for r in ranks)
     R = lay.R
     rec = {"d": d, "k": k, "T": T, "jobs": len(ranks), "ranks": list(ranks),
-           "step_ms": e0.elapsed_time(e1) / reps,
+           "step_ms": step_ms,
            "gemm_ms": (ms6[capi.L_FWD] + ms6[capi.L_DX]) / reps,
            "gemm_flops": (fl6[capi.L_FWD] + fl6[capi.L_DX]) / reps,
            "lowrank_ms": sum(ms6[i] for i in (capi.L_SHRINK, capi.L_DH, capi.L_DB, capi.L_DA)) / reps,
@@ -80,6 +86,42 @@ def measure(d, k, ranks, tokens_per_job, reps=10):
     return rec
 
 
+def fit(grid):
+    """Model v2 (include/lora_fleet/hardware.hpp):
+        step = fixed + gemm_flops / F + lowrank_bytes / BW + optimizer_bytes / BW_opt
+    F and BW: slopes of the event-bracketed fused-GEMM (fwd + dX) and low-rank launch times;
+    fixed and BW_opt: least squares of the unbracketed step time minus those two terms."""
+    A = np.array([[2.0, r["gemm_flops"]] for r in grid])
+    y = np.array([r["gemm_ms"] * 1e-3 for r in grid])
+    (_, g_inv), *_ = np.linalg.lstsq(A, y, rcond=None)
+    A2 = np.array([[3.0, r["lowrank_bytes"]] for r in grid])
+    y2 = np.array([r["lowrank_ms"] * 1e-3 for r in grid])
+    (_, l_inv), *_ = np.linalg.lstsq(A2, y2, rcond=None)
+    rest = np.array([r["step_ms"] * 1e-3 - r["gemm_flops"] * g_inv - r["lowrank_bytes"] * l_inv
+                     for r in grid])
+    A3 = np.array([[1.0, r["optimizer_bytes"]] for r in grid])
+    (fixed, o_inv), *_ = np.linalg.lstsq(A3, rest, rcond=None)
+    F, BW, BWo = 1.0 / g_inv, 1.0 / l_inv, 1.0 / o_inv
+
+    def predict(r):
+        return fixed + r["gemm_flops"] / F + r["lowrank_bytes"] / BW + r["optimizer_bytes"] / BWo
+
+    errs = [abs(predict(r) - r["step_ms"] * 1e-3) / (r["step_ms"] * 1e-3) for r in grid]
+    return {
+        "model_version": 2,
+        "model": "step_s = fixed_overhead_s + gemm_flops/F + lowrank_bytes/BW + "
+                 "optimizer_bytes/optimizer_BW",
+        "F_flops_per_s": F, "BW_bytes_per_s": BW, "optimizer_BW_bytes_per_s": BWo,
+        "fixed_overhead_s": fixed,
+        "fit_rel_err_median": float(np.median(errs)), "fit_rel_err_max": float(np.max(errs)),
+        "hardware_spec": {  # drop-in values for proj/include/lora_fleet/hardware.hpp
+            "gpu_flops": F, "kernel_launch_overhead": fixed, "weight_stream_bw": BW,
+            "note": "gpu_flops = sustained fused base+LoRA GEMM rate under the 1 kW cap; "
+                    "kernel_launch_overhead = fixed cost of one fused layer's training step "
+                    "(its launches), per nano-batch as nano_pipeline.hpp:79 charges it"},
+    }
+
+
 def main():
     grid = []
     for d, k in ((1024, 1024), (2048, 2048), (4096, 1024), (4096, 4096), (4096, 12288), (12288, 4096)):
@@ -88,38 +130,9 @@ def main():
                 grid.append(measure(d, k, ranks, tpj))
                 print(f"d={d} k={k} jobs={len(ranks)} T={grid[-1]['T']} "
                       f"step={grid[-1]['step_ms']:.3f} ms", flush=True)
-    # fused GEMMs: t = a + flops / F (two launches per step)
-    A = np.array([[2.0, r["gemm_flops"]] for r in grid])
-    y = np.array([r["gemm_ms"] * 1e-3 for r in grid])
-    (g_over, g_inv), *_ = np.linalg.lstsq(A, y, rcond=None)
-    # low-rank launches: t = a + bytes / BW (three per step: shrink, dH, dB+dA)
-    A2 = np.array([[3.0, r["lowrank_bytes"]] for r in grid])
-    y2 = np.array([r["lowrank_ms"] * 1e-3 for r in grid])
-    (l_over, l_inv), *_ = np.linalg.lstsq(A2, y2, rcond=None)
-    F, BW = 1.0 / g_inv, 1.0 / l_inv
-    other = [r["step_ms"] * 1e-3 - r["gemm_ms"] * 1e-3 - r["lowrank_ms"] * 1e-3 for r in grid]
-    other_per_byte = np.median([o / r["optimizer_bytes"] for o, r in zip(other, grid)])
-
-    def predict(r):
-        return (2 * g_over + r["gemm_flops"] / F + 3 * l_over + r["lowrank_bytes"] / BW
-                + other_per_byte * r["optimizer_bytes"])
-
-    errs = [abs(predict(r) - r["step_ms"] * 1e-3) / (r["step_ms"] * 1e-3) for r in grid]
-    out = {
-        "device": torch.cuda.get_device_name(0),
-        "model": "step_s = 2*gemm_overhead + gemm_flops/F + 3*lowrank_overhead + "
-                 "lowrank_bytes/BW + optimizer_s_per_byte*optimizer_bytes",
-        "F_flops_per_s": F, "gemm_launch_overhead_s": g_over,
-        "BW_bytes_per_s": BW, "lowrank_launch_overhead_s": l_over,
-        "optimizer_s_per_byte": other_per_byte,
-        "fit_rel_err_median": float(np.median(errs)), "fit_rel_err_max": float(np.max(errs)),
-        "hardware_spec": {  # drop-in values for proj/include/lora_fleet/hardware.hpp
-            "gpu_flops": F,
-            "kernel_launch_overhead": float((2 * g_over + 3 * l_over) / 5),
-            "note": "gpu_flops = sustained fused base+LoRA GEMM rate under the 1 kW cap; "
-                    "kernel_launch_overhead = mean fixed cost per fused-layer launch"},
-        "grid": grid,
-    }
+    out = fit(grid)
+    out["device"] = torch.cuda.get_device_name(0)
+    out["grid"] = grid
     path = Path(sys.argv[1]) if len(sys.argv) > 1 else ROOT / "profiles" / "b200_cost_profile.json"
     path.write_text(json.dumps(out, indent=1))
     print(json.dumps({k: v for k, v in out.items() if k != "grid"}, indent=1))
