@@ -37,6 +37,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -536,7 +537,18 @@ int tlora_step_create(const tlora_step_desc* desc, tlora_comm* comm, tlora_step*
       ST_CUDA(cudaMemcpy(st->present, pres.data(), (size_t)st->S * 4, cudaMemcpyHostToDevice));
     }
     ST_CUDA(cudaStreamCreateWithFlags(&st->exec, cudaStreamNonBlocking));
-    if (D.flags & TLORA_STEP_SIDE_GRADS) ST_CUDA(cudaStreamCreateWithFlags(&st->side, cudaStreamNonBlocking));
+    if (D.flags & TLORA_STEP_SIDE_GRADS) {
+      // TLORA_SIDE_PRIORITY=1 (A/B knob): the side stream's CTAs are scheduled ahead of the
+      // main stream's when SMs free up (the fused GEMM's tail)
+      const char* e = std::getenv("TLORA_SIDE_PRIORITY");
+      if (e && e[0] == '1') {
+        int lo = 0, hi = 0;
+        ST_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        ST_CUDA(cudaStreamCreateWithPriority(&st->side, cudaStreamNonBlocking, hi));
+      } else {
+        ST_CUDA(cudaStreamCreateWithFlags(&st->side, cudaStreamNonBlocking));
+      }
+    }
     if (comm) ST_CUDA(cudaStreamCreateWithFlags(&st->comm_s, cudaStreamNonBlocking));
     ST_CUDA(cudaEventCreate(&st->t_begin));
     ST_CUDA(cudaEventCreate(&st->t_end));

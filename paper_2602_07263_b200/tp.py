@@ -15,8 +15,9 @@ activations between projection groups):
            (all-reduced over TP once per step).
 
 The combined batch (Σ_j B_j samples) is cut into N nano-batches with the reference's
-balanced `partition` (nano_pipeline.hpp:51-60); samples keep job order, so every nano-batch
-is job-contiguous (the fast case of the tile packer). A compute stream runs the tlora
+balanced `partition` counts (nano_pipeline.hpp:51-60) and the rank-aware map of the step
+executor (tlora_nano_assign: LoRA work balanced across nano-batches); every nano-batch is
+job-contiguous (the fast case of the tile packer). A compute stream runs the tlora
 launches and a comm stream runs the NCCL collectives: the all-gather of nano n+1 and the
 reduce-scatter of nano n-1 overlap the GEMMs of nano n. N is adapted online by the
 reference's AIMD rule (nano_pipeline.hpp:99-112) from CUDA-event step times — the real
@@ -59,17 +60,18 @@ class NanoBatch:
 
 
 def nano_batches(wl: Workload, n: int) -> list[NanoBatch]:
-    """partition(Σ_j B_j, n) samples into nano-batches, job order kept (rank-aware in the
-    sense that each nano-batch holds whole samples of consecutive jobs, so its tile plan
-    packs at most a few ranks per M-tile)."""
-    samples = [(s, j.seq_len) for s, j in enumerate(wl.jobs) for _ in range(j.batch)]
-    n_eff, counts = partition(len(samples), n)
-    out, i, t0 = [], 0, 0
-    for idx, c in enumerate(counts):
-        chunk = samples[i:i + c]
-        slots = np.concatenate([np.full(seq, s, np.int32) for s, seq in chunk])
+    """partition(Σ_j B_j, n) samples into nano-batches with the executor's rank-aware map
+    (tlora_nano_assign: partition's counts, per-sample work balanced across nano-batches,
+    each (nano, job) a contiguous range of the job's samples); inside a nano-batch the jobs
+    stay contiguous in slot order, the fast case of the tile packer."""
+    from .step import nano_assign, sample_weights
+    batch = [j.batch for j in wl.jobs]
+    k, per, _, ns = nano_assign(batch, sample_weights(wl), n)
+    out, t0 = [], 0
+    for idx in range(k):
+        slots = np.concatenate([np.full(int(ns[idx, s]) * j.seq_len, s, np.int32)
+                                for s, j in enumerate(wl.jobs)])
         out.append(NanoBatch(idx, t0, int(slots.shape[0]), slots))
-        i += c
         t0 += int(slots.shape[0])
     return out
 

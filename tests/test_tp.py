@@ -30,8 +30,15 @@ def test_nano_batches_follow_reference_partition(name, n):
     assert len(nb) == n_ref
     seq = {j.seq_len for j in wl.jobs}.pop()
     assert [b.tokens for b in nb] == [c * seq for c in counts]
-    # whole samples, job order kept: concatenation == the job-contiguous batch
-    assert np.array_equal(np.concatenate([b.slots for b in nb]), wl.token_slots())
+    # whole samples, the rank-aware map (oracle restatement): nano i holds ns[i, s] samples
+    # of job s, jobs in slot order
+    from paper_2602_07263_b200.step import sample_weights
+    _, _, _, ns = O.nano_assign([j.batch for j in wl.jobs], sample_weights(wl), n)
+    for i, b in enumerate(nb):
+        want = np.concatenate([np.full(ns[i, s] * j.seq_len, s, np.int32)
+                               for s, j in enumerate(wl.jobs)])
+        assert np.array_equal(b.slots, want)
+    assert np.array_equal(np.sort(np.concatenate([b.slots for b in nb])), wl.token_slots())
     assert [b.t0 for b in nb] == list(np.cumsum([0] + [b.tokens for b in nb])[:-1])
     for b in nb:  # job-contiguous inside each nano-batch
         assert np.all(np.diff(b.slots) >= 0)

@@ -1,12 +1,16 @@
 """profiles/traffic.json from an ncu launch list of ONE step's 14 fused-GEMM launches.
 
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \\
-      --clock-control none -k regex:lora_gemm2 --launch-skip 14 -c 14 --csv \\
-      --log-file traffic14.csv python bench.py --steps 1 --warmup 3 --no-graph
-  python tools/traffic_from_ncu.py traffic14.csv
+      --clock-control none -k regex:lora_gemm2 --launch-skip 31 -c 14 --csv \\
+      --log-file traffic14.csv python tools/prof_step.py --warmup 2 --steps 1
+  python tools/traffic_from_ncu.py traffic14.csv <commit> [out.json]
+
+(the executor's step: one standalone shrink launch, then the 14 fused GEMMs; skip two
+steps + the third step's shrink).
 
 Launch order of a chained C2 step: fwd q,k,v,o,gate,up,down (each carrying the next
-projection's shrink tiles), then dX down,up,gate,o,v,k,q (each carrying the next dH).
+projection's shrink tiles; the last one the backward's first dH), then dX
+down,up,gate,o,v,k,q (each carrying the next dH).
 `traffic` in bench.py's roofline = mean DRAM bytes (read + write) per launch; the
 algorithmic bytes per launch (each operand / output touched once) are reported beside it.
 """
@@ -35,7 +39,7 @@ def main():
     T = wl.tokens
     R = sum((j.rank + 7) // 8 * 8 for j in wl.jobs)
     projs = wl.projections
-    fwd = [(p, projs[i + 1] if i + 1 < len(projs) else None) for i, p in enumerate(projs)]
+    fwd = [(p, projs[i + 1] if i + 1 < len(projs) else "dh") for i, p in enumerate(projs)]
     rev = list(reversed(projs))
     bwd = [(p, rev[i + 1] if i + 1 < len(rev) else None) for i, p in enumerate(rev)]
     launches = []
@@ -43,15 +47,21 @@ def main():
         for (name, d, k), nxt in seq:
             main_b = 2 * (T * d + d * k + T * k + T * R + R * (k if kind == "fwd" else d))
             sec = 0
-            if nxt is not None:
+            if nxt == "dh":  # the last forward launch prefetches dH of its own projection
+                sec = 2 * (T * k + R * k + T * R)
+                nxt = (name, d, k)
+                label = f"fwd {name} + dH {name}"
+            elif nxt is not None:
                 nn, nd, nk = nxt
                 if kind == "fwd":  # X_next (unless shared with this projection's X) + Aᵀ + H_next
                     shared = INPUT_GROUP.get(nn) == INPUT_GROUP.get(name)
                     sec = 2 * ((0 if shared else T * nd) + R * nd + T * R)
                 else:              # dY_next + Bcat + dH_next
                     sec = 2 * (T * nk + R * nk + T * R)
-            launches.append({"launch": f"{kind} {name}" + (f" + {'shrink' if kind == 'fwd' else 'dH'} {nxt[0]}" if nxt else ""),
-                             "algorithmic_bytes": main_b + sec})
+            if not (kind == "fwd" and nxt == (name, d, k)):
+                label = f"{kind} {name}" + (f" + {'shrink' if kind == 'fwd' else 'dH'} {nxt[0]}"
+                                            if nxt else "")
+            launches.append({"launch": label, "algorithmic_bytes": main_b + sec})
     ids = sorted(by)
     assert len(ids) == len(launches), (len(ids), len(launches))
     for i, L in zip(ids, launches):
@@ -69,11 +79,13 @@ def main():
            "traffic_over_algorithmic": round(mean_dram / mean_alg, 2),
            "source": f"{src.name}: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
                      "--clock-control none (cache flushed per launch)",
+           "commit": sys.argv[2] if len(sys.argv) > 2 else None,
            "note": "the launches are tensor-pipe bound (~90% tensor active, DRAM ~20% of peak); "
                    "the L2 panel raster (48 MB budget) minimises DRAM bytes among the budgets "
                    "swept (8..64 MB: 6.2 .. 2.35 GB for gate fwd); the re-reads do not bind",
            "launches": launches}
-    (ROOT / "profiles" / "traffic.json").write_text(json.dumps(out, indent=1))
+    dst = Path(sys.argv[3]) if len(sys.argv) > 3 else ROOT / "profiles" / "traffic.json"
+    dst.write_text(json.dumps(out, indent=1))
     print(json.dumps({k: v for k, v in out.items() if k != "launches"}, indent=1))
 
 
