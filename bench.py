@@ -240,7 +240,7 @@ def run_executor(args, rank, world, local_rank):
     comm = make_comm(local_rank, rank, world) if world > 1 else None
     st = TrainingStep(wl, device=local_rank, nano_fixed=max(0, args.nano_batches),
                       nano_init=args.nano_init, graphs=not args.no_graph, input_sets=2,
-                      comm=comm)
+                      comm=comm, sharded_opt=args.dp_sharded_opt and world > 1)
     st.init_random(seed=wl.seed + rank)
     st.enable_optimizer()
     stream = torch.cuda.current_stream()
@@ -398,8 +398,12 @@ def run_executor(args, rank, world, local_rank):
                    "projections": wl.projections, "parallelism": f"dp{world}",
                    "driver": "C++ step executor (tlora_step_run: libtlora.so)",
                    "nano_batches": nano_desc, "aimd_trajectory_n_ms": traj,
-                   "dp_allreduce": None if world == 1 else "nccl via tlora_comm (C-ABI), per key "
-                                   "after its last nano-batch, on the executor's comm stream",
+                   "dp_allreduce": None if world == 1 else (
+                       "sharded optimizer: per key reduce-scatter (fp32) -> AdamW on this rank's "
+                       "packed-row shard -> all-gather (bf16 operands), nccl via tlora_comm"
+                       if args.dp_sharded_opt else
+                       "nccl all-reduce via tlora_comm (C-ABI), per key after its last "
+                       "nano-batch, on the executor's comm stream"),
                    "cuda_graph": not args.no_graph and world == 1,
                    "graph_replays_timed": graph_launches,
                    "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)",
@@ -1042,6 +1046,9 @@ def main():
                     help="cpp: run the pure C++ host binary (tests/cpp/_build/step_main)")
     ap.add_argument("--nano-batches", type=int, default=NANO_DEFAULT,
                     help="executor: fixed nano-batch count N (> 0), or 0 = AIMD every step")
+    ap.add_argument("--dp-sharded-opt", action="store_true",
+                    help="executor, N > 1 GPUs: sharded optimizer (reduce-scatter, AdamW on 1/N "
+                         "of the rows, all-gather) instead of the gradient all-reduce")
     ap.add_argument("--nano-init", type=int, default=4,
                     help="executor: AIMD initial N (reference default 4)")
     ap.add_argument("--fused-rs", default="auto",

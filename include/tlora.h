@@ -151,6 +151,11 @@ int tlora_layer_optimizer_step(tlora_layer* layer, float grad_scale, void* strea
  * they are). present == NULL updates every slot (= tlora_layer_optimizer_step). */
 int tlora_layer_optimizer_step_masked(tlora_layer* layer, const int32_t* present, float grad_scale,
                                       void* stream);
+/* AdamW on the packed rows [row_lo, row_hi) only (even bounds): a data-parallel rank's
+ * shard of the sharded optimizer (tlora_layer_dp_shard). Step counters advance for every
+ * present slot, so all ranks stay in step. */
+int tlora_layer_optimizer_step_rows(tlora_layer* layer, const int32_t* present, float grad_scale,
+                                    int64_t row_lo, int64_t row_hi, void* stream);
 /* Copy one slot's fp32 master adapter out: A is d x r, B is r x k. */
 int tlora_layer_read_adapter(tlora_layer* layer, int32_t slot, float* A, float* B, int where,
                              void* stream);
@@ -382,8 +387,10 @@ enum tlora_step_flags {
   TLORA_STEP_SIDE_GRADS = 1, /* dB+dA (and AdamW) of each key on a side stream             */
   TLORA_STEP_GRAPH = 2,      /* capture each (N, input set) step into a CUDA graph after its
                                 first eager run and replay it (single replica only)        */
-  TLORA_STEP_EARLY_GRADS = 4 /* a key's dB+dA waits only for the launch that produced its dH,
-                                so it may overlap the key's own dX launch                   */
+  TLORA_STEP_EARLY_GRADS = 4, /* a key's dB+dA waits only for the launch that produced its
+                                 dH, so it may overlap the key's own dX launch              */
+  TLORA_STEP_SHARDED_OPT = 8  /* with a communicator: reduce-scatter the gradients, AdamW on
+                                 this rank's row shard, all-gather the bf16 operands         */
 };
 enum tlora_run_flags { TLORA_RUN_EAGER = 1 /* launch eagerly even if a graph exists */ };
 typedef struct tlora_step_desc {
@@ -447,7 +454,8 @@ int tlora_step_run(tlora_step* step, int32_t set, int32_t flags, void* stream,
 
 /* One op of the step schedule (host-only view for tests and drivers). */
 enum tlora_op_kind { TLORA_OP_SHRINK = 0, TLORA_OP_FWD = 1, TLORA_OP_DH = 2, TLORA_OP_DX = 3,
-                     TLORA_OP_GRADS = 4, TLORA_OP_ALLREDUCE = 5, TLORA_OP_ADAMW = 6 };
+                     TLORA_OP_GRADS = 4, TLORA_OP_ALLREDUCE = 5, TLORA_OP_ADAMW = 6,
+                     TLORA_OP_REDUCE_SCATTER = 7, TLORA_OP_ALLGATHER = 8 };
 enum tlora_stream_id { TLORA_STREAM_MAIN = 0, TLORA_STREAM_SIDE = 1, TLORA_STREAM_COMM = 2 };
 typedef struct tlora_step_op {
   int32_t kind, stream, key, nano;
@@ -458,10 +466,24 @@ typedef struct tlora_step_op {
   int32_t wait0, wait1;                 /* ops (on other streams) waited for, -1         */
 } tlora_step_op;
 /* side_grads: 0 = gradients on the main stream, 1 = side stream, 2 = side stream with
- * TLORA_STEP_EARLY_GRADS. */
+ * TLORA_STEP_EARLY_GRADS. data_parallel: 0 = one replica, 1 = all-reduce, 2 = sharded
+ * optimizer (TLORA_STEP_SHARDED_OPT). */
 int tlora_step_schedule_host(int32_t keys, int32_t nano, int32_t ring, int32_t side_grads,
                              int32_t data_parallel, tlora_step_op* out, int32_t cap,
                              int32_t* count);
+
+/* Sharded data-parallel optimizer (the alternative to tlora_layer_allreduce_grads + a full
+ * AdamW on every rank): the packed rank rows are split evenly over `group`; this rank owns
+ * [row_lo, row_hi). reduce_scatter_grads sums the fp32 gradients of the owned rows over the
+ * group (in place); tlora_layer_optimizer_step_rows updates them; allgather_operands
+ * gathers every rank's refreshed bf16 rows (Aᵀcat, Bcat) and rebuilds the transposed copies
+ * the kernels read. fp32 masters / moments of rows a rank does not own are not kept
+ * current on that rank. Needs R % group size == 0 with even shards. */
+int tlora_layer_dp_shard(const tlora_layer* layer, const tlora_comm* comm, int group,
+                         int64_t* row_lo, int64_t* row_hi);
+int tlora_layer_reduce_scatter_grads(tlora_layer* layer, tlora_comm* comm, int group,
+                                     void* stream);
+int tlora_layer_allgather_operands(tlora_layer* layer, tlora_comm* comm, int group, void* stream);
 
 #ifdef __cplusplus
 }

@@ -66,10 +66,10 @@ class StepOpC(C.Structure):
                                          "wait1")]
 
 
-STEP_SIDE_GRADS, STEP_GRAPH, STEP_EARLY_GRADS = 1, 2, 4
+STEP_SIDE_GRADS, STEP_GRAPH, STEP_EARLY_GRADS, STEP_SHARDED_OPT = 1, 2, 4, 8
 RUN_EAGER = 1
 BUF_X, BUF_DY, BUF_Y, BUF_DX, BUF_H = range(5)
-OP_SHRINK, OP_FWD, OP_DH, OP_DX, OP_GRADS, OP_ALLREDUCE, OP_ADAMW = range(7)
+OP_SHRINK, OP_FWD, OP_DH, OP_DX, OP_GRADS, OP_ALLREDUCE, OP_ADAMW, OP_REDUCE_SCATTER, OP_ALLGATHER = range(9)
 STREAM_MAIN, STREAM_SIDE, STREAM_COMM = range(3)
 
 # exported symbol -> (restype, argtypes); also the list the CPU test checks against the header
@@ -105,6 +105,12 @@ SIGNATURES = {
     "tlora_layer_optimizer_step_masked": (C.c_int, [C.c_void_p, C.c_void_p, C.c_float,
                                                     C.c_void_p]),
     "tlora_plan_present_mask": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "tlora_layer_optimizer_step_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_float, C.c_int64,
+                                                  C.c_int64, C.c_void_p]),
+    "tlora_layer_dp_shard": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_int64)]),
+    "tlora_layer_reduce_scatter_grads": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "tlora_layer_allgather_operands": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "tlora_layer_read_adapter": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int,
                                            C.c_void_p]),
     "tlora_plan_create": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_int32),

@@ -327,6 +327,24 @@ __global__ void pack_adapter_kernel(const void* A, const void* B, int dtype, int
   }
 }
 
+// out (N x R) = in (R x N)ᵀ for bf16, 32 x 32 tiles through shared memory: the transposed
+// operand copies (Acat, BcatT) rebuilt from the row-major ones (AT, Bcat) after a
+// data-parallel all-gather of the refreshed row shards.
+__global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ in, int64_t R, int64_t N,
+                                      __nv_bfloat16* __restrict__ out) {
+  __shared__ __nv_bfloat16 tile[32][34];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < R && c < N) tile[i][threadIdx.x] = in[r * N + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < R && c < N) out[c * R + r] = tile[threadIdx.x][i];
+  }
+}
+
 // Fused multi-job AdamW over a layer's packed adapters P (R x N, fp32 master) with
 // gradient G and moments; per-row job hyperparameters via row_slot -> hp[slot]. Writes the
 // bf16 operand copies in both layouts the kernels read: P16 (R x N) and P16t (N x R).
@@ -354,13 +372,16 @@ struct AdamJob {
 __global__ void __launch_bounds__(256) adamw_layer_kernel(
     const AdamJob j0, const AdamJob j1, const int32_t* __restrict__ row_slot,
     const float2* __restrict__ hp, int32_t* __restrict__ steps, int32_t num_slots, float b1,
-    float b2, float eps, float grad_scale, int64_t R, const int32_t* __restrict__ present) {
+    float b2, float eps, float grad_scale, int64_t R, const int32_t* __restrict__ present,
+    int64_t row_lo, int64_t row_hi) {
+  // rows [row_lo, row_hi) of both packed matrices (the whole [0, R) unless a data-parallel
+  // rank updates only its shard); R stays the row pitch of the transposed copies
   __shared__ float tile[32][65];
   __shared__ bool last;
   const bool second = (int)blockIdx.x >= j0.nblocks;
   const AdamJob& J = second ? j1 : j0;
   const int b = second ? (int)blockIdx.x - j0.nblocks : (int)blockIdx.x;
-  const int64_t r0 = (int64_t)(b / J.blocks_x) * 32, c0 = (int64_t)(b % J.blocks_x) * 64;
+  const int64_t r0 = row_lo + (int64_t)(b / J.blocks_x) * 32, c0 = (int64_t)(b % J.blocks_x) * 64;
   const int tid = threadIdx.x;
   const int N = (int)J.N;
 #pragma unroll
@@ -368,7 +389,7 @@ __global__ void __launch_bounds__(256) adamw_layer_kernel(
     const int i = it * 16 + tid / 16, cq = (tid % 16) * 4;
     const int64_t r = r0 + i, c = c0 + cq;
     float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < R && c < N) {
+    if (r < row_hi && c < N) {
       const int sl = row_slot[r];
       const int64_t idx = r * N + c;
       // slots absent from the step (present[sl] == 0) take no optimizer step: masters,
@@ -418,7 +439,7 @@ __global__ void __launch_bounds__(256) adamw_layer_kernel(
   for (int it = 0; it < 4; ++it) {
     const int cc = it * 16 + tid / 16, rr = (tid % 16) * 2;
     const int64_t c = c0 + cc, r = r0 + rr;
-    if (c < N && r < R)  // R % 8 == 0: r + 1 < R too
+    if (c < N && r < row_hi)  // row_lo, row_hi even: r + 1 < row_hi too
       *reinterpret_cast<uint32_t*>(J.P16t + c * R + r) =
           tlora::ptx::pack_bf16x2(tile[rr][cc], tile[rr + 1][cc]);
   }
@@ -1112,34 +1133,52 @@ int tlora_layer_optimizer_step(tlora_layer* layer, float grad_scale, void* strea
   return tlora_layer_optimizer_step_masked(layer, nullptr, grad_scale, stream);
 }
 
+namespace {
+void adamw_rows(tlora_layer* layer, const int32_t* present, float grad_scale, int64_t row_lo,
+                int64_t row_hi, cudaStream_t s) {
+  require(layer->opt_set, TLORA_ERR_ARG, "optimizer not configured (tlora_layer_set_optimizer)");
+  const int S = (int)layer->L.rank.size();
+  const int64_t R = layer->L.R, d = layer->L.d, k = layer->L.k;
+  require(row_lo >= 0 && row_lo <= row_hi && row_hi <= R && row_lo % 2 == 0 && row_hi % 2 == 0,
+          TLORA_ERR_ARG, "optimizer row range must be even bounds inside [0, R]");
+  // enqueue-only, no host data: capturable in a CUDA graph
+  AdamJob job[2];
+  const int64_t Ns[2] = {d, k};
+  float* G[2] = {layer->dAT.p, layer->dB.p};
+  float* P[2] = {layer->ATm.p, layer->Bm.p};
+  float* M[2] = {layer->mA.p, layer->mB.p};
+  float* V[2] = {layer->vA.p, layer->vB.p};
+  __nv_bfloat16* P16[2] = {layer->AT.p, layer->Bcat.p};
+  __nv_bfloat16* P16t[2] = {layer->Acat.p, layer->BcatT.p};
+  const int64_t rows = std::max<int64_t>(row_hi - row_lo, 1);
+  for (int j = 0; j < 2; ++j) {
+    const int bx = (int)tlora::ceil_div(Ns[j], 64);
+    job[j] = {G[j], P[j], M[j], V[j], P16[j], P16t[j], Ns[j], bx,
+              bx * (int)tlora::ceil_div(rows, 32)};
+  }
+  adamw_layer_kernel<<<job[0].nblocks + job[1].nblocks, 256, 0, s>>>(
+      job[0], job[1], layer->row_slot.p, layer->hparams.p, layer->steps_dev.p, S, layer->beta1,
+      layer->beta2, layer->eps, grad_scale, R, present, row_lo, row_hi);
+  TL_CUDA(cudaGetLastError());
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+}  // namespace
+
 int tlora_layer_optimizer_step_masked(tlora_layer* layer, const int32_t* present, float grad_scale,
                                       void* stream) {
   return guarded([&] {
     require(layer != nullptr, TLORA_ERR_ARG, "layer is null");
-    require(layer->opt_set, TLORA_ERR_ARG, "optimizer not configured (tlora_layer_set_optimizer)");
     DeviceGuard g(layer->device);
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const int S = (int)layer->L.rank.size();
-    const int64_t R = layer->L.R, d = layer->L.d, k = layer->L.k;
-    // enqueue-only, no host data: capturable in a CUDA graph
-    AdamJob job[2];
-    const int64_t Ns[2] = {d, k};
-    float* G[2] = {layer->dAT.p, layer->dB.p};
-    float* P[2] = {layer->ATm.p, layer->Bm.p};
-    float* M[2] = {layer->mA.p, layer->mB.p};
-    float* V[2] = {layer->vA.p, layer->vB.p};
-    __nv_bfloat16* P16[2] = {layer->AT.p, layer->Bcat.p};
-    __nv_bfloat16* P16t[2] = {layer->Acat.p, layer->BcatT.p};
-    for (int j = 0; j < 2; ++j) {
-      const int bx = (int)tlora::ceil_div(Ns[j], 64);
-      job[j] = {G[j], P[j], M[j], V[j], P16[j], P16t[j], Ns[j], bx,
-                bx * (int)tlora::ceil_div(R, 32)};
-    }
-    adamw_layer_kernel<<<job[0].nblocks + job[1].nblocks, 256, 0, s>>>(
-        job[0], job[1], layer->row_slot.p, layer->hparams.p, layer->steps_dev.p, S,
-        layer->beta1, layer->beta2, layer->eps, grad_scale, R, present);
-    TL_CUDA(cudaGetLastError());
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    adamw_rows(layer, present, grad_scale, 0, layer->L.R, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int tlora_layer_optimizer_step_rows(tlora_layer* layer, const int32_t* present, float grad_scale,
+                                    int64_t row_lo, int64_t row_hi, void* stream) {
+  return guarded([&] {
+    require(layer != nullptr, TLORA_ERR_ARG, "layer is null");
+    DeviceGuard g(layer->device);
+    adamw_rows(layer, present, grad_scale, row_lo, row_hi, reinterpret_cast<cudaStream_t>(stream));
   });
 }
 

@@ -224,4 +224,70 @@ int tlora_layer_allreduce_grads(tlora_layer* layer, tlora_comm* comm, int group,
   });
 }
 
+// Sharded data-parallel optimizer (ZeRO-1 style over the packed adapters): reduce-scatter
+// the fp32 gradients by packed-row shards, AdamW on this rank's shard, all-gather the
+// refreshed bf16 operands and rebuild their transposed copies.
+int tlora_layer_dp_shard(const tlora_layer* layer, const tlora_comm* comm, int group,
+                         int64_t* row_lo, int64_t* row_hi) {
+  return guarded([&] {
+    require(layer != nullptr && comm != nullptr, TLORA_ERR_ARG, "null argument");
+    require(group == TLORA_GROUP_DP || group == TLORA_GROUP_WORLD, TLORA_ERR_ARG,
+            "shard over the DP (or world) group");
+    const int32_t P = group == TLORA_GROUP_DP ? comm->dp : comm->world;
+    const int32_t me = group == TLORA_GROUP_DP ? comm->rank / comm->tp : comm->rank;
+    const int64_t R = layer->L.R;
+    require(R % P == 0 && (R / P) % 2 == 0, TLORA_ERR_SHAPE,
+            "packed rank width R must split into even row shards over the group");
+    if (row_lo) *row_lo = me * (R / P);
+    if (row_hi) *row_hi = (me + 1) * (R / P);
+  });
+}
+
+int tlora_layer_reduce_scatter_grads(tlora_layer* layer, tlora_comm* comm, int group,
+                                     void* stream) {
+  return guarded([&] {
+    int64_t lo = 0, hi = 0;
+    if (tlora_layer_dp_shard(layer, comm, group, &lo, &hi) != TLORA_OK)
+      throw Status(TLORA_ERR_SHAPE, g_last_error);
+    ncclComm_t c = group_comm(comm, group);
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const NcclApi& api = nccl();
+    const size_t nA = (size_t)(hi - lo) * layer->L.d, nB = (size_t)(hi - lo) * layer->L.k;
+    // in place: this rank's shard of rows [lo, hi) receives the sum (recv = send + rank * n)
+    TL_NCCL(api.group_start());
+    TL_NCCL(api.reduce_scatter(layer->dAT.p, layer->dAT.p + (size_t)lo * layer->L.d, nA,
+                               ncclFloat32, ncclSum, c, s));
+    TL_NCCL(api.reduce_scatter(layer->dB.p, layer->dB.p + (size_t)lo * layer->L.k, nB,
+                               ncclFloat32, ncclSum, c, s));
+    TL_NCCL(api.group_end());
+  });
+}
+
+int tlora_layer_allgather_operands(tlora_layer* layer, tlora_comm* comm, int group, void* stream) {
+  return guarded([&] {
+    int64_t lo = 0, hi = 0;
+    if (tlora_layer_dp_shard(layer, comm, group, &lo, &hi) != TLORA_OK)
+      throw Status(TLORA_ERR_SHAPE, g_last_error);
+    ncclComm_t c = group_comm(comm, group);
+    DeviceGuard g(layer->device);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const NcclApi& api = nccl();
+    const int64_t R = layer->L.R, d = layer->L.d, k = layer->L.k;
+    TL_NCCL(api.group_start());
+    TL_NCCL(api.all_gather(layer->AT.p + (size_t)lo * d, layer->AT.p, (size_t)(hi - lo) * d,
+                           ncclBfloat16, c, s));
+    TL_NCCL(api.all_gather(layer->Bcat.p + (size_t)lo * k, layer->Bcat.p, (size_t)(hi - lo) * k,
+                           ncclBfloat16, c, s));
+    TL_NCCL(api.group_end());
+    const dim3 blk(32, 8);
+    transpose_bf16_kernel<<<dim3((unsigned)tlora::ceil_div(d, 32), (unsigned)tlora::ceil_div(R, 32)),
+                            blk, 0, s>>>(layer->AT.p, R, d, layer->Acat.p);
+    transpose_bf16_kernel<<<dim3((unsigned)tlora::ceil_div(k, 32), (unsigned)tlora::ceil_div(R, 32)),
+                            blk, 0, s>>>(layer->Bcat.p, R, k, layer->BcatT.p);
+    TL_CUDA(cudaGetLastError());
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+  });
+}
+
 }  // extern "C"

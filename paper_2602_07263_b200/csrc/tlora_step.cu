@@ -26,7 +26,9 @@
 //   side stream   per (key, nano) the combined dB+dA launch (accumulating over nano-
 //                 batches), then, after the last nano-batch, the key's AdamW;
 //   comm stream   (data-parallel replicas) the key's gradient all-reduce as soon as its
-//                 last nano-batch's gradients exist, then its AdamW (grads / replicas).
+//                 last nano-batch's gradients exist, then its AdamW (grads / replicas); or,
+//                 with the sharded optimizer, reduce-scatter -> AdamW of this rank's row
+//                 shard -> all-gather of the refreshed bf16 operands.
 // The backward's dH values live in a ring of buffers; a dX launch that overwrites a ring
 // slot waits for the side-stream reader of that slot.
 // Buffers are row-major bf16, one step-sized buffer per tensor; nano-batch i is the row
@@ -103,7 +105,9 @@ struct Op {
 
 // early: a GRADS op waits only for the launch that produced its dH (it may then overlap the
 // key's own dX launch) instead of for the key's dX launch.
-std::vector<Op> build_schedule(int32_t keys, int32_t n, int32_t ring, bool side, bool dp,
+// dp: 0 one replica, 1 all-reduce + full AdamW, 2 sharded optimizer (reduce-scatter,
+// AdamW on this rank's rows, all-gather of the refreshed bf16 operands)
+std::vector<Op> build_schedule(int32_t keys, int32_t n, int32_t ring, bool side, int dp,
                                bool early = false) {
   need(keys >= 1 && n >= 1 && ring >= 2, TLORA_ERR_ARG, "schedule: bad sizes");
   std::vector<Op> ops;
@@ -157,7 +161,11 @@ std::vector<Op> build_schedule(int32_t keys, int32_t n, int32_t ring, bool side,
                                i > 0 ? 1 : 0, gstream == TLORA_STREAM_MAIN ? -1 : after, -1});
       grads_op.push_back(gr);
       if (i + 1 == n) {
-        if (dp) {
+        if (dp == 2) {
+          push({TLORA_OP_REDUCE_SCATTER, TLORA_STREAM_COMM, key, i, -1, -1, -1, -1, -1, 0, gr, -1});
+          push({TLORA_OP_ADAMW, TLORA_STREAM_COMM, key, i, -1, -1, -1, -1, -1, 0, -1, -1});
+          push({TLORA_OP_ALLGATHER, TLORA_STREAM_COMM, key, i, -1, -1, -1, -1, -1, 0, -1, -1});
+        } else if (dp) {
           push({TLORA_OP_ALLREDUCE, TLORA_STREAM_COMM, key, i, -1, -1, -1, -1, -1, 0, gr, -1});
           push({TLORA_OP_ADAMW, TLORA_STREAM_COMM, key, i, -1, -1, -1, -1, -1, 0, -1, -1});
         } else {
@@ -311,7 +319,8 @@ Layout& tlora_step::layout(int32_t n) {
                             &lo->plans[(size_t)i][(size_t)p]));
   }
   lo->ops = build_schedule(L * P, m.n, ring, (desc.flags & TLORA_STEP_SIDE_GRADS) != 0,
-                           comm != nullptr, (desc.flags & TLORA_STEP_EARLY_GRADS) != 0);
+                           comm == nullptr ? 0 : (desc.flags & TLORA_STEP_SHARDED_OPT) ? 2 : 1,
+                           (desc.flags & TLORA_STEP_EARLY_GRADS) != 0);
   lo->needs_event.assign(lo->ops.size(), 0);
   for (const auto& o : lo->ops)
     for (int32_t w : {o.wait0, o.wait1})
@@ -388,8 +397,20 @@ void tlora_step::enqueue(Layout& lo, int set, cudaStream_t main) {
       case TLORA_OP_ALLREDUCE:
         chk(tlora_layer_allreduce_grads(l, comm, TLORA_GROUP_DP, 0, sv));
         break;
+      case TLORA_OP_REDUCE_SCATTER:
+        chk(tlora_layer_reduce_scatter_grads(l, comm, TLORA_GROUP_DP, sv));
+        break;
+      case TLORA_OP_ALLGATHER:
+        chk(tlora_layer_allgather_operands(l, comm, TLORA_GROUP_DP, sv));
+        break;
       case TLORA_OP_ADAMW:
-        chk(tlora_layer_optimizer_step_masked(l, present, gscale, sv));
+        if (comm && (desc.flags & TLORA_STEP_SHARDED_OPT)) {
+          int64_t lo = 0, hi = 0;
+          chk(tlora_layer_dp_shard(l, comm, TLORA_GROUP_DP, &lo, &hi));
+          chk(tlora_layer_optimizer_step_rows(l, present, gscale, lo, hi, sv));
+        } else {
+          chk(tlora_layer_optimizer_step_masked(l, present, gscale, sv));
+        }
         break;
       default:
         throw StepError(TLORA_ERR_ARG, "unknown op kind");
@@ -413,7 +434,7 @@ int tlora_step_schedule_host(int32_t keys, int32_t nano, int32_t ring, int32_t s
                              int32_t data_parallel, tlora_step_op* out, int32_t cap,
                              int32_t* count) {
   return step_guard([&] {
-    const auto ops = build_schedule(keys, nano, ring, side_grads != 0, data_parallel != 0,
+    const auto ops = build_schedule(keys, nano, ring, side_grads != 0, data_parallel,
                                     side_grads == 2);
     if (count) *count = (int32_t)ops.size();
     if (out)

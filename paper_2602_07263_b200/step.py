@@ -106,7 +106,8 @@ class TrainingStep:
     def __init__(self, wl: Workload, device: int = 0, nano_fixed: int = 1, nano_init: int = 4,
                  side_grads: bool = True, graphs: bool = True, dh_ring: int = 8,
                  input_sets: int = 1, comm=None, y_dtype=torch.bfloat16, aimd_alpha: int = 4,
-                 aimd_beta: float = 0.5, aimd_tau_rel: float = 0.0, early_grads: bool | None = None):
+                 aimd_beta: float = 0.5, aimd_tau_rel: float = 0.0, early_grads: bool | None = None,
+                 sharded_opt: bool = False):
         self.wl, self.device = wl, int(device)
         self.dev = torch.device("cuda", self.device)
         self.names = [p[0] for p in wl.projections]
@@ -129,7 +130,8 @@ class TrainingStep:
             import os
             early_grads = os.environ.get("TLORA_EARLY_GRADS", "0") == "1"
         flags = ((capi.STEP_SIDE_GRADS if side_grads else 0) | (capi.STEP_GRAPH if graphs else 0)
-                 | (capi.STEP_EARLY_GRADS if early_grads and side_grads else 0))
+                 | (capi.STEP_EARLY_GRADS if early_grads and side_grads else 0)
+                 | (capi.STEP_SHARDED_OPT if sharded_opt else 0))
         desc = capi.StepDescC(self.device, wl.layers, P, a["d"], a["k"], a["inp"], S, a["ranks"],
                               a["batch"], a["seq"], capi.BF16 if y_dtype == torch.bfloat16 else capi.F32,
                               flags, dh_ring, input_sets, nano_init, nano_fixed, aimd_alpha,
@@ -255,7 +257,7 @@ class TrainingStep:
 
 
 def schedule_host(keys: int, nano: int, ring: int = 8, side_grads: bool | int = True,
-                  data_parallel: bool = False):
+                  data_parallel: bool | int = False):
     """The executor's op list for (keys, nano-batches) (host-only, no device)."""
     n = C.c_int32()
     call("tlora_step_schedule_host", keys, nano, ring, int(side_grads), int(data_parallel), None, 0,

@@ -6,7 +6,9 @@ executor's comm stream right after the key's last nano-batch, then AdamW applies
 Checks: (1) after the step, every rank's gradient buffers equal the sum over ranks of the
 gradients a communicator-less executor computes locally on the same batch (bitwise at 2
 ranks; fp32 reassociation tolerance beyond); (2) all ranks hold bitwise-identical adapters
-after two steps; (3) the replicas agree with each other on the AIMD-free N.
+after two steps; (3) the sharded optimizer (reduce-scatter, AdamW on the owned packed-row
+shard, all-gather of the bf16 operands) reproduces the all-reduce path: the next forward's
+Y and the owned rows' fp32 masters are equal (bitwise at 2 ranks).
 """
 import os
 import sys
@@ -74,6 +76,47 @@ def main():
             dist.all_gather(parts, t)
             ok &= all(torch.equal(parts[0], p) for p in parts)
     ok &= s1.nano_used == 2
+    # ---- sharded optimizer: reduce-scatter -> AdamW on this rank's packed-row shard ->
+    # all-gather of the bf16 operands; the same two steps from the same start state
+    sh = TrainingStep(wl, device=local, nano_fixed=2, graphs=True, comm=comm, sharded_opt=True)
+    sh.init_random(wl.seed + rank)
+    g0 = torch.Generator(device="cuda").manual_seed(999)
+    for key in sh.keys:
+        ls = sh.layers[key]
+        W = (torch.randn(ls.d, ls.k, generator=g0, device="cuda") * ls.d ** -0.5).bfloat16()
+        ls.set_base(W)
+        for s, r in enumerate(ls.ranks):
+            ls.set_adapter(s, torch.randn(ls.d, r, generator=g0, device="cuda") * ls.d ** -0.5,
+                           torch.randn(r, ls.k, generator=g0, device="cuda") * r ** -0.5)
+    sh.enable_optimizer(1e-3, 0.01)
+    sh.run()
+    sh.run()
+    torch.cuda.synchronize()
+    # step 2's forward read the adapters step 1 refreshed: Y equal => the all-gathered bf16
+    # operands equal the all-reduce path's (bitwise at 2 ranks, where a + b is exact-order)
+    for name in sh.names:
+        a, b = sh.Y[name], dp.Y[name]
+        ok &= bool(torch.equal(a, b)) if world == 2 else bool(
+            torch.allclose(a.float(), b.float(), rtol=2e-2, atol=2e-2))
+    # masters of the rows this rank owns == the all-reduce path's masters
+    import ctypes as C
+    from paper_2602_07263_b200 import capi
+    for key in sh.keys:
+        lay = sh.layers[key]
+        lo, hi = C.c_int64(), C.c_int64()
+        capi.call("tlora_layer_dp_shard", lay._h, comm, capi.GROUP_DP, C.byref(lo), C.byref(hi))
+        for s in range(len(lay.ranks)):
+            o, r = lay.offsets[s], lay.ranks[s]
+            cols = [c for c in range(r) if lo.value <= o + c < hi.value]
+            if not cols:
+                continue
+            Ash, Bsh = lay.read_adapter(s)
+            Aar, Bar = dp.layers[key].read_adapter(s)
+            idx = torch.tensor(cols, device="cuda")
+            same = torch.equal(Ash[:, idx], Aar[:, idx]) and torch.equal(Bsh[idx], Bar[idx])
+            ok &= bool(same) if world == 2 else bool(
+                torch.allclose(Ash[:, idx], Aar[:, idx], rtol=1e-4, atol=1e-6))
+    sh.close()
     flag = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     if rank == 0:

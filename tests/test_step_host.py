@@ -97,7 +97,14 @@ def _check_schedule(ops, keys, n, ring, side, dp, early=False):
         assert len(adam) == 1
         last_grads = idx[(capi.OP_GRADS, key, n - 1)][0]
         assert adam[0] > last_grads
-        if dp:
+        if dp == 2:  # sharded optimizer: reduce-scatter -> AdamW (own rows) -> all-gather
+            rs = [i for i, o in enumerate(ops) if o["kind"] == capi.OP_REDUCE_SCATTER and o["key"] == key]
+            ag = [i for i, o in enumerate(ops) if o["kind"] == capi.OP_ALLGATHER and o["key"] == key]
+            assert len(rs) == 1 and len(ag) == 1 and rs[0] < adam[0] < ag[0]
+            assert ops[rs[0]]["wait0"] == last_grads
+            assert ops[rs[0]]["stream"] == ops[adam[0]]["stream"] == ops[ag[0]]["stream"] == capi.STREAM_COMM
+            assert not any(o["kind"] == capi.OP_ALLREDUCE for o in ops)
+        elif dp:
             ar = [i for i, o in enumerate(ops) if o["kind"] == capi.OP_ALLREDUCE and o["key"] == key]
             assert len(ar) == 1 and ar[0] < adam[0] and ops[ar[0]]["wait0"] == last_grads
             assert ops[ar[0]]["stream"] == ops[adam[0]]["stream"] == capi.STREAM_COMM
@@ -144,7 +151,7 @@ def _check_schedule(ops, keys, n, ring, side, dp, early=False):
 def test_schedule_invariants(keys, n):
     for ring in (2, 3, 8):
         for side in (2, 1, 0):
-            for dp in (False, True):
+            for dp in (0, 1, 2):
                 ops = schedule_host(keys, n, ring, side, dp)
                 _check_schedule(ops, keys, n, ring, bool(side), dp, early=side == 2)
 
