@@ -384,30 +384,46 @@ __global__ void __launch_bounds__(256) adamw_layer_kernel(
   const int64_t r0 = row_lo + (int64_t)(b / J.blocks_x) * 32, c0 = (int64_t)(b % J.blocks_x) * 64;
   const int tid = threadIdx.x;
   const int N = (int)J.N;
+  // Both row groups' G / P / M / V float4s are loaded before any arithmetic (8 x 16 B in
+  // flight per thread). Everything but the bf16 operand copies is touched once per step and
+  // re-read only by the next step's optimizer: streaming loads / stores (evict-first), so
+  // the concurrently running fused GEMMs keep their operand panels in L2.
+  int sl[2];
+  bool on[2];
+  int64_t idx[2];
+  float4 g4[2], p4[2], m4[2], v4[2];
 #pragma unroll
   for (int it = 0; it < 2; ++it) {
     const int i = it * 16 + tid / 16, cq = (tid % 16) * 4;
     const int64_t r = r0 + i, c = c0 + cq;
+    on[it] = r < row_hi && c < N;
+    idx[it] = r * N + c;
+    sl[it] = on[it] ? row_slot[r] : -1;
+    if (on[it]) p4[it] = __ldcs(reinterpret_cast<const float4*>(J.P + idx[it]));
+    // slots absent from the step (present[sl] == 0) take no optimizer step: masters,
+    // moments and step counter unchanged (their bf16 copies are rewritten unchanged)
+    if (sl[it] >= 0 && present != nullptr && !present[sl[it]]) sl[it] = -2;
+    if (sl[it] >= 0) {
+      g4[it] = __ldcs(reinterpret_cast<const float4*>(J.G + idx[it]));
+      m4[it] = __ldcs(reinterpret_cast<const float4*>(J.M + idx[it]));
+      v4[it] = __ldcs(reinterpret_cast<const float4*>(J.V + idx[it]));
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int i = it * 16 + tid / 16, cq = (tid % 16) * 4;
     float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < row_hi && c < N) {
-      const int sl = row_slot[r];
-      const int64_t idx = r * N + c;
-      // slots absent from the step (present[sl] == 0) take no optimizer step: masters,
-      // moments and step counter unchanged (their bf16 copies are rewritten unchanged)
-      if (sl >= 0 && present != nullptr && !present[sl]) {
-        val = *reinterpret_cast<const float4*>(J.P + idx);
-      } else if (sl >= 0) {
-        const float2 h = hp[sl];  // lr, wd
-        const float t = (float)(steps[sl] + 1);
+    if (on[it]) {
+      if (sl[it] == -2) {
+        val = p4[it];
+      } else if (sl[it] >= 0) {
+        const float2 h = hp[sl[it]];  // lr, wd
+        const float t = (float)(steps[sl[it]] + 1);
         const float c1 = 1.f / (1.f - powf(b1, t)), c2 = 1.f / (1.f - powf(b2, t));
-        const float4 g4 = *reinterpret_cast<const float4*>(J.G + idx);
-        float4 p4 = *reinterpret_cast<const float4*>(J.P + idx);
-        float4 m4 = *reinterpret_cast<const float4*>(J.M + idx);
-        float4 v4 = *reinterpret_cast<const float4*>(J.V + idx);
-        const float* gp = &g4.x;
-        float* pp = &p4.x;
-        float* mp = &m4.x;
-        float* vp = &v4.x;
+        const float* gp = &g4[it].x;
+        float* pp = &p4[it].x;
+        float* mp = &m4[it].x;
+        float* vp = &v4[it].x;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float g = gp[q] * grad_scale;
@@ -419,15 +435,15 @@ __global__ void __launch_bounds__(256) adamw_layer_kernel(
           mp[q] = m;
           vp[q] = v;
         }
-        *reinterpret_cast<float4*>(J.P + idx) = p4;
-        *reinterpret_cast<float4*>(J.M + idx) = m4;
-        *reinterpret_cast<float4*>(J.V + idx) = v4;
-        val = p4;
+        __stcs(reinterpret_cast<float4*>(J.P + idx[it]), p4[it]);
+        __stcs(reinterpret_cast<float4*>(J.M + idx[it]), m4[it]);
+        __stcs(reinterpret_cast<float4*>(J.V + idx[it]), v4[it]);
+        val = p4[it];
       }
       uint2 w;
       w.x = tlora::ptx::pack_bf16x2(val.x, val.y);
       w.y = tlora::ptx::pack_bf16x2(val.z, val.w);
-      *reinterpret_cast<uint2*>(J.P16 + idx) = w;
+      *reinterpret_cast<uint2*>(J.P16 + idx[it]) = w;
     }
     tile[i][cq + 0] = val.x;
     tile[i][cq + 1] = val.y;
