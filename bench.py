@@ -151,6 +151,37 @@ class ClockSampler:
                 "window": "settle steps + timed region" if window is not None else "whole run"}
 
 
+def nvlink_bytes():
+    """NVML NVLink data counters of every visible GPU, summed over links (KiB counters x 1024):
+    {gpu index: (tx_bytes, rx_bytes)}; {} when NVML or the counters are unavailable. Sampled
+    around a timed region, the difference is the NVLink payload that region moved."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        out = {}
+        ids = [(pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, 0xFFFFFFFF),
+               (pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 0xFFFFFFFF)]
+        for i in range(pynvml.nvmlDeviceGetCount()):
+            h = pynvml.nvmlDeviceGetHandleByIndex(i)
+            v = pynvml.nvmlDeviceGetFieldValues(h, ids)
+            if v[0].nvmlReturn != 0 or v[1].nvmlReturn != 0:
+                continue
+            out[i] = (int(v[0].value.ullVal) * 1024, int(v[1].value.ullVal) * 1024)
+        return out
+    except Exception:
+        return {}
+
+
+def nvlink_delta(before, after, steps):
+    if not before or not after:
+        return None
+    per = {str(i): {"tx_bytes_per_step": (after[i][0] - before[i][0]) / steps,
+                    "rx_bytes_per_step": (after[i][1] - before[i][1]) / steps}
+           for i in after if i in before}
+    return {"source": "NVML NVLINK_THROUGHPUT_DATA_TX/RX, all links, sampled around the timed "
+                      "region (every process on the GPUs counts)", "per_gpu": per}
+
+
 def bind_host_numa(device: int):
     """Pin this process to the CPUs NVML reports as closest to `device` (NVML CPU
     affinity), so the pinned host buffers of the e2e path are first-touched on the GPU's
@@ -265,6 +296,9 @@ def run_executor(args, rank, world, local_rank):
     graph_launches = n_launch = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     traj = []
+    nv0 = nvlink_bytes() if world > 1 and rank == 0 else None
+    if world > 1:
+        dist.barrier()
     e0.record(stream)
     for i in range(args.steps):
         last = i == args.steps - 1 and os.environ.get("TLORA_BENCH_PROF", "1") != "0"
@@ -279,6 +313,7 @@ def run_executor(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    nvl = nvlink_delta(nv0, nvlink_bytes(), args.steps) if nv0 is not None else None
     cnt = (C.c_int32 * 6)()
     ms6 = (C.c_double * 6)()
     fl6 = (C.c_double * 6)()
@@ -419,6 +454,7 @@ def run_executor(args, rank, world, local_rank):
         "gpu_launches": n_launch,
         "roofline": roofline,
         "aimd": aimd,
+        "nvlink": nvl,
         "cpu_baseline": cpu,
         "cpu_baseline_oracle_f32": cpu_f32,
         "clocks": clk,
@@ -905,6 +941,8 @@ def run_tp(args, rank, world, local_rank):
     torch.cuda.synchronize()
     lib = capi.lib()
     n0 = lib.tlora_launch_count()
+    nv0 = nvlink_bytes() if rank == 0 else None
+    dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
@@ -912,6 +950,7 @@ def run_tp(args, rank, world, local_rank):
     e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
+    nvl = nvlink_delta(nv0, nvlink_bytes(), args.steps) if rank == 0 else None
     clk = clocks.stop()
     t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -971,6 +1010,7 @@ def run_tp(args, rank, world, local_rank):
         "gpu_launches": n_launch,
         "roofline": roofline,
         "pipeline_monitor": reading,
+        "nvlink": nvl,
         "clocks": clk,
     }
 
