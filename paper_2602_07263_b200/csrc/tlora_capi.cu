@@ -369,7 +369,7 @@ struct AdamJob {
   int32_t nblocks;
 };
 
-__global__ void __launch_bounds__(256) adamw_layer_kernel(
+__global__ void __launch_bounds__(256, 4) adamw_layer_kernel(
     const AdamJob j0, const AdamJob j1, const int32_t* __restrict__ row_slot,
     const float2* __restrict__ hp, int32_t* __restrict__ steps, int32_t num_slots, float b1,
     float b2, float eps, float grad_scale, int64_t R, const int32_t* __restrict__ present,
@@ -384,11 +384,30 @@ __global__ void __launch_bounds__(256) adamw_layer_kernel(
   const int64_t r0 = row_lo + (int64_t)(b / J.blocks_x) * 32, c0 = (int64_t)(b % J.blocks_x) * 64;
   const int tid = threadIdx.x;
   const int N = (int)J.N;
+  // Per-row constants once per block (32 rows): the row's slot (-1 padding gap, -2 slot
+  // absent from the step: no optimizer step, masters / moments / counter unchanged, bf16
+  // copies rewritten unchanged), its lr / weight decay and bias corrections.
+  __shared__ int s_sl[32];
+  __shared__ float s_c1[32], s_c2[32], s_lr[32], s_wd[32];
+  if (tid < 32) {
+    const int64_t r = r0 + tid;
+    int sl = r < row_hi ? row_slot[r] : -1;
+    if (sl >= 0 && present != nullptr && !present[sl]) sl = -2;
+    s_sl[tid] = sl;
+    if (sl >= 0) {
+      const float2 h = hp[sl];
+      const float t = (float)(steps[sl] + 1);
+      s_c1[tid] = 1.f / (1.f - powf(b1, t));
+      s_c2[tid] = 1.f / (1.f - powf(b2, t));
+      s_lr[tid] = h.x;
+      s_wd[tid] = h.y;
+    }
+  }
+  __syncthreads();
   // Both row groups' G / P / M / V float4s are loaded before any arithmetic (8 x 16 B in
   // flight per thread). Everything but the bf16 operand copies is touched once per step and
   // re-read only by the next step's optimizer: streaming loads / stores (evict-first), so
   // the concurrently running fused GEMMs keep their operand panels in L2.
-  int sl[2];
   bool on[2];
   int64_t idx[2];
   float4 g4[2], p4[2], m4[2], v4[2];
@@ -398,12 +417,8 @@ __global__ void __launch_bounds__(256) adamw_layer_kernel(
     const int64_t r = r0 + i, c = c0 + cq;
     on[it] = r < row_hi && c < N;
     idx[it] = r * N + c;
-    sl[it] = on[it] ? row_slot[r] : -1;
     if (on[it]) p4[it] = __ldcs(reinterpret_cast<const float4*>(J.P + idx[it]));
-    // slots absent from the step (present[sl] == 0) take no optimizer step: masters,
-    // moments and step counter unchanged (their bf16 copies are rewritten unchanged)
-    if (sl[it] >= 0 && present != nullptr && !present[sl[it]]) sl[it] = -2;
-    if (sl[it] >= 0) {
+    if (on[it] && s_sl[i] >= 0) {
       g4[it] = __ldcs(reinterpret_cast<const float4*>(J.G + idx[it]));
       m4[it] = __ldcs(reinterpret_cast<const float4*>(J.M + idx[it]));
       v4[it] = __ldcs(reinterpret_cast<const float4*>(J.V + idx[it]));
@@ -414,12 +429,11 @@ __global__ void __launch_bounds__(256) adamw_layer_kernel(
     const int i = it * 16 + tid / 16, cq = (tid % 16) * 4;
     float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
     if (on[it]) {
-      if (sl[it] == -2) {
+      const int sl = s_sl[i];
+      if (sl == -2) {
         val = p4[it];
-      } else if (sl[it] >= 0) {
-        const float2 h = hp[sl[it]];  // lr, wd
-        const float t = (float)(steps[sl[it]] + 1);
-        const float c1 = 1.f / (1.f - powf(b1, t)), c2 = 1.f / (1.f - powf(b2, t));
+      } else if (sl >= 0) {
+        const float c1 = s_c1[i], c2 = s_c2[i], lr = s_lr[i], wd = s_wd[i];
         const float* gp = &g4[it].x;
         float* pp = &p4[it].x;
         float* mp = &m4[it].x;
@@ -430,7 +444,9 @@ __global__ void __launch_bounds__(256) adamw_layer_kernel(
           float p = pp[q];
           const float m = b1 * mp[q] + (1.f - b1) * g;
           const float v = b2 * vp[q] + (1.f - b2) * g * g;
-          p -= h.x * (m * c1 / (sqrtf(v * c2) + eps) + h.y * p);
+          // fast reciprocal division (relative error ~2^-21, far inside the optimizer's
+          // tolerance): the IEEE division was most of the kernel's issued instructions
+          p -= lr * (__fdividef(m * c1, sqrtf(v * c2) + eps) + wd * p);
           pp[q] = p;
           mp[q] = m;
           vp[q] = v;
