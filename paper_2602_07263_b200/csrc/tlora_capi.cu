@@ -378,103 +378,109 @@ __global__ void __launch_bounds__(256, 4) adamw_layer_kernel(
   // rank updates only its shard); R stays the row pitch of the transposed copies
   __shared__ float tile[32][65];
   __shared__ bool last;
-  const bool second = (int)blockIdx.x >= j0.nblocks;
-  const AdamJob& J = second ? j1 : j0;
-  const int b = second ? (int)blockIdx.x - j0.nblocks : (int)blockIdx.x;
-  const int64_t r0 = row_lo + (int64_t)(b / J.blocks_x) * 32, c0 = (int64_t)(b % J.blocks_x) * 64;
-  const int tid = threadIdx.x;
-  const int N = (int)J.N;
-  // Per-row constants once per block (32 rows): the row's slot (-1 padding gap, -2 slot
-  // absent from the step: no optimizer step, masters / moments / counter unchanged, bf16
-  // copies rewritten unchanged), its lr / weight decay and bias corrections.
   __shared__ int s_sl[32];
   __shared__ float s_c1[32], s_c2[32], s_lr[32], s_wd[32];
-  if (tid < 32) {
-    const int64_t r = r0 + tid;
-    int sl = r < row_hi ? row_slot[r] : -1;
-    if (sl >= 0 && present != nullptr && !present[sl]) sl = -2;
-    s_sl[tid] = sl;
-    if (sl >= 0) {
-      const float2 h = hp[sl];
-      const float t = (float)(steps[sl] + 1);
-      s_c1[tid] = 1.f / (1.f - powf(b1, t));
-      s_c2[tid] = 1.f / (1.f - powf(b2, t));
-      s_lr[tid] = h.x;
-      s_wd[tid] = h.y;
-    }
-  }
-  __syncthreads();
-  // Both row groups' G / P / M / V float4s are loaded before any arithmetic (8 x 16 B in
-  // flight per thread). Everything but the bf16 operand copies is touched once per step and
-  // re-read only by the next step's optimizer: streaming loads / stores (evict-first), so
-  // the concurrently running fused GEMMs keep their operand panels in L2.
-  bool on[2];
-  int64_t idx[2];
-  float4 g4[2], p4[2], m4[2], v4[2];
-#pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const int i = it * 16 + tid / 16, cq = (tid % 16) * 4;
-    const int64_t r = r0 + i, c = c0 + cq;
-    on[it] = r < row_hi && c < N;
-    idx[it] = r * N + c;
-    if (on[it]) p4[it] = __ldcs(reinterpret_cast<const float4*>(J.P + idx[it]));
-    if (on[it] && s_sl[i] >= 0) {
-      g4[it] = __ldcs(reinterpret_cast<const float4*>(J.G + idx[it]));
-      m4[it] = __ldcs(reinterpret_cast<const float4*>(J.M + idx[it]));
-      v4[it] = __ldcs(reinterpret_cast<const float4*>(J.V + idx[it]));
-    }
-  }
-#pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const int i = it * 16 + tid / 16, cq = (tid % 16) * 4;
-    float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (on[it]) {
-      const int sl = s_sl[i];
-      if (sl == -2) {
-        val = p4[it];
-      } else if (sl >= 0) {
-        const float c1 = s_c1[i], c2 = s_c2[i], lr = s_lr[i], wd = s_wd[i];
-        const float* gp = &g4[it].x;
-        float* pp = &p4[it].x;
-        float* mp = &m4[it].x;
-        float* vp = &v4[it].x;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float g = gp[q] * grad_scale;
-          float p = pp[q];
-          const float m = b1 * mp[q] + (1.f - b1) * g;
-          const float v = b2 * vp[q] + (1.f - b2) * g * g;
-          // fast reciprocal division (relative error ~2^-21, far inside the optimizer's
-          // tolerance): the IEEE division was most of the kernel's issued instructions
-          p -= lr * (__fdividef(m * c1, sqrtf(v * c2) + eps) + wd * p);
-          pp[q] = p;
-          mp[q] = m;
-          vp[q] = v;
-        }
-        __stcs(reinterpret_cast<float4*>(J.P + idx[it]), p4[it]);
-        __stcs(reinterpret_cast<float4*>(J.M + idx[it]), m4[it]);
-        __stcs(reinterpret_cast<float4*>(J.V + idx[it]), v4[it]);
-        val = p4[it];
+  const int tid = threadIdx.x;
+  // persistent: a grid of a few blocks per SM walks the (32-row x 64-column) tiles of both
+  // problems, so small layers do not pay a partial second wave
+  for (int tix = blockIdx.x; tix < j0.nblocks + j1.nblocks; tix += gridDim.x) {
+    __syncthreads();  // the previous tile's shared rows / transpose tile are consumed
+    const bool second = tix >= j0.nblocks;
+    const AdamJob& J = second ? j1 : j0;
+    const int b = second ? tix - j0.nblocks : tix;
+    const int64_t r0 = row_lo + (int64_t)(b / J.blocks_x) * 32, c0 = (int64_t)(b % J.blocks_x) * 64;
+    const int N = (int)J.N;
+    // Per-row constants once per block (32 rows): the row's slot (-1 padding gap, -2 slot
+    // absent from the step: no optimizer step, masters / moments / counter unchanged, bf16
+    // copies rewritten unchanged), its lr / weight decay and bias corrections.
+    if (tid < 32) {
+      const int64_t r = r0 + tid;
+      int sl = r < row_hi ? row_slot[r] : -1;
+      if (sl >= 0 && present != nullptr && !present[sl]) sl = -2;
+      s_sl[tid] = sl;
+      if (sl >= 0) {
+        const float2 h = hp[sl];
+        const float t = (float)(steps[sl] + 1);
+        s_c1[tid] = 1.f / (1.f - powf(b1, t));
+        s_c2[tid] = 1.f / (1.f - powf(b2, t));
+        s_lr[tid] = h.x;
+        s_wd[tid] = h.y;
       }
-      uint2 w;
-      w.x = tlora::ptx::pack_bf16x2(val.x, val.y);
-      w.y = tlora::ptx::pack_bf16x2(val.z, val.w);
-      *reinterpret_cast<uint2*>(J.P16 + idx[it]) = w;
     }
-    tile[i][cq + 0] = val.x;
-    tile[i][cq + 1] = val.y;
-    tile[i][cq + 2] = val.z;
-    tile[i][cq + 3] = val.w;
-  }
-  __syncthreads();
+    __syncthreads();
+    // Both row groups' G / P / M / V float4s are loaded before any arithmetic (8 x 16 B in
+    // flight per thread). Everything but the bf16 operand copies is touched once per step and
+    // re-read only by the next step's optimizer: streaming loads / stores (evict-first), so
+    // the concurrently running fused GEMMs keep their operand panels in L2.
+    bool on[2];
+    int64_t idx[2];
+    float4 g4[2], p4[2], m4[2], v4[2];
 #pragma unroll
-  for (int it = 0; it < 4; ++it) {
-    const int cc = it * 16 + tid / 16, rr = (tid % 16) * 2;
-    const int64_t c = c0 + cc, r = r0 + rr;
-    if (c < N && r < row_hi)  // row_lo, row_hi even: r + 1 < row_hi too
-      *reinterpret_cast<uint32_t*>(J.P16t + c * R + r) =
-          tlora::ptx::pack_bf16x2(tile[rr][cc], tile[rr + 1][cc]);
+    for (int it = 0; it < 2; ++it) {
+      const int i = it * 16 + tid / 16, cq = (tid % 16) * 4;
+      const int64_t r = r0 + i, c = c0 + cq;
+      on[it] = r < row_hi && c < N;
+      idx[it] = r * N + c;
+      if (on[it]) p4[it] = __ldcs(reinterpret_cast<const float4*>(J.P + idx[it]));
+      if (on[it] && s_sl[i] >= 0) {
+        g4[it] = __ldcs(reinterpret_cast<const float4*>(J.G + idx[it]));
+        m4[it] = __ldcs(reinterpret_cast<const float4*>(J.M + idx[it]));
+        v4[it] = __ldcs(reinterpret_cast<const float4*>(J.V + idx[it]));
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int i = it * 16 + tid / 16, cq = (tid % 16) * 4;
+      float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (on[it]) {
+        const int sl = s_sl[i];
+        if (sl == -2) {
+          val = p4[it];
+        } else if (sl >= 0) {
+          const float c1 = s_c1[i], c2 = s_c2[i], lr = s_lr[i], wd = s_wd[i];
+          const float* gp = &g4[it].x;
+          float* pp = &p4[it].x;
+          float* mp = &m4[it].x;
+          float* vp = &v4[it].x;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float g = gp[q] * grad_scale;
+            float p = pp[q];
+            const float m = b1 * mp[q] + (1.f - b1) * g;
+            const float v = b2 * vp[q] + (1.f - b2) * g * g;
+            // fast reciprocal division (relative error ~2^-21, far inside the optimizer's
+            // tolerance): the IEEE division was most of the kernel's issued instructions
+            p -= lr * (__fdividef(m * c1, sqrtf(v * c2) + eps) + wd * p);
+            pp[q] = p;
+            mp[q] = m;
+            vp[q] = v;
+          }
+          __stcs(reinterpret_cast<float4*>(J.P + idx[it]), p4[it]);
+          __stcs(reinterpret_cast<float4*>(J.M + idx[it]), m4[it]);
+          __stcs(reinterpret_cast<float4*>(J.V + idx[it]), v4[it]);
+          val = p4[it];
+        }
+        uint2 w;
+        w.x = tlora::ptx::pack_bf16x2(val.x, val.y);
+        w.y = tlora::ptx::pack_bf16x2(val.z, val.w);
+        *reinterpret_cast<uint2*>(J.P16 + idx[it]) = w;
+      }
+      tile[i][cq + 0] = val.x;
+      tile[i][cq + 1] = val.y;
+      tile[i][cq + 2] = val.z;
+      tile[i][cq + 3] = val.w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int cc = it * 16 + tid / 16, rr = (tid % 16) * 2;
+      const int64_t c = c0 + cc, r = r0 + rr;
+      if (c < N && r < row_hi)  // row_lo, row_hi even: r + 1 < row_hi too
+        *reinterpret_cast<uint32_t*>(J.P16t + c * R + r) =
+            tlora::ptx::pack_bf16x2(tile[rr][cc], tile[rr + 1][cc]);
+    }
   }
+
   // ticket: every block has read steps[] before it arrives; the last one bumps them
   __syncthreads();
   if (tid == 0) {
@@ -1188,7 +1194,8 @@ void adamw_rows(tlora_layer* layer, const int32_t* present, float grad_scale, in
     job[j] = {G[j], P[j], M[j], V[j], P16[j], P16t[j], Ns[j], bx,
               bx * (int)tlora::ceil_div(rows, 32)};
   }
-  adamw_layer_kernel<<<job[0].nblocks + job[1].nblocks, 256, 0, s>>>(
+  const int grid = std::min(job[0].nblocks + job[1].nblocks, 4 * layer->sm_count);
+  adamw_layer_kernel<<<grid, 256, 0, s>>>(
       job[0], job[1], layer->row_slot.p, layer->hparams.p, layer->steps_dev.p, S, layer->beta1,
       layer->beta2, layer->eps, grad_scale, R, present, row_lo, row_hi);
   TL_CUDA(cudaGetLastError());
