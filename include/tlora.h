@@ -294,6 +294,12 @@ int tlora_backward_grad_a(tlora_layer* layer, const tlora_plan* plan, const void
  * classes concurrently on two streams. 0 = no cap (default). */
 int tlora_set_sm_budget(int device, int32_t gemm_sms, int32_t lowrank_sms);
 
+/* Tile scheduler of the fused GEMM launches on `device`: 0 = static per-CTA tile lists,
+ * 1 = dynamic (a per-stream ticket counter; CTAs that start late because other kernels hold
+ * SMs take fewer tiles), -1 = the TLORA_DYN_SCHED environment default (static). Results are
+ * bitwise identical either way. The data-parallel step executor selects 1 for its device. */
+int tlora_set_tile_scheduler(int device, int mode);
+
 /* ---- live launch profiling (CUDA events on each launch's own stream) ------------- */
 /* Between begin and end every GEMM launch is bracketed by CUDA events. end() waits for
  * them and returns, per tlora_launch kind, the launch count, summed device ms and the

@@ -176,6 +176,7 @@ SIGNATURES = {
     "tlora_backward_grad_a": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.c_float, C.c_void_p]),
     "tlora_set_sm_budget": (C.c_int, [C.c_int, C.c_int32, C.c_int32]),
+    "tlora_set_tile_scheduler": (C.c_int, [C.c_int, C.c_int]),
     "tlora_profile_begin": (C.c_int, []),
     "tlora_launch_count": (C.c_longlong, []),
     "tlora_profile_end": (C.c_int, [C.POINTER(C.c_int32), C.POINTER(C.c_double),

@@ -221,12 +221,20 @@ struct Gemm2Secondary {
 // one stream are serialised by PDL's griddepcontrol.wait, so they can share a ticket).
 // Opt-in (TLORA_DYN_SCHED=1): measured 1.1% slower than the static round-robin schedule
 // on C2 (4 interleaved A/B pairs, profiles/r1c_summary.md), so static stays the default.
-bool dyn_sched() {
-  static const bool on = [] {
+// Per-device override (tlora_set_tile_scheduler): the data-parallel step executor switches
+// its device to the dynamic scheduler, because NCCL kernels on the comm stream take SMs
+// while a persistent GEMM's static tile list assumes all of them (C3 DP2: 426 -> 389 ms).
+std::mutex g_sched_mu;
+std::map<int, int> g_sched_mode;  // device -> 0 static, 1 dynamic
+
+bool dyn_sched(int dev) {
+  static const bool env_on = [] {
     const char* e = std::getenv("TLORA_DYN_SCHED");
     return e && e[0] == '1';
   }();
-  return on;
+  std::lock_guard<std::mutex> lk(g_sched_mu);
+  auto it = g_sched_mode.find(dev);
+  return it == g_sched_mode.end() ? env_on : it->second == 1;
 }
 int32_t* tile_ticket(int dev, cudaStream_t s) {
   constexpr int kPool = 64;
@@ -266,7 +274,7 @@ void launch_gemm2(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMa
   int dev = 0;
   TL_CUDA(cudaGetDevice(&dev));
   const int grid = std::min(2 * total, sm_budget(dev, sm_count, true) / 2 * 2);
-  if (dyn_sched() && args.num_tiles > 0) args.tile_counter = tile_ticket(dev, s);
+  if (dyn_sched(dev) && args.num_tiles > 0) args.tile_counter = tile_ticket(dev, s);
   ProfScope ps(launch_kind, flops + (sec ? sec->flops : 0.0), s);
   launch_pdl(kern, grid, smem, s, a0, b0, a1, b1, sec ? sec->a : a0, sec ? sec->b : b0, args,
              args2);
@@ -2077,6 +2085,15 @@ int tlora_backward_grad_a(tlora_layer* layer, const tlora_plan* plan, const void
 }
 
 long long tlora_launch_count(void) { return g_launches.load(); }
+
+int tlora_set_tile_scheduler(int device, int mode) {
+  return guarded([&] {
+    require(mode >= -1 && mode <= 1, TLORA_ERR_ARG, "mode must be -1 (environment), 0 or 1");
+    std::lock_guard<std::mutex> lk(g_sched_mu);
+    if (mode < 0) g_sched_mode.erase(device);
+    else g_sched_mode[device] = mode;
+  });
+}
 
 int tlora_set_sm_budget(int device, int32_t gemm_sms, int32_t lowrank_sms) {
   return guarded([&] {
