@@ -329,6 +329,14 @@ def run_executor(args, rank, world, local_rank):
     tokens = wl.tokens * world
     value = tokens / (ms_per_step / 1e3)
 
+    # ---- one traced step (eager, a timing event after every op): where the step's time goes
+    # per stream, and the reference's monitor() reading (nano_pipeline.hpp:114-126) from
+    # measured per-nano-batch main-stream spans (t_comp) and comm-stream spans (t_comm)
+    step_trace = None
+    if os.environ.get("TLORA_BENCH_TRACE", "1") != "0":
+        s_ = st.run(stream=stream, trace=True)
+        step_trace = trace_summary(st.trace(), s_.ms)
+
     # ---- the AIMD-driven executor on the same workload (after the timed region): N chosen
     # every step by the reference's controller from the measured step time
     aimd = None
@@ -454,11 +462,42 @@ def run_executor(args, rank, world, local_rank):
         "gpu_launches": n_launch,
         "roofline": roofline,
         "aimd": aimd,
+        "step_trace": step_trace,
         "nvlink": nvl,
         "cpu_baseline": cpu,
         "cpu_baseline_oracle_f32": cpu_f32,
         "clocks": clk,
     }
+
+
+def trace_summary(trace, step_ms):
+    """Per-stream end times of a traced executor step and monitor()'s reading from measured
+    per-nano-batch spans: t_comp[i] = main-stream span of nano-batch i, t_comm[i] = span of
+    its comm-stream ops (0 for one replica)."""
+    from paper_2602_07263_b200 import capi
+    from paper_2602_07263_b200.layer import monitor
+    ends = {}
+    for op, ms in trace:
+        ends[op["stream"]] = max(ends.get(op["stream"], 0.0), ms)
+    nanos = sorted({op["nano"] for op, _ in trace if op["nano"] >= 0})
+    t_comp, t_comm, prev = [], [], 0.0
+    for i in nanos:
+        main = [ms for op, ms in trace if op["nano"] == i and op["stream"] == capi.STREAM_MAIN]
+        comm = [ms for op, ms in trace if op["nano"] == i and op["stream"] == capi.STREAM_COMM]
+        end = max(main) if main else prev
+        t_comp.append((end - prev) / 1e3)
+        t_comm.append(((max(comm) - end) if comm and max(comm) > end else 0.0) / 1e3)
+        prev = end
+    analytic = max(sum(t_comp), sum(t_comm))
+    eta, stall = monitor(t_comp, t_comm, step_ms / 1e3, analytic, num_stages=1)
+    names = {capi.STREAM_MAIN: "main", capi.STREAM_SIDE: "side", capi.STREAM_COMM: "comm"}
+    return {"step_ms": round(step_ms, 3),
+            "stream_end_ms": {names[k]: round(v, 3) for k, v in sorted(ends.items())},
+            "t_comp_ms": [round(x * 1e3, 3) for x in t_comp],
+            "t_comm_ms": [round(x * 1e3, 3) for x in t_comm],
+            "monitor": {"eta_util": round(eta, 4), "delta_stall_ms": round(stall * 1e3, 3)},
+            "note": "eager traced step (an event after every op); the step ends on the main "
+                    "stream after the side / comm streams"}
 
 
 def roofline_block(cnt, ms6, fl6, timing):

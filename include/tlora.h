@@ -398,7 +398,10 @@ enum tlora_step_flags {
   TLORA_STEP_SHARDED_OPT = 8  /* with a communicator: reduce-scatter the gradients, AdamW on
                                  this rank's row shard, all-gather the bf16 operands         */
 };
-enum tlora_run_flags { TLORA_RUN_EAGER = 1 /* launch eagerly even if a graph exists */ };
+enum tlora_run_flags {
+  TLORA_RUN_EAGER = 1, /* launch eagerly even if a graph exists                          */
+  TLORA_RUN_TRACE = 2  /* eager, with a timing event after every op (tlora_step_trace)   */
+};
 typedef struct tlora_step_desc {
   int32_t device;
   int32_t num_layers;
@@ -457,6 +460,12 @@ int tlora_step_next_n(const tlora_step* step, int32_t* n);
  * feeds AIMD). stats may be NULL. */
 int tlora_step_run(tlora_step* step, int32_t set, int32_t flags, void* stream,
                    tlora_step_stats* stats);
+
+/* After a TLORA_RUN_TRACE step: its ops (schedule order) and each op's completion time on
+ * its own stream in ms after the step's start event (ops, end_ms: cap entries; NULL ok). */
+typedef struct tlora_step_op tlora_step_op;
+int tlora_step_trace(const tlora_step* step, tlora_step_op* ops, double* end_ms, int32_t cap,
+                     int32_t* count);
 
 /* One op of the step schedule (host-only view for tests and drivers). */
 enum tlora_op_kind { TLORA_OP_SHRINK = 0, TLORA_OP_FWD = 1, TLORA_OP_DH = 2, TLORA_OP_DX = 3,

@@ -67,7 +67,7 @@ class StepOpC(C.Structure):
 
 
 STEP_SIDE_GRADS, STEP_GRAPH, STEP_EARLY_GRADS, STEP_SHARDED_OPT = 1, 2, 4, 8
-RUN_EAGER = 1
+RUN_EAGER, RUN_TRACE = 1, 2
 BUF_X, BUF_DY, BUF_Y, BUF_DX, BUF_H = range(5)
 OP_SHRINK, OP_FWD, OP_DH, OP_DX, OP_GRADS, OP_ALLREDUCE, OP_ADAMW, OP_REDUCE_SCATTER, OP_ALLGATHER = range(9)
 STREAM_MAIN, STREAM_SIDE, STREAM_COMM = range(3)
@@ -206,6 +206,8 @@ SIGNATURES = {
                                             C.c_double, C.c_double]),
     "tlora_step_run": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                  C.POINTER(StepStatsC)]),
+    "tlora_step_trace": (C.c_int, [C.c_void_p, C.POINTER(StepOpC), C.POINTER(C.c_double),
+                                   C.c_int32, C.POINTER(C.c_int32)]),
     "tlora_step_schedule_host": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                            C.POINTER(StepOpC), C.c_int32, C.POINTER(C.c_int32)]),
     "tlora_aimd_step": (C.c_int, [C.POINTER(C.c_int32), C.POINTER(C.c_int32),

@@ -250,7 +250,12 @@ struct tlora_step {
     return (char*)dH + ((size_t)slot * T + row) * R * 2;
   }
   Layout& layout(int32_t n);
-  void enqueue(Layout& lo, int set, cudaStream_t main);
+  void enqueue(Layout& lo, int set, cudaStream_t main, bool trace = false);
+  // trace of the last TLORA_RUN_TRACE step: per op its stream and end time (ms after the
+  // step's start event)
+  std::vector<cudaEvent_t> trace_ev;
+  std::vector<Op> trace_ops;
+  std::vector<double> trace_ms;
 };
 
 tlora_step::~tlora_step() {
@@ -262,6 +267,7 @@ tlora_step::~tlora_step() {
   }
   for (auto* l : layers) tlora_layer_destroy(l);
   for (auto e : events) cudaEventDestroy(e);
+  for (auto e : trace_ev) cudaEventDestroy(e);
   for (auto e : {t_begin, t_end, ev_side, ev_comm, ev_in})
     if (e) cudaEventDestroy(e);
   if (exec) cudaStreamDestroy(exec);
@@ -335,7 +341,13 @@ Layout& tlora_step::layout(int32_t n) {
   return ref;
 }
 
-void tlora_step::enqueue(Layout& lo, int set, cudaStream_t main) {
+void tlora_step::enqueue(Layout& lo, int set, cudaStream_t main, bool trace) {
+  if (trace)
+    while (trace_ev.size() < lo.ops.size()) {
+      cudaEvent_t e;
+      ST_CUDA(cudaEventCreate(&e));
+      trace_ev.push_back(e);
+    }
   const cudaStream_t streams[3] = {main, side ? side : main, comm_s ? comm_s : main};
   const int y_dt = desc.y_dtype;
   const float gscale = 1.0f / (float)dp;
@@ -416,6 +428,7 @@ void tlora_step::enqueue(Layout& lo, int set, cudaStream_t main) {
         throw StepError(TLORA_ERR_ARG, "unknown op kind");
     }
     if (lo.needs_event[idx]) ST_CUDA(cudaEventRecord(events[idx], s));
+    if (trace) ST_CUDA(cudaEventRecord(trace_ev[idx], s));
   }
   // join: the step ends on the main stream after the side / comm work
   if (side) {
@@ -664,6 +677,21 @@ int tlora_step_layout(tlora_step* step, int32_t n, int32_t* n_out, int64_t* nano
   });
 }
 
+int tlora_step_trace(const tlora_step* step, tlora_step_op* ops, double* end_ms, int32_t cap,
+                     int32_t* count) {
+  return step_guard([&] {
+    need(step != nullptr, TLORA_ERR_ARG, "step is null");
+    const auto& o = step->trace_ops;
+    if (count) *count = (int32_t)o.size();
+    for (size_t i = 0; i < o.size() && (int32_t)i < cap; ++i) {
+      if (ops)
+        ops[i] = {o[i].kind, o[i].stream, o[i].key, o[i].nano, o[i].slot, o[i].sec_kind,
+                  o[i].sec_key, o[i].sec_nano, o[i].sec_slot, o[i].beta, o[i].wait0, o[i].wait1};
+      if (end_ms) end_ms[i] = step->trace_ms[i];
+    }
+  });
+}
+
 int tlora_step_set_controller(tlora_step* step, int32_t nano_fixed, int32_t nano_init,
                               int32_t aimd_alpha, double aimd_beta, double aimd_tau_rel) {
   return step_guard([&] {
@@ -723,21 +751,31 @@ int tlora_step_run(tlora_step* step, int32_t set, int32_t flags, void* stream,
       ST_CUDA(cudaMemsetAsync(st.dH, 0, (size_t)st.ring * st.T * st.R * 2, main));
       st.zeroed_for = n;
     }
+    const bool trace = (flags & TLORA_RUN_TRACE) != 0;
     const bool graphs = (st.desc.flags & TLORA_STEP_GRAPH) && st.comm == nullptr &&
-                        !(flags & TLORA_RUN_EAGER);
+                        !(flags & (TLORA_RUN_EAGER | TLORA_RUN_TRACE));
     const long long l0 = tlora_launch_count();
     bool replayed = false;
     if (graphs && lo.graph[set] != nullptr) {
       ST_CUDA(cudaGraphLaunch(lo.graph[set], main));
       replayed = true;
     } else {
-      st.enqueue(lo, set, main);
+      st.enqueue(lo, set, main, trace);
     }
     ST_CUDA(cudaEventRecord(st.t_end, main));
     ST_CUDA(cudaStreamWaitEvent(caller, st.t_end, 0));  // and the caller's stream after it
     ST_CUDA(cudaEventSynchronize(st.t_end));
     float ms = 0.f;
     ST_CUDA(cudaEventElapsedTime(&ms, st.t_begin, st.t_end));
+    if (trace) {
+      st.trace_ops = lo.ops;
+      st.trace_ms.assign(lo.ops.size(), 0.0);
+      for (size_t i = 0; i < lo.ops.size(); ++i) {
+        float t = 0.f;
+        ST_CUDA(cudaEventElapsedTime(&t, st.t_begin, st.trace_ev[i]));
+        st.trace_ms[i] = t;
+      }
+    }
     if (!replayed) lo.launches = tlora_launch_count() - l0;
     const long long launches = lo.launches;
     if (graphs && !replayed) {

@@ -211,10 +211,11 @@ class TrainingStep:
         self.lrs, self.weight_decay = lrs, weight_decay
 
     # ---- execution
-    def run(self, input_set: int = 0, eager: bool = False, stream=None) -> StepStats:
+    def run(self, input_set: int = 0, eager: bool = False, stream=None,
+            trace: bool = False) -> StepStats:
         st = capi.StepStatsC()
-        call("tlora_step_run", self._h, int(input_set), capi.RUN_EAGER if eager else 0,
-             _stream_ptr(stream), C.byref(st))
+        flags = (capi.RUN_EAGER if eager else 0) | (capi.RUN_TRACE if trace else 0)
+        call("tlora_step_run", self._h, int(input_set), flags, _stream_ptr(stream), C.byref(st))
         s = StepStats(st.nano_used, st.next_nano, st.ms, bool(st.replayed_graph), st.launches,
                       st.tokens)
         self.trajectory.append((s.nano_used, s.ms))
@@ -225,6 +226,16 @@ class TrainingStep:
         """nano_fixed > 0 pins N; 0 = AIMD from nano_init with a fresh controller state."""
         call("tlora_step_set_controller", self._h, int(nano_fixed), int(nano_init), int(alpha),
              float(beta), float(tau_rel))
+
+    def trace(self):
+        """[(op dict, end_ms)] of the last run(trace=True) step, schedule order."""
+        n = C.c_int32()
+        call("tlora_step_trace", self._h, None, None, 0, C.byref(n))
+        ops = (capi.StepOpC * max(1, n.value))()
+        ms = (C.c_double * max(1, n.value))()
+        call("tlora_step_trace", self._h, ops, ms, n.value, C.byref(n))
+        return [({f: getattr(o, f) for f, _ in capi.StepOpC._fields_}, ms[i])
+                for i, o in enumerate(ops[: n.value])]
 
     def next_n(self) -> int:
         n = C.c_int32()

@@ -222,3 +222,28 @@ def test_executor_data_parallel_multi_gpu():
                        capture_output=True, text=True, timeout=600)
     print(p.stdout[-3000:])
     assert p.returncode == 0 and "STEP_DP_CHECK PASS" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+def test_traced_step_timeline():
+    """TLORA_RUN_TRACE: every op of the schedule gets its completion time on its own stream;
+    times are ordered along each stream, cross-stream waits are respected (a GRADS op ends
+    after the dX launch it waited for), and nothing ends after the step's end event."""
+    from paper_2602_07263_b200 import capi
+    ex = TrainingStep(MINI, device=0, nano_fixed=2, graphs=True)
+    ex.init_random(MINI.seed)
+    ex.enable_optimizer()
+    ex.run()
+    s = ex.run(trace=True)
+    assert not s.replayed_graph
+    tr = ex.trace()
+    assert len(tr) == len(ex.layers) * 2 * 2 + 1 + len(ex.layers) * 2 + len(ex.layers)
+    last = {}
+    for i, (op, ms) in enumerate(tr):
+        assert 0.0 < ms <= s.ms + 1e-3
+        if op["stream"] in last:
+            assert ms >= last[op["stream"]] - 1e-3
+        last[op["stream"]] = ms
+        for w in (op["wait0"], op["wait1"]):
+            if w >= 0:
+                assert ms >= tr[w][1] - 1e-3
+    assert {op["stream"] for op, _ in tr} == {capi.STREAM_MAIN, capi.STREAM_SIDE}
