@@ -41,3 +41,18 @@ def test_clock_window_too_small_falls_back_to_all():
     cs = _sampler_with(rows)
     out = cs.stop(window=(103.5, 104.5))  # 1 sample inside: use all 5
     assert out["samples"] == 5 and out["sm_mhz"] == 1400
+
+
+def test_trace_summary_monitor_reading():
+    """bench.trace_summary: per-stream end times and the reference monitor() reading
+    (nano_pipeline.hpp:114-126) from per-nano-batch main / comm spans of a traced step."""
+    from paper_2602_07263_b200 import capi
+    op = lambda kind, stream, nano: {"kind": kind, "stream": stream, "nano": nano}  # noqa: E731
+    trace = [(op(capi.OP_SHRINK, capi.STREAM_MAIN, 0), 0.1), (op(capi.OP_FWD, capi.STREAM_MAIN, 0), 2.0),
+             (op(capi.OP_GRADS, capi.STREAM_SIDE, 0), 2.5), (op(capi.OP_FWD, capi.STREAM_MAIN, 1), 5.0),
+             (op(capi.OP_ALLREDUCE, capi.STREAM_COMM, 1), 6.0), (op(capi.OP_ADAMW, capi.STREAM_COMM, 1), 6.5)]
+    out = bench.trace_summary(trace, 7.0)
+    assert out["stream_end_ms"] == {"main": 5.0, "side": 2.5, "comm": 6.5}
+    assert out["t_comp_ms"] == [2.0, 3.0] and out["t_comm_ms"] == [0.0, 1.5]
+    # eta = sum(t_comp) / (1 * t_iter) ; stall = t_iter - max(sum t_comp, sum t_comm)
+    assert out["monitor"] == {"eta_util": round(5.0 / 7.0, 4), "delta_stall_ms": 2.0}
