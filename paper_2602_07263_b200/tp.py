@@ -106,7 +106,6 @@ class TPLayerSetStep:
             _call("tlora_set_tile_scheduler", device, 1)
         # adapter-gradient launches (HBM-bound) run on their own stream, overlapping the
         # fused GEMMs of the compute stream (as runner.LayerSetStep.enable_side_grads)
-        import os
         self.gside = (torch.cuda.Stream(self.dev) if os.environ.get("TLORA_TP_SIDE_GRADS", "1") != "0"
                       else self.compute)
         seed = wl.seed if seed is None else seed
