@@ -535,9 +535,12 @@ int tlora_step_create(const tlora_step_desc* desc, tlora_comm* comm, tlora_step*
       chk(tlora_comm_info(comm, &w, &r, &tp, &dpn));
       need(tp == 1, TLORA_ERR_ARG, "the step executor runs data-parallel replicas (tp_size 1)");
       st->dp = dpn;
-      // NCCL kernels on the comm stream take SMs from the persistent fused GEMMs: dynamic
-      // tile scheduling keeps those GEMMs balanced (unless TLORA_DYN_SCHED says otherwise)
-      if (!std::getenv("TLORA_DYN_SCHED")) chk(tlora_set_tile_scheduler(D.device, 1));
+      // NCCL kernels on the comm stream take SMs from the persistent fused GEMMs: for layer
+      // stacks (hundreds of per-key all-reduces per step) dynamic tile scheduling keeps the
+      // GEMMs balanced (C3 8 layers DP2: 426 -> 389 ms); a single layer set measured 3%
+      // better with the static lists (C2 DP2, 2 interleaved pairs). TLORA_DYN_SCHED overrides.
+      if (!std::getenv("TLORA_DYN_SCHED") && D.num_layers > 1)
+        chk(tlora_set_tile_scheduler(D.device, 1));
     }
     int prev = -1;
     ST_CUDA(cudaGetDevice(&prev));
