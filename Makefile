@@ -39,6 +39,7 @@ $(CPPTEST): tests/cpp/test_dropin.cpp include/lora_fleet/*.hpp include/tlora.h $
 OBJDIR   := build
 CAPI_O   := $(OBJDIR)/tlora_capi.o
 STEP_O   := $(OBJDIR)/tlora_step.o
+TP_O     := $(OBJDIR)/tlora_tp.o
 
 $(CAPI_O): $(CSRC)/tlora_capi.cu $(CSRC)/tlora_comm.cuh $(CSRC)/lora_gemm2.cuh $(CSRC)/lora_grad.cuh $(CSRC)/lora_gemm.cuh $(CSRC)/sm100_ptx.cuh $(CSRC)/tlora_plan.hpp include/tlora.h
 	mkdir -p $(OBJDIR)
@@ -49,8 +50,13 @@ $(STEP_O): $(CSRC)/tlora_step.cu $(CSRC)/tlora_nano.hpp include/tlora.h
 	mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/tlora_step.cu
 
-$(LIB): $(CAPI_O) $(STEP_O)
-	$(NVCC) $(ARCH) -shared -o $@ $(CAPI_O) $(STEP_O)
+# host-side tensor-parallel step: its own translation unit
+$(TP_O): $(CSRC)/tlora_tp.cu $(CSRC)/tlora_nano.hpp include/tlora.h
+	mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c -o $@ $(CSRC)/tlora_tp.cu
+
+$(LIB): $(CAPI_O) $(STEP_O) $(TP_O)
+	$(NVCC) $(ARCH) -shared -o $@ $(CAPI_O) $(STEP_O) $(TP_O)
 
 $(ORACLE): oracle/tlora_oracle.c oracle/tlora_oracle.h
 	$(CC) -O3 -march=x86-64-v3 -fopenmp -fPIC -shared -std=c11 -o $@ oracle/tlora_oracle.c -lm
@@ -59,6 +65,6 @@ ref:
 	$(MAKE) -C oracle ref
 
 clean:
-	rm -f $(LIB) $(ORACLE) $(CPPTEST) $(STEPMAIN) $(COSTMAIN) $(CAPI_O) $(STEP_O) build_ptxas.log
+	rm -f $(LIB) $(ORACLE) $(CPPTEST) $(STEPMAIN) $(COSTMAIN) $(CAPI_O) $(STEP_O) $(TP_O) build_ptxas.log
 
 .PHONY: all clean ref

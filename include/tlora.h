@@ -487,6 +487,62 @@ int tlora_step_schedule_host(int32_t keys, int32_t nano, int32_t ring, int32_t s
                              int32_t data_parallel, tlora_step_op* out, int32_t cap,
                              int32_t* count);
 
+/* ---- tensor-parallel layer-set step (C++ host; the TP path of SURVEY §8(e)) ------------
+ * One process per GPU, the communicator's world = the TP group. Column-parallel projections
+ * (q, k, v, gate, up: proj_row_parallel 0) hold W[:, k/P], B_j[:, k/P] and the replicated
+ * A_j; row-parallel ones (o, down: 1) hold W[d/P, :], A_j[d/P, :] and the replicated B_j.
+ * Sequence-parallel activations between groups. Per nano-batch (rank-aware map, AIMD as
+ * tlora_step_run): shrink on the SP shard -> all-gather [X | H] -> column GEMMs; row GEMMs
+ * -> reduce-scatter Y (fused into the GEMM epilogue over NVLink peer memory with
+ * TLORA_TP_FUSED_RS); backward all-gather dY (row), reduce-scatter [dX | dH] (column);
+ * the replicated adapter halves' gradients are all-reduced once per step; masked AdamW.
+ * Collectives of nano n+1 / n-1 run on a comm stream while nano n's GEMMs run; with
+ * TLORA_TP_COPY_ENGINE the all-gathers / reduce-scatters are copy-engine pushes into
+ * peer-mapped (CUDA IPC) buffers with stream-memory-op flags instead of NCCL kernels. */
+typedef struct tlora_tp_step tlora_tp_step;
+enum tlora_tp_flags {
+  TLORA_TP_FUSED_RS = 1,     /* row-parallel reduce-scatter fused into the GEMM epilogue  */
+  TLORA_TP_COPY_ENGINE = 2,  /* all-gather / reduce-scatter by copy-engine push            */
+  TLORA_TP_SIDE_GRADS = 4    /* adapter-gradient launches on a side stream                 */
+};
+typedef struct tlora_tp_desc {
+  int32_t device;
+  int32_t num_projections;
+  const int64_t* proj_d;             /* [P] full in-features                             */
+  const int64_t* proj_k;             /* [P] full out-features                            */
+  const int32_t* proj_input;         /* [P] input group of the column-parallel projections */
+  const int32_t* proj_row_parallel;  /* [P] 1 = row-parallel, 0 = column-parallel        */
+  int32_t num_slots;
+  const int32_t* ranks;
+  const int32_t* batch;
+  const int32_t* seq_len;
+  int32_t flags;                     /* tlora_tp_flags                                    */
+  int32_t nano_init, nano_fixed, aimd_alpha;
+  double aimd_beta, aimd_tau_rel;
+} tlora_tp_desc;
+enum tlora_tp_buffer_kind {
+  TLORA_TP_X_SHARD = 0,   /* index = input group: T/P x d   (column inputs, SP shard)   */
+  TLORA_TP_X_LOC = 1,     /* index = projection (row): T x d/P                           */
+  TLORA_TP_DY = 2,        /* index = projection (column): T x k/P                        */
+  TLORA_TP_DY_SHARD = 3,  /* index = projection (row): T/P x k                           */
+  TLORA_TP_Y = 4,         /* index = projection (column): T x k/P                        */
+  TLORA_TP_Y_SHARD = 5,   /* index = projection (row): T/P x k                           */
+  TLORA_TP_DX_SHARD = 6,  /* index = input group: T/P x d (summed over the group)        */
+  TLORA_TP_DX_LOC = 7     /* index = projection (row): T x d/P                           */
+};
+int tlora_tp_create(const tlora_tp_desc* desc, tlora_comm* comm, tlora_tp_step** out);
+int tlora_tp_destroy(tlora_tp_step* step);
+/* This rank's shard layer of projection p (set base / adapters / optimizer through it). */
+int tlora_tp_layer(tlora_tp_step* step, int32_t proj, tlora_layer** out);
+int tlora_tp_buffer(tlora_tp_step* step, int32_t kind, int32_t index, void** ptr, int64_t* rows,
+                    int64_t* cols);
+/* nano_t0[n_out + 1] (global token rows) and nano_slot[n_out x S] of nano count n. */
+int tlora_tp_layout(tlora_tp_step* step, int32_t n, int32_t* n_out, int64_t* nano_t0,
+                    int32_t* nano_slot);
+/* One training step (collective: every rank calls it); waits for its CUDA-event time,
+ * averaged over the group before the AIMD update (so all ranks agree on the next N). */
+int tlora_tp_run(tlora_tp_step* step, int32_t flags, void* stream, tlora_step_stats* stats);
+
 /* Sharded data-parallel optimizer (the alternative to tlora_layer_allreduce_grads + a full
  * AdamW on every rank): the packed rank rows are split evenly over `group`; this rank owns
  * [row_lo, row_hi). reduce_scatter_grads sums the fp32 gradients of the owned rows over the

@@ -210,6 +210,14 @@ SIGNATURES = {
                                    C.c_int32, C.POINTER(C.c_int32)]),
     "tlora_step_schedule_host": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                            C.POINTER(StepOpC), C.c_int32, C.POINTER(C.c_int32)]),
+    "tlora_tp_create": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "tlora_tp_destroy": (C.c_int, [C.c_void_p]),
+    "tlora_tp_layer": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    "tlora_tp_buffer": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p),
+                                  C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "tlora_tp_layout": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_void_p,
+                                  C.c_void_p]),
+    "tlora_tp_run": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(StepStatsC)]),
     "tlora_aimd_step": (C.c_int, [C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                   C.POINTER(C.c_double), C.c_int32, C.c_double, C.c_double,
                                   C.c_double]),

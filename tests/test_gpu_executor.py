@@ -247,3 +247,21 @@ def test_traced_step_timeline():
             if w >= 0:
                 assert ms >= tr[w][1] - 1e-3
     assert {op["stream"] for op, _ in tr} == {capi.STREAM_MAIN, capi.STREAM_SIDE}
+
+
+def test_tp_executor_matches_python_tp_driver_multi_gpu():
+    """tests/tp_exec_check.py under torchrun (>= 2 GPUs): the C++ TP step == the Python TP
+    driver (bitwise activations, gradients within fp32 reassociation)."""
+    import socket
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs (run via gpurun --gpus 2)")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    n = min(torch.cuda.device_count(), 4)
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), str(ROOT / "tests" / "tp_exec_check.py")],
+                       capture_output=True, text=True, timeout=900)
+    print(p.stdout[-3000:])
+    assert p.returncode == 0 and "TP_EXEC_CHECK PASS" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
