@@ -230,7 +230,7 @@ def ref_tokens_per_job(wl, threads: int, per_thread: int = 64) -> int:
 
 
 # ------------------------------------------------------------------------------ GPU arm
-def make_comm(local_rank, rank, world):
+def make_comm(local_rank, rank, world, tp_size=1):
     """tlora_comm (NCCL through the C-ABI) for the executor's data-parallel all-reduce: rank 0
     makes the unique id, torch.distributed broadcasts it (host plumbing only)."""
     import ctypes as C
@@ -245,7 +245,7 @@ def make_comm(local_rank, rank, world):
     dist.broadcast(uid, 0)
     idb = (C.c_uint8 * capi.UNIQUE_ID_BYTES)(*uid.cpu().tolist())
     h = C.c_void_p()
-    capi.call("tlora_comm_create", local_rank, idb, world, rank, 1, C.byref(h))
+    capi.call("tlora_comm_create", local_rank, idb, world, rank, tp_size, C.byref(h))
     return h
 
 
@@ -1054,6 +1054,76 @@ def run_tp(args, rank, world, local_rank):
     }
 
 
+def run_tp_exec(args, rank, world, local_rank):
+    """Tensor-parallel layer set through the C++ TP step (tlora_tp_*): one layer of the
+    configured model (C4 by default) split over the torchrun group, per-nano-batch
+    copy-engine all-gathers / reduce-scatters and the fused GEMM + reduce-scatter over
+    NVLink, N chosen by AIMD every step (--nano-batches 0) or fixed. Strong scaling: the
+    global token batch is fixed, value = global tokens / step time (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_07263_b200 import capi
+    from paper_2602_07263_b200.tp_step import TPExecutor
+    from paper_2602_07263_b200.workload import config
+
+    torch.cuda.set_device(local_rank)
+    wl = config(args.config)
+    comm = make_comm(local_rank, rank, world, tp_size=world)
+    # TP default: AIMD every step (the nano-batches hide the boundary traffic); an explicit
+    # --nano-batches N pins N
+    nano_fixed = max(0, args.nano_batches) if "--nano-batches" in sys.argv else 0
+    args.nano_batches = nano_fixed
+    ex = TPExecutor(wl, rank, world, local_rank, comm, nano_fixed=nano_fixed,
+                    nano_init=args.nano, fused_rs=args.fused_rs != "none",
+                    copy_engine=os.environ.get("TLORA_TP_CE_AG", "1") != "0")
+    ex.enable_optimizer()
+    stream = torch.cuda.current_stream()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    clocks.wait_ready()
+    for _ in range(args.warmup):
+        ex.run(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    nv0 = nvlink_bytes() if rank == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    traj, launches = [], 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        s_ = ex.run(stream)
+        traj.append([s_.nano_used, round(s_.ms, 3)])
+        launches += s_.launches
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    nvl = nvlink_delta(nv0, nvlink_bytes(), args.steps) if rank == 0 else None
+    clk = clocks.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = t.item() / args.steps
+    flops = wl.flops_fwd_bwd() / wl.layers
+    return {
+        "metric": METRIC, "value": round(wl.tokens / (ms_per_step / 1e3), 1), "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded normal activations/grads, random-init W and adapters)",
+        "config": {"workload": f"{wl.name}: {wl.notes} (one layer of the stack per step)",
+                   "tokens_global": wl.tokens, "parallelism": f"tp{world}",
+                   "driver": "C++ tensor-parallel step (tlora_tp_run: libtlora.so)",
+                   "row_parallel_reduce_scatter": "fused GEMM epilogue -> NVLink peer slots"
+                   if args.fused_rs != "none" else "copy engine / NCCL",
+                   "nano_batches": ("AIMD every step" if args.nano_batches <= 0
+                                    else f"fixed N={args.nano_batches}"),
+                   "aimd_trajectory_n_ms": traj,
+                   "algorithmic_tflop_per_step": round(flops / 1e12, 3),
+                   "achieved_tflops_aggregate": round(flops / (ms_per_step / 1e3) / 1e12, 1)},
+        "gpu_launches": int(launches),
+        "nvlink": nvl,
+        "clocks": clk,
+    }
+
+
 def run_reference(args, rank, world):
     """Reference arm: the reference's own CPU implementation of the path (oracle/_ref/
     ref_bench: unmodified fused_forward for fwd and dX, shim GEMM for dA/dB) on all host
@@ -1119,6 +1189,8 @@ def main():
     ap.add_argument("--tp", action="store_true",
                     help="tensor-parallel layer set over the torchrun group (default config C4)")
     ap.add_argument("--nano", type=int, default=4, help="initial nano-batch count (TP mode)")
+    ap.add_argument("--tp-driver", default="cpp", choices=["cpp", "python"],
+                    help="--tp: the C++ TP step (default) or round 1's Python TP driver")
     ap.add_argument("--driver", default="cpp", choices=["cpp", "python"],
                     help="cpp: the C++ step executor (default); python: runner.LayerSetStep")
     ap.add_argument("--host", default="python", choices=["python", "cpp"],
@@ -1180,6 +1252,8 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.host == "cpp":
         out = run_cpp_host(args)
+    elif args.tp and args.tp_driver == "cpp":
+        out = run_tp_exec(args, rank, world, local_rank)
     elif args.tp:
         out = run_tp(args, rank, world, local_rank)
     elif args.driver == "python" or args.shuffle or args.overlap != 0:

@@ -29,7 +29,7 @@ def main():
     nano = int(os.environ.get("TP_NANO", "3"))
     py = TPLayerSetStep(wl, rank, world, local, nano=nano, fused_rs=True)
     py.enable_optimizer()
-    comm = bench.make_comm(local, rank, world)
+    comm = bench.make_comm(local, rank, world, tp_size=world)
     ex = TPExecutor(wl, rank, world, local, comm, nano_fixed=nano, fused_rs=True, copy_engine=True)
     ex.enable_optimizer()
     py.step(nano)
