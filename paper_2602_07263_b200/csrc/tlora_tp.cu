@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -746,17 +748,23 @@ int tlora_tp_run(tlora_tp_step* step, int32_t flags, void* stream, tlora_step_st
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(stream);
     const int32_t n_use = st.desc.nano_fixed > 0 ? std::min(st.desc.nano_fixed, st.total_samples)
                                                  : st.aimd_n;
+    using clk = std::chrono::steady_clock;
+    const auto h0 = clk::now();
     Layout& lo = st.layout(n_use);
     st.ev_next = 0;
     st.wait(st.main, caller);
     const long long l0 = tlora_launch_count();
     TP_CUDA(cudaEventRecord(st.t_begin, st.main));
+    const auto h1 = clk::now();
     st.forward(lo);
+    const auto h2 = clk::now();
     st.backward(lo);
     for (auto* l : st.layers) chk(tlora_layer_optimizer_step_masked(l, st.present, 1.f, st.main));
     TP_CUDA(cudaEventRecord(st.t_end, st.main));
     st.wait(caller, st.main);
+    const auto h3 = clk::now();
     TP_CUDA(cudaEventSynchronize(st.t_end));
+    const auto h4 = clk::now();
     float ms = 0.f;
     TP_CUDA(cudaEventElapsedTime(&ms, st.t_begin, st.t_end));
     // the group's mean step time: every rank feeds the same value to AIMD, so all ranks
@@ -767,6 +775,12 @@ int tlora_tp_run(tlora_tp_step* step, int32_t flags, void* stream, tlora_step_st
     TP_CUDA(cudaMemcpyAsync(&msd, st.ms_dev, sizeof msd, cudaMemcpyDeviceToHost, st.main));
     TP_CUDA(cudaStreamSynchronize(st.main));
     const double t_group = msd / 1e3;
+    if (std::getenv("TLORA_TP_DEBUG")) {
+      auto ms_ = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "[tlora_tp rank %d] layout+wait %.3f fwd-enqueue %.3f bwd-enqueue %.3f "
+                   "sync %.3f aimd %.3f device %.3f ms\n", st.rank, ms_(h0, h1), ms_(h1, h2),
+                   ms_(h2, h3), ms_(h3, h4), ms_(h4, clk::now()), (double)ms);
+    }
     if (st.desc.nano_fixed <= 0) {
       const int32_t alpha = st.desc.aimd_alpha ? st.desc.aimd_alpha : 4;
       const double beta = st.desc.aimd_beta != 0.0 ? st.desc.aimd_beta : 0.5;
