@@ -426,7 +426,7 @@ typedef struct tlora_step_desc {
 typedef struct tlora_step_stats {
   int32_t nano_used;      /* N of the step just run                                        */
   int32_t next_nano;      /* N the controller chose for the next step                      */
-  double ms;              /* CUDA-event time of the step on the caller's stream            */
+  double ms;              /* CUDA-event time of the step (see tlora_step_run; -1 unknown)  */
   int32_t replayed_graph; /* 1 if the step was a CUDA-graph replay                         */
   long long launches;     /* kernels in the step (a replay re-launches the eager run's)     */
   int64_t tokens;
@@ -456,8 +456,10 @@ int tlora_step_set_controller(tlora_step* step, int32_t nano_fixed, int32_t nano
                               int32_t aimd_alpha, double aimd_beta, double aimd_tau_rel);
 /* N the next tlora_step_run will use (fill the inputs in that layout). */
 int tlora_step_next_n(const tlora_step* step, int32_t* n);
-/* One training step on input set `set`, enqueued on `stream` and waited for (the step time
- * feeds AIMD). stats may be NULL. */
+/* One training step on input set `set`, enqueued on `stream`. Under AIMD (nano_fixed 0) or
+ * TLORA_RUN_TRACE the call waits for the step (its time feeds the controller) and stats->ms
+ * is this step's time; with a fixed N it returns right after enqueueing and stats->ms is
+ * the time of the latest completed step (-1 if none). stats may be NULL. */
 int tlora_step_run(tlora_step* step, int32_t set, int32_t flags, void* stream,
                    tlora_step_stats* stats);
 
@@ -539,8 +541,10 @@ int tlora_tp_buffer(tlora_tp_step* step, int32_t kind, int32_t index, void** ptr
 /* nano_t0[n_out + 1] (global token rows) and nano_slot[n_out x S] of nano count n. */
 int tlora_tp_layout(tlora_tp_step* step, int32_t n, int32_t* n_out, int64_t* nano_t0,
                     int32_t* nano_slot);
-/* One training step (collective: every rank calls it); waits for its CUDA-event time,
- * averaged over the group before the AIMD update (so all ranks agree on the next N). */
+/* One training step (collective: every rank calls it). Under AIMD (nano_fixed 0) it waits
+ * for the step's CUDA-event time, averaged over the group before the AIMD update (so all
+ * ranks agree on the next N); with a fixed N it returns after enqueueing and stats->ms is
+ * the latest completed step's time (-1 if none). */
 int tlora_tp_run(tlora_tp_step* step, int32_t flags, void* stream, tlora_step_stats* stats);
 
 /* Sharded data-parallel optimizer (the alternative to tlora_layer_allreduce_grads + a full

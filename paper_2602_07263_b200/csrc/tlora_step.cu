@@ -214,8 +214,13 @@ struct tlora_step {
   // exec: the step's own main stream (a captured graph needs a capturable stream; the
   // caller's may be the legacy default stream); it joins the caller's stream both ways
   cudaStream_t exec = nullptr, side = nullptr, comm_s = nullptr;
-  cudaEvent_t t_begin = nullptr, t_end = nullptr, ev_side = nullptr, ev_comm = nullptr,
-              ev_in = nullptr;
+  cudaEvent_t ev_side = nullptr, ev_comm = nullptr, ev_in = nullptr;
+  // step timing events, a ring of 4 (begin, end) pairs: with a fixed N nothing needs the
+  // host to wait for a step, so run() returns right after enqueueing and reports the time
+  // of the latest step that has completed
+  static constexpr int kTimeRing = 4;
+  cudaEvent_t t_begin_r[kTimeRing] = {}, t_end_r[kTimeRing] = {};
+  long long t_step_r[kTimeRing] = {-1, -1, -1, -1};
   std::vector<cudaEvent_t> events;  // per op of the largest schedule
   std::map<int32_t, std::unique_ptr<Layout>> layouts;
   int32_t zeroed_for = -1;          // nano count the H / dH arenas were last zeroed for
@@ -268,8 +273,11 @@ tlora_step::~tlora_step() {
   for (auto* l : layers) tlora_layer_destroy(l);
   for (auto e : events) cudaEventDestroy(e);
   for (auto e : trace_ev) cudaEventDestroy(e);
-  for (auto e : {t_begin, t_end, ev_side, ev_comm, ev_in})
+  for (auto e : {ev_side, ev_comm, ev_in})
     if (e) cudaEventDestroy(e);
+  for (int i = 0; i < kTimeRing; ++i)
+    for (auto e : {t_begin_r[i], t_end_r[i]})
+      if (e) cudaEventDestroy(e);
   if (exec) cudaStreamDestroy(exec);
   if (side) cudaStreamDestroy(side);
   if (comm_s) cudaStreamDestroy(comm_s);
@@ -590,8 +598,10 @@ int tlora_step_create(const tlora_step_desc* desc, tlora_comm* comm, tlora_step*
       }
     }
     if (comm) ST_CUDA(cudaStreamCreateWithFlags(&st->comm_s, cudaStreamNonBlocking));
-    ST_CUDA(cudaEventCreate(&st->t_begin));
-    ST_CUDA(cudaEventCreate(&st->t_end));
+    for (int i = 0; i < tlora_step::kTimeRing; ++i) {
+      ST_CUDA(cudaEventCreate(&st->t_begin_r[i]));
+      ST_CUDA(cudaEventCreate(&st->t_end_r[i]));
+    }
     ST_CUDA(cudaEventCreateWithFlags(&st->ev_side, cudaEventDisableTiming));
     ST_CUDA(cudaEventCreateWithFlags(&st->ev_comm, cudaEventDisableTiming));
     ST_CUDA(cudaEventCreateWithFlags(&st->ev_in, cudaEventDisableTiming));
@@ -743,10 +753,15 @@ int tlora_step_run(tlora_step* step, int32_t set, int32_t flags, void* stream,
                                                  : st.aimd_n;
     Layout& lo = st.layout(n_use);
     const int32_t n = lo.map.n;
+    const bool trace = (flags & TLORA_RUN_TRACE) != 0;
+    // AIMD needs this step's time before the next step; a fixed N (and no trace) does not
+    const bool lazy = st.desc.nano_fixed > 0 && !trace;
+    const int tslot = (int)(st.steps_run % tlora_step::kTimeRing);
+    cudaEvent_t t_begin = st.t_begin_r[tslot], t_end = st.t_end_r[tslot];
     // the step starts after everything already enqueued on the caller's stream
     ST_CUDA(cudaEventRecord(st.ev_in, caller));
     ST_CUDA(cudaStreamWaitEvent(main, st.ev_in, 0));
-    ST_CUDA(cudaEventRecord(st.t_begin, main));
+    ST_CUDA(cudaEventRecord(t_begin, main));
     if (st.zeroed_for != n) {
       // the H stashes / dH ring must be zero outside each row's own packed-rank columns;
       // a new token layout moves jobs between rows
@@ -754,7 +769,6 @@ int tlora_step_run(tlora_step* step, int32_t set, int32_t flags, void* stream,
       ST_CUDA(cudaMemsetAsync(st.dH, 0, (size_t)st.ring * st.T * st.R * 2, main));
       st.zeroed_for = n;
     }
-    const bool trace = (flags & TLORA_RUN_TRACE) != 0;
     const bool graphs = (st.desc.flags & TLORA_STEP_GRAPH) && st.comm == nullptr &&
                         !(flags & (TLORA_RUN_EAGER | TLORA_RUN_TRACE));
     const long long l0 = tlora_launch_count();
@@ -765,17 +779,31 @@ int tlora_step_run(tlora_step* step, int32_t set, int32_t flags, void* stream,
     } else {
       st.enqueue(lo, set, main, trace);
     }
-    ST_CUDA(cudaEventRecord(st.t_end, main));
-    ST_CUDA(cudaStreamWaitEvent(caller, st.t_end, 0));  // and the caller's stream after it
-    ST_CUDA(cudaEventSynchronize(st.t_end));
-    float ms = 0.f;
-    ST_CUDA(cudaEventElapsedTime(&ms, st.t_begin, st.t_end));
+    ST_CUDA(cudaEventRecord(t_end, main));
+    ST_CUDA(cudaStreamWaitEvent(caller, t_end, 0));  // and the caller's stream after it
+    st.t_step_r[tslot] = st.steps_run;
+    float ms = -1.f;
+    if (!lazy) {
+      ST_CUDA(cudaEventSynchronize(t_end));
+      ST_CUDA(cudaEventElapsedTime(&ms, t_begin, t_end));
+    } else {  // the latest step whose end event has completed (-1: none yet)
+      long long best = -1;
+      for (int i = 0; i < tlora_step::kTimeRing; ++i) {
+        if (st.t_step_r[i] <= best || cudaEventQuery(st.t_end_r[i]) != cudaSuccess) continue;
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, st.t_begin_r[i], st.t_end_r[i]) == cudaSuccess) {
+          best = st.t_step_r[i];
+          ms = t;
+        }
+      }
+      (void)cudaGetLastError();  // cudaErrorNotReady of the queries is not an error here
+    }
     if (trace) {
       st.trace_ops = lo.ops;
       st.trace_ms.assign(lo.ops.size(), 0.0);
       for (size_t i = 0; i < lo.ops.size(); ++i) {
         float t = 0.f;
-        ST_CUDA(cudaEventElapsedTime(&t, st.t_begin, st.trace_ev[i]));
+        ST_CUDA(cudaEventElapsedTime(&t, t_begin, st.trace_ev[i]));
         st.trace_ms[i] = t;
       }
     }
@@ -783,7 +811,7 @@ int tlora_step_run(tlora_step* step, int32_t set, int32_t flags, void* stream,
     const long long launches = lo.launches;
     if (graphs && !replayed) {
       // capture this layout's step for the next visits (every scratch buffer now exists;
-      // the exec stream is idle)
+      // the eager run may still be executing: capture only records)
       cudaGraph_t g = nullptr;
       ST_CUDA(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
       try {

@@ -142,7 +142,12 @@ struct tlora_tp_step {
   std::vector<void*> ipc_opened;
   int32_t* present = nullptr;
   cudaStream_t main = nullptr, comm_s = nullptr, side = nullptr;
-  cudaEvent_t t_begin = nullptr, t_end = nullptr;
+  // step timing: a ring of (begin, end) pairs; with a fixed N run() does not wait for the
+  // step and reports the latest completed one
+  static constexpr int kTimeRing = 4;
+  cudaEvent_t t_begin_r[kTimeRing] = {}, t_end_r[kTimeRing] = {};
+  long long t_step_r[kTimeRing] = {-1, -1, -1, -1};
+  long long steps_run = 0;
   std::vector<cudaEvent_t> evpool;
   size_t ev_next = 0;
   std::map<int32_t, std::unique_ptr<Layout>> layouts;
@@ -195,8 +200,9 @@ tlora_tp_step::~tlora_tp_step() {
   for (auto* l : layers) tlora_layer_destroy(l);
   for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
   for (auto e : evpool) cudaEventDestroy(e);
-  for (auto e : {t_begin, t_end})
-    if (e) cudaEventDestroy(e);
+  for (int i = 0; i < kTimeRing; ++i)
+    for (auto e : {t_begin_r[i], t_end_r[i]})
+      if (e) cudaEventDestroy(e);
   for (auto s : {main, comm_s, side})
     if (s) cudaStreamDestroy(s);
   for (void* p : owned) cudaFree(p);
@@ -595,8 +601,10 @@ int tlora_tp_create(const tlora_tp_desc* desc, tlora_comm* comm, tlora_tp_step**
     TP_CUDA(cudaStreamCreateWithFlags(&st->main, cudaStreamNonBlocking));
     TP_CUDA(cudaStreamCreateWithFlags(&st->comm_s, cudaStreamNonBlocking));
     if (D.flags & TLORA_TP_SIDE_GRADS) TP_CUDA(cudaStreamCreateWithFlags(&st->side, cudaStreamNonBlocking));
-    TP_CUDA(cudaEventCreate(&st->t_begin));
-    TP_CUDA(cudaEventCreate(&st->t_end));
+    for (int i = 0; i < tlora_tp_step::kTimeRing; ++i) {
+      TP_CUDA(cudaEventCreate(&st->t_begin_r[i]));
+      TP_CUDA(cudaEventCreate(&st->t_end_r[i]));
+    }
     st->ms_dev = (double*)st->alloc(sizeof(double));
     for (int32_t p = 0; p < st->NP; ++p) {
       tlora_layer* l = nullptr;
@@ -751,42 +759,59 @@ int tlora_tp_run(tlora_tp_step* step, int32_t flags, void* stream, tlora_step_st
     using clk = std::chrono::steady_clock;
     const auto h0 = clk::now();
     Layout& lo = st.layout(n_use);
+    const bool lazy = st.desc.nano_fixed > 0;  // nothing needs this step's time now
+    const int tslot = (int)(st.steps_run % tlora_tp_step::kTimeRing);
+    cudaEvent_t t_begin = st.t_begin_r[tslot], t_end = st.t_end_r[tslot];
     st.ev_next = 0;
     st.wait(st.main, caller);
     const long long l0 = tlora_launch_count();
-    TP_CUDA(cudaEventRecord(st.t_begin, st.main));
+    TP_CUDA(cudaEventRecord(t_begin, st.main));
     const auto h1 = clk::now();
     st.forward(lo);
     const auto h2 = clk::now();
     st.backward(lo);
     for (auto* l : st.layers) chk(tlora_layer_optimizer_step_masked(l, st.present, 1.f, st.main));
-    TP_CUDA(cudaEventRecord(st.t_end, st.main));
+    TP_CUDA(cudaEventRecord(t_end, st.main));
     st.wait(caller, st.main);
+    st.t_step_r[tslot] = st.steps_run++;
     const auto h3 = clk::now();
-    TP_CUDA(cudaEventSynchronize(st.t_end));
+    float ms = -1.f;
+    if (!lazy) {
+      TP_CUDA(cudaEventSynchronize(t_end));
+      TP_CUDA(cudaEventElapsedTime(&ms, t_begin, t_end));
+    } else {
+      long long best = -1;
+      for (int i = 0; i < tlora_tp_step::kTimeRing; ++i) {
+        if (st.t_step_r[i] <= best || cudaEventQuery(st.t_end_r[i]) != cudaSuccess) continue;
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, st.t_begin_r[i], st.t_end_r[i]) == cudaSuccess) {
+          best = st.t_step_r[i];
+          ms = t;
+        }
+      }
+      (void)cudaGetLastError();  // cudaErrorNotReady of the queries is not an error here
+    }
     const auto h4 = clk::now();
-    float ms = 0.f;
-    TP_CUDA(cudaEventElapsedTime(&ms, st.t_begin, st.t_end));
-    // the group's mean step time: every rank feeds the same value to AIMD, so all ranks
-    // take the same N next step
-    double msd = ms;
-    TP_CUDA(cudaMemcpyAsync(st.ms_dev, &msd, sizeof msd, cudaMemcpyHostToDevice, st.main));
-    chk(tlora_comm_all_reduce(st.comm, TLORA_GROUP_WORLD, st.ms_dev, st.ms_dev, 1, TLORA_F64, 1, st.main));
-    TP_CUDA(cudaMemcpyAsync(&msd, st.ms_dev, sizeof msd, cudaMemcpyDeviceToHost, st.main));
-    TP_CUDA(cudaStreamSynchronize(st.main));
-    const double t_group = msd / 1e3;
+    if (!lazy) {
+      // the group's mean step time: every rank feeds the same value to AIMD, so all ranks
+      // take the same N next step
+      double msd = ms;
+      TP_CUDA(cudaMemcpyAsync(st.ms_dev, &msd, sizeof msd, cudaMemcpyHostToDevice, st.main));
+      chk(tlora_comm_all_reduce(st.comm, TLORA_GROUP_WORLD, st.ms_dev, st.ms_dev, 1, TLORA_F64, 1,
+                                st.main));
+      TP_CUDA(cudaMemcpyAsync(&msd, st.ms_dev, sizeof msd, cudaMemcpyDeviceToHost, st.main));
+      TP_CUDA(cudaStreamSynchronize(st.main));
+      const int32_t alpha = st.desc.aimd_alpha ? st.desc.aimd_alpha : 4;
+      const double beta = st.desc.aimd_beta != 0.0 ? st.desc.aimd_beta : 0.5;
+      chk(tlora_aimd_step(&st.aimd_n, &st.has_prev, &st.t_prev, alpha, beta, st.desc.aimd_tau_rel,
+                          msd / 1e3));
+      st.aimd_n = std::min(st.aimd_n, st.total_samples);
+    }
     if (std::getenv("TLORA_TP_DEBUG")) {
       auto ms_ = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
       std::fprintf(stderr, "[tlora_tp rank %d] layout+wait %.3f fwd-enqueue %.3f bwd-enqueue %.3f "
                    "sync %.3f aimd %.3f device %.3f ms\n", st.rank, ms_(h0, h1), ms_(h1, h2),
                    ms_(h2, h3), ms_(h3, h4), ms_(h4, clk::now()), (double)ms);
-    }
-    if (st.desc.nano_fixed <= 0) {
-      const int32_t alpha = st.desc.aimd_alpha ? st.desc.aimd_alpha : 4;
-      const double beta = st.desc.aimd_beta != 0.0 ? st.desc.aimd_beta : 0.5;
-      chk(tlora_aimd_step(&st.aimd_n, &st.has_prev, &st.t_prev, alpha, beta, st.desc.aimd_tau_rel,
-                          t_group));
-      st.aimd_n = std::min(st.aimd_n, st.total_samples);
     }
     if (stats) {
       stats->nano_used = lo.map.n;
