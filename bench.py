@@ -1102,6 +1102,18 @@ def run_tp_exec(args, rank, world, local_rank):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = t.item() / args.steps
     flops = wl.flops_fwd_bwd() / wl.layers
+    # one traced step after the timed region: the reference's PipelineTrace / monitor()
+    # (nano_pipeline.hpp:28-34, 114-126) from measured per-nano-batch spans
+    from paper_2602_07263_b200.layer import monitor
+    s_ = ex.run(stream, trace=True)
+    comp, comm_ms = ex.trace()
+    t_it = s_.ms / 1e3
+    t_an = max(sum(comp), sum(comm_ms)) / 1e3
+    eta, stall = monitor([c / 1e3 for c in comp], [c / 1e3 for c in comm_ms], t_it, t_an, 1)
+    reading = {"t_comp_s": [round(c / 1e3, 6) for c in comp],
+               "t_comm_s": [round(c / 1e3, 6) for c in comm_ms], "t_iter_event_s": round(t_it, 6),
+               "t_iter_analytic_s": round(t_an, 6), "eta_util": round(eta, 6),
+               "delta_stall_s": round(stall, 6)}
     return {
         "metric": METRIC, "value": round(wl.tokens / (ms_per_step / 1e3), 1), "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -1119,6 +1131,7 @@ def run_tp_exec(args, rank, world, local_rank):
                    "algorithmic_tflop_per_step": round(flops / 1e12, 3),
                    "achieved_tflops_aggregate": round(flops / (ms_per_step / 1e3) / 1e12, 1)},
         "gpu_launches": int(launches),
+        "pipeline_monitor": reading,
         "nvlink": nvl,
         "clocks": clk,
     }

@@ -546,6 +546,11 @@ int tlora_tp_layout(tlora_tp_step* step, int32_t n, int32_t* n_out, int64_t* nan
  * ranks agree on the next N); with a fixed N it returns after enqueueing and stats->ms is
  * the latest completed step's time (-1 if none). */
 int tlora_tp_run(tlora_tp_step* step, int32_t flags, void* stream, tlora_step_stats* stats);
+/* After a tlora_tp_run with TLORA_RUN_TRACE: per nano-batch the summed compute spans (main
+ * stream, forward + backward) and boundary-traffic spans (comm stream), ms — the measured
+ * PipelineTrace t_comp / t_comm (nano_pipeline.hpp:28-34). */
+int tlora_tp_trace(const tlora_tp_step* step, double* t_comp_ms, double* t_comm_ms, int32_t cap,
+                   int32_t* count);
 
 /* Sharded data-parallel optimizer (the alternative to tlora_layer_allreduce_grads + a full
  * AdamW on every rank): the packed rank rows are split evenly over `group`; this rank owns

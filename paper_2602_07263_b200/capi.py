@@ -218,6 +218,8 @@ SIGNATURES = {
     "tlora_tp_layout": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.c_void_p,
                                   C.c_void_p]),
     "tlora_tp_run": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(StepStatsC)]),
+    "tlora_tp_trace": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                 C.c_int32, C.POINTER(C.c_int32)]),
     "tlora_aimd_step": (C.c_int, [C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                   C.POINTER(C.c_double), C.c_int32, C.c_double, C.c_double,
                                   C.c_double]),

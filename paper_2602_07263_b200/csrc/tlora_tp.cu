@@ -148,6 +148,27 @@ struct tlora_tp_step {
   cudaEvent_t t_begin_r[kTimeRing] = {}, t_end_r[kTimeRing] = {};
   long long t_step_r[kTimeRing] = {-1, -1, -1, -1};
   long long steps_run = 0;
+  // TLORA_RUN_TRACE: CUDA events around every nano-batch's compute (main stream) and
+  // boundary traffic (comm stream): the measured PipelineTrace (nano_pipeline.hpp:28-34)
+  bool tracing = false;
+  struct Mark {
+    int kind, nano, edge;  // kind: 0 compute, 1 communication
+    cudaEvent_t ev;
+  };
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> mark_pool;
+  std::vector<double> trace_comp, trace_comm;  // per nano-batch, ms (last traced step)
+  void mark(cudaStream_t s, int kind, int nano, int edge) {
+    if (!tracing) return;
+    if (marks.size() == mark_pool.size()) {
+      cudaEvent_t e;
+      TP_CUDA(cudaEventCreate(&e));
+      mark_pool.push_back(e);
+    }
+    cudaEvent_t e = mark_pool[marks.size()];
+    TP_CUDA(cudaEventRecord(e, s));
+    marks.push_back({kind, nano, edge, e});
+  }
   std::vector<cudaEvent_t> evpool;
   size_t ev_next = 0;
   std::map<int32_t, std::unique_ptr<Layout>> layouts;
@@ -200,6 +221,7 @@ tlora_tp_step::~tlora_tp_step() {
   for (auto* l : layers) tlora_layer_destroy(l);
   for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
   for (auto e : evpool) cudaEventDestroy(e);
+  for (auto e : mark_pool) cudaEventDestroy(e);
   for (int i = 0; i < kTimeRing; ++i)
     for (auto e : {t_begin_r[i], t_end_r[i]})
       if (e) cudaEventDestroy(e);
@@ -355,6 +377,7 @@ void tlora_tp_step::forward(Layout& lo) {
                                rows_of(H_shard[(size_t)p], b.t0 / P, R[(size_t)p]), main));
     }
     wait(comm_s, main);
+    mark(comm_s, 1, (int)i, 0);
     for (int g = 0; g < groups; ++g)
       all_gather("X" + std::to_string(g), X_full[(size_t)g], X_shard[(size_t)g],
                  (size_t)gdim[(size_t)g] * 2, b);
@@ -363,6 +386,7 @@ void tlora_tp_step::forward(Layout& lo) {
         all_gather("H" + std::to_string(p), H_full[(size_t)p], H_shard[(size_t)p],
                    (size_t)R[(size_t)p] * 2, b);
     if (ce) ep_g[i] = ce_raise();
+    mark(comm_s, 1, (int)i, 1);
     ev_g[i] = ev();
     TP_CUDA(cudaEventRecord(ev_g[i], comm_s));
     (void)nr;
@@ -373,6 +397,7 @@ void tlora_tp_step::forward(Layout& lo) {
     const Nano& b = lo.nanos[i];
     TP_CUDA(cudaStreamWaitEvent(main, ev_g[i], 0));
     if (ce) ce_wait(main, ep_g[i]);
+    mark(main, 0, (int)i, 0);
     for (int32_t p = 0; p < NP; ++p) {
       if (row[(size_t)p]) continue;
       const int g = input[(size_t)p];
@@ -398,8 +423,10 @@ void tlora_tp_step::forward(Layout& lo) {
                                TLORA_BF16, main));
       }
     }
+    mark(main, 0, (int)i, 1);
     // reduce-scatter of the row-parallel outputs, off the main stream
     wait(comm_s, main);
+    mark(comm_s, 1, (int)i, 0);
     for (int32_t p = 0; p < NP; ++p) {
       if (!row[(size_t)p]) continue;
       const int64_t kk = k[(size_t)p];
@@ -413,6 +440,7 @@ void tlora_tp_step::forward(Layout& lo) {
                                       (b.tokens / P) * kk, TLORA_BF16, comm_s));
       }
     }
+    mark(comm_s, 1, (int)i, 1);
   }
   wait(main, comm_s);
 }
@@ -426,11 +454,13 @@ void tlora_tp_step::backward(Layout& lo) {
   std::vector<uint32_t> ep_dy(n, 0);
   auto gather_dy = [&](size_t i) {
     const Nano& b = lo.nanos[i];
+    mark(comm_s, 1, (int)i, 0);
     for (int32_t p = 0; p < NP; ++p)
       if (row[(size_t)p])
         all_gather("dY" + std::to_string(p), dY_full[(size_t)p], dY_shard[(size_t)p],
                    (size_t)k[(size_t)p] * 2, b);
     if (ce) ep_dy[i] = ce_raise();
+    mark(comm_s, 1, (int)i, 1);
     ev_dy[i] = ev();
     TP_CUDA(cudaEventRecord(ev_dy[i], comm_s));
   };
@@ -461,6 +491,7 @@ void tlora_tp_step::backward(Layout& lo) {
     const float beta = i ? 1.f : 0.f;
     TP_CUDA(cudaStreamWaitEvent(main, ev_dy[i], 0));
     if (ce) ce_wait(main, ep_dy[i]);
+    mark(main, 0, (int)i, 0);
     auto dy_dh = [&](int32_t p, char*& dYp, char*& dHp) {
       if (row[(size_t)p]) {
         dYp = rows_of(dY_full[(size_t)p], b.t0, k[(size_t)p]);
@@ -506,8 +537,10 @@ void tlora_tp_step::backward(Layout& lo) {
       else
         chk(tlora_backward_grad_b(l, pl, rows_of(H_full[(size_t)p], b.t0, R[(size_t)p]), dYp, beta, G));
     }
+    mark(main, 0, (int)i, 1);
     // reduce-scatter [dX | dH] of the column-parallel projections
     wait(comm_s, main);
+    mark(comm_s, 1, (int)i, 0);
     for (int g = 0; g < groups; ++g)
       reduce_scatter("rsX" + std::to_string(g), dX_part[(size_t)g], dX_shard[(size_t)g],
                      gdim[(size_t)g], b);
@@ -528,6 +561,7 @@ void tlora_tp_step::backward(Layout& lo) {
                                  nr, R[(size_t)p], rows_of(dH_shard[(size_t)p], row0, R[(size_t)p]),
                                  comm_s));
     }
+    mark(comm_s, 1, (int)i, 1);
     cudaEvent_t ev_r = ev();
     TP_CUDA(cudaEventRecord(ev_r, comm_s));
     if (ev_prev_rs) grad_a_cols(prev_i, ev_prev_rs);
@@ -732,6 +766,19 @@ int tlora_tp_buffer(tlora_tp_step* step, int32_t kind, int32_t index, void** ptr
   });
 }
 
+int tlora_tp_trace(const tlora_tp_step* step, double* t_comp_ms, double* t_comm_ms, int32_t cap,
+                   int32_t* count) {
+  return tp_guard([&] {
+    need(step != nullptr, TLORA_ERR_ARG, "step is null");
+    const size_t n = step->trace_comp.size();
+    if (count) *count = (int32_t)n;
+    for (size_t i = 0; i < n && (int32_t)i < cap; ++i) {
+      if (t_comp_ms) t_comp_ms[i] = step->trace_comp[i];
+      if (t_comm_ms) t_comm_ms[i] = step->trace_comm[i];
+    }
+  });
+}
+
 int tlora_tp_layout(tlora_tp_step* step, int32_t n, int32_t* n_out, int64_t* nano_t0,
                     int32_t* nano_slot) {
   return tp_guard([&] {
@@ -752,14 +799,16 @@ int tlora_tp_run(tlora_tp_step* step, int32_t flags, void* stream, tlora_step_st
     need(step != nullptr, TLORA_ERR_ARG, "step is null");
     auto& st = *step;
     DevGuard g(st.device);
-    (void)flags;
     cudaStream_t caller = reinterpret_cast<cudaStream_t>(stream);
     const int32_t n_use = st.desc.nano_fixed > 0 ? std::min(st.desc.nano_fixed, st.total_samples)
                                                  : st.aimd_n;
     using clk = std::chrono::steady_clock;
     const auto h0 = clk::now();
     Layout& lo = st.layout(n_use);
-    const bool lazy = st.desc.nano_fixed > 0;  // nothing needs this step's time now
+    st.tracing = (flags & TLORA_RUN_TRACE) != 0;
+    st.marks.clear();
+    // nothing needs this step's time now (a traced step waits for its events)
+    const bool lazy = st.desc.nano_fixed > 0 && !st.tracing;
     const int tslot = (int)(st.steps_run % tlora_tp_step::kTimeRing);
     cudaEvent_t t_begin = st.t_begin_r[tslot], t_end = st.t_end_r[tslot];
     st.ev_next = 0;
@@ -792,6 +841,22 @@ int tlora_tp_run(tlora_tp_step* step, int32_t flags, void* stream, tlora_step_st
       (void)cudaGetLastError();  // cudaErrorNotReady of the queries is not an error here
     }
     const auto h4 = clk::now();
+    if (st.tracing) {  // spans per nano-batch: compute on main, boundary traffic on comm
+      st.trace_comp.assign(lo.nanos.size(), 0.0);
+      st.trace_comm.assign(lo.nanos.size(), 0.0);
+      std::map<std::pair<int, int>, cudaEvent_t> open;
+      for (const auto& m : st.marks) {
+        const auto key = std::make_pair(m.kind, m.nano);
+        if (m.edge == 0) {
+          open[key] = m.ev;
+          continue;
+        }
+        float t = 0.f;
+        TP_CUDA(cudaEventElapsedTime(&t, open.at(key), m.ev));
+        (m.kind == 0 ? st.trace_comp : st.trace_comm)[(size_t)m.nano] += t;
+      }
+      st.tracing = false;
+    }
     if (!lazy) {
       // the group's mean step time: every rank feeds the same value to AIMD, so all ranks
       // take the same N next step

@@ -137,10 +137,20 @@ class TPExecutor:
         call("tlora_tp_layout", self._h, int(n), C.byref(out), t0.ctypes.data, ns.ctypes.data)
         return out.value, t0, ns.reshape(m, S)
 
-    def run(self, stream=None) -> StepStats:
+    def run(self, stream=None, trace: bool = False) -> StepStats:
         st = capi.StepStatsC()
-        call("tlora_tp_run", self._h, 0, _stream_ptr(stream), C.byref(st))
+        call("tlora_tp_run", self._h, capi.RUN_TRACE if trace else 0, _stream_ptr(stream),
+             C.byref(st))
         return StepStats(st.nano_used, st.next_nano, st.ms, False, st.launches, st.tokens)
+
+    def trace(self):
+        """(t_comp_ms, t_comm_ms) per nano-batch of the last run(trace=True)."""
+        n = C.c_int32()
+        call("tlora_tp_trace", self._h, None, None, 0, C.byref(n))
+        a = (C.c_double * max(1, n.value))()
+        b = (C.c_double * max(1, n.value))()
+        call("tlora_tp_trace", self._h, a, b, n.value, C.byref(n))
+        return list(a[: n.value]), list(b[: n.value])
 
     def close(self):
         if getattr(self, "_h", None):
