@@ -808,7 +808,8 @@ int tlora_tp_run(tlora_tp_step* step, int32_t flags, void* stream, tlora_step_st
     st.tracing = (flags & TLORA_RUN_TRACE) != 0;
     st.marks.clear();
     // nothing needs this step's time now (a traced step waits for its events)
-    const bool lazy = st.desc.nano_fixed > 0 && !st.tracing;
+    static const bool force_sync = std::getenv("TLORA_TP_SYNC") != nullptr;  // A/B knob
+    const bool lazy = st.desc.nano_fixed > 0 && !st.tracing && !force_sync;
     const int tslot = (int)(st.steps_run % tlora_tp_step::kTimeRing);
     cudaEvent_t t_begin = st.t_begin_r[tslot], t_end = st.t_end_r[tslot];
     st.ev_next = 0;
