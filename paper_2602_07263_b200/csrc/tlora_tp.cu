@@ -304,8 +304,16 @@ uint32_t tlora_tp_step::ce_raise() {
 }
 
 void tlora_tp_step::ce_wait(cudaStream_t s, uint32_t ep) {
+  // TLORA_TP_MEMOP_MAIN=0 (A/B knob): keep the stream wait-value ops off the GEMM stream —
+  // the comm stream waits for the flags and the main stream waits for the comm stream
+  static const bool off_main = [] {
+    const char* e = std::getenv("TLORA_TP_MEMOP_MAIN");
+    return e && e[0] == '0';
+  }();
+  cudaStream_t w = (off_main && s == main) ? comm_s : s;
   for (int q = 0; q < P; ++q)
-    if (q != rank) chk(tlora_stream_wait_u32(s, flags.ptr[rank] + 4 * q, ep));
+    if (q != rank) chk(tlora_stream_wait_u32(w, flags.ptr[rank] + 4 * q, ep));
+  if (w != s) wait(s, w);
 }
 
 // Rows [t0, t0 + tokens) of the gathered buffer: rank q's shard lands at t0 + q * tokens / P

@@ -10,8 +10,8 @@ PY
 }
 tp() { local name=$1; local envs=$2; shift 2; env $envs python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 500)) bench.py --gpus $N --tp "$@" > "$OUT/$name.log" 2>&1; summ "$OUT/$name.log" $name; }
 tp cpp "TLORA_DYN_SCHED=1" --steps 8 --warmup 3 --nano-batches 2
-tp cpp_sync "TLORA_DYN_SCHED=1 TLORA_TP_SYNC=1" --steps 8 --warmup 3 --nano-batches 2
-tp cpp_conn32 "TLORA_DYN_SCHED=1 CUDA_DEVICE_MAX_CONNECTIONS=32" --steps 8 --warmup 3 --nano-batches 2
+tp cpp_memop_off "TLORA_DYN_SCHED=1 TLORA_TP_MEMOP_MAIN=0" --steps 8 --warmup 3 --nano-batches 2
+tp cpp_b "TLORA_DYN_SCHED=1" --steps 8 --warmup 3 --nano-batches 2
 tp py "TLORA_DYN_SCHED=1" --steps 8 --warmup 3 --tp-driver python --nano 2 --aimd-steps 0
-tp py_conn32 "TLORA_DYN_SCHED=1 CUDA_DEVICE_MAX_CONNECTIONS=32" --steps 8 --warmup 3 --tp-driver python --nano 2 --aimd-steps 0
-tp cpp_aimd "TLORA_DYN_SCHED=1" --steps 12 --warmup 3
+tp cpp_memop_off_b "TLORA_DYN_SCHED=1 TLORA_TP_MEMOP_MAIN=0" --steps 8 --warmup 3 --nano-batches 2
+
