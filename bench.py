@@ -1089,8 +1089,9 @@ def run_tp_exec(args, rank, world, local_rank):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     traj, launches = [], 0
     e0.record(stream)
+    trace_all = os.environ.get("TLORA_TP_TRACE_ALL") == "1"  # diagnostic: trace every step
     for _ in range(args.steps):
-        s_ = ex.run(stream)
+        s_ = ex.run(stream, trace=trace_all)
         traj.append([s_.nano_used, round(s_.ms, 3)])
         launches += s_.launches
     e1.record(stream)
