@@ -196,6 +196,29 @@ void cpu_comm_arguments() {  // communicator handle: argument errors surface as 
                                         "rank"));
 }
 
+void cpu_trainer_errors() {  // trainer.hpp: bad descriptors fail before any device work
+  ModelSpec m;
+  m.name = "x";
+  m.num_layers = 1;
+  m.base_memory_bytes = 1.0;
+  JobSpec j;
+  j.job_id = "a";
+  j.model = m;
+  j.rank = 8;
+  SsmLayerSet set = fuse_projections({j}, {{"q", 64, 64}, {"o", 48, 32}});
+  TrainerOptions opt;
+  CHECK(throws_with<std::runtime_error>([&] { LayerSetTrainer t(set, opt, {0, 5}); }, "input group"));
+  CHECK(throws_with<std::runtime_error>([&] { LayerSetTrainer t(set, opt, {0, 0}); }, "same d"));
+  opt.input_sets = 3;
+  CHECK(throws_with<std::runtime_error>([&] { LayerSetTrainer t(set, opt, {0, 1}); }, "input_sets"));
+  // the executor's schedule is a pure host function
+  std::vector<tlora_step_op> ops(64);
+  int32_t n = 0;
+  CHECK(tlora_step_schedule_host(2, 2, 8, 1, 0, ops.data(), 64, &n) == TLORA_OK);
+  CHECK(n == 1 + 2 * (2 + 2 * 2) + 2);  // shrink, per nano 2 FWD + 2 DX + 2 GRADS, 2 AdamW
+  CHECK(tlora_step_schedule_host(0, 1, 8, 1, 0, nullptr, 0, &n) == TLORA_ERR_ARG);
+}
+
 void cpu_nano_and_fuse() {  // test_nano_pipeline.cpp:28-38, 90-123; test_ssm_plan.cpp:62-78
   auto s = partition(10, 4);
   CHECK(s.n == 4);
@@ -424,6 +447,7 @@ int main(int argc, char** argv) {
     cases.push_back({"partition / aimd_step / fuse", cpu_nano_and_fuse});
     cases.push_back({"communicator argument errors", cpu_comm_arguments});
     cases.push_back({"projection-level layer set", cpu_projection_layer_set});
+    cases.push_back({"trainer descriptor errors, host schedule", cpu_trainer_errors});
   }
   if (mode == "gpu" || mode == "all") {
     cases.push_back({"fused_forward matches the materialized oracle", gpu_matches_oracle});
