@@ -821,6 +821,7 @@ const void* stage_input(const void* src, size_t count, int dtype, int where, Dev
 // thread-local slot tlora_last_error() reads.
 namespace tlora {
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace tlora
 
 // ==================================================================== C-ABI

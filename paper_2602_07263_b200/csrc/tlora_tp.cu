@@ -42,9 +42,27 @@
 
 namespace tlora {
 void set_last_error(const std::string& msg);  // tlora_capi.cu
+void note_launch();                           // tlora_capi.cu: library launch counter
 }
 
 namespace {
+
+// Wait until every peer's epoch flag reached `ep` (lane q polls flags[q]; q = self skipped).
+// The kernel form of the flag wait: a spinning 32-thread CTA occupies no front-end channel,
+// where a blocked stream wait-value op can hold back unrelated streams sharing its
+// hardware queue while later work is already enqueued.
+__global__ void flag_wait_kernel(const uint32_t* flags, int P, int self, uint32_t ep) {
+  const int q = threadIdx.x;
+  if (q < P && q != self) {
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + q) : "memory");
+      if ((int32_t)(v - ep) >= 0) break;
+      __nanosleep(64);
+    } while (true);
+  }
+  __syncwarp();
+}
 
 struct TpError : std::runtime_error {
   int code;
@@ -310,9 +328,21 @@ void tlora_tp_step::ce_wait(cudaStream_t s, uint32_t ep) {
     const char* e = std::getenv("TLORA_TP_MEMOP_MAIN");
     return e && e[0] == '0';
   }();
+  // TLORA_TP_WAIT=memop|kernel (A/B knob): stream wait-value ops or a polling kernel
+  static const bool kernel_wait = [] {
+    const char* e = std::getenv("TLORA_TP_WAIT");
+    return e && std::strcmp(e, "kernel") == 0;
+  }();
   cudaStream_t w = (off_main && s == main) ? comm_s : s;
-  for (int q = 0; q < P; ++q)
-    if (q != rank) chk(tlora_stream_wait_u32(w, flags.ptr[rank] + 4 * q, ep));
+  if (kernel_wait) {
+    flag_wait_kernel<<<1, 32, 0, w>>>(reinterpret_cast<const uint32_t*>(flags.ptr[rank]), P, rank,
+                                      ep);
+    TP_CUDA(cudaGetLastError());
+    tlora::note_launch();
+  } else {
+    for (int q = 0; q < P; ++q)
+      if (q != rank) chk(tlora_stream_wait_u32(w, flags.ptr[rank] + 4 * q, ep));
+  }
   if (w != s) wait(s, w);
 }
 
