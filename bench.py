@@ -984,10 +984,19 @@ def run_tp(args, rank, world, local_rank):
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    step_ev = os.environ.get("TLORA_BENCH_STEP_EVENTS") == "1"  # diagnostic: per-step spans
+    evs = []
     for _ in range(args.steps):
+        if step_ev:
+            evs.append(torch.cuda.Event(enable_timing=True))
+            evs[-1].record(stream)
         st.step(st.n)
     e1.record(stream)
     torch.cuda.synchronize()
+    if step_ev:
+        spans = [a.elapsed_time(b) for a, b in zip(evs, evs[1:] + [e1])]
+        print(f"[rank {rank}] caller-stream step spans ms (N={st.n}): "
+              f"{[round(x, 3) for x in spans]}", file=sys.stderr, flush=True)
     dist.barrier()
     nvl = nvlink_delta(nv0, nvlink_bytes(), args.steps) if rank == 0 else None
     clk = clocks.stop()
@@ -1081,21 +1090,33 @@ def run_tp_exec(args, rank, world, local_rank):
     clocks = ClockSampler(local_rank)
     clocks.start()
     clocks.wait_ready()
-    for _ in range(args.warmup):
+    # AIMD every step: a nano-batch count used for the first time builds its layout (plans,
+    # split-K scratch) on the host, so settle untimed until the controller's cycle is warm
+    settle = args.warmup if nano_fixed > 0 else max(args.warmup, 12)
+    for _ in range(settle):
         ex.run(stream)
     torch.cuda.synchronize()
+    nv0 = nvlink_bytes() if rank == 0 else None  # (host-side NVML reads: before the barrier)
     dist.barrier()
-    nv0 = nvlink_bytes() if rank == 0 else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     traj, launches = [], 0
     e0.record(stream)
     trace_all = os.environ.get("TLORA_TP_TRACE_ALL") == "1"  # diagnostic: trace every step
+    step_ev = os.environ.get("TLORA_BENCH_STEP_EVENTS") == "1"  # diagnostic: per-step spans
+    evs = []
     for _ in range(args.steps):
+        if step_ev:
+            evs.append(torch.cuda.Event(enable_timing=True))
+            evs[-1].record(stream)
         s_ = ex.run(stream, trace=trace_all)
         traj.append([s_.nano_used, round(s_.ms, 3)])
         launches += s_.launches
     e1.record(stream)
     torch.cuda.synchronize()
+    if step_ev:
+        spans = [a.elapsed_time(b) for a, b in zip(evs, evs[1:] + [e1])]
+        print(f"[rank {rank}] caller-stream step spans ms: {[round(x, 3) for x in spans]}",
+              file=sys.stderr, flush=True)
     dist.barrier()
     nvl = nvlink_delta(nv0, nvlink_bytes(), args.steps) if rank == 0 else None
     clk = clocks.stop()
@@ -1128,7 +1149,7 @@ def run_tp_exec(args, rank, world, local_rank):
                    if args.fused_rs != "none" else "copy engine / NCCL",
                    "nano_batches": ("AIMD every step" if args.nano_batches <= 0
                                     else f"fixed N={args.nano_batches}"),
-                   "aimd_trajectory_n_ms": traj,
+                   "aimd_trajectory_n_ms": traj, "untimed_steps_before_timing": settle,
                    "algorithmic_tflop_per_step": round(flops / 1e12, 3),
                    "achieved_tflops_aggregate": round(flops / (ms_per_step / 1e3) / 1e12, 1)},
         "gpu_launches": int(launches),

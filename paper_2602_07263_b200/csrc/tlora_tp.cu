@@ -913,9 +913,18 @@ int tlora_tp_run(tlora_tp_step* step, int32_t flags, void* stream, tlora_step_st
     }
     if (std::getenv("TLORA_TP_DEBUG")) {
       auto ms_ = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      // device idle time between the previous step's end and this step's begin (only
+      // meaningful when the step synchronised: TLORA_TP_SYNC / AIMD)
+      float gap = -1.f;
+      if (!lazy && st.steps_run >= 2) {
+        const int prev = (int)((st.steps_run - 2) % tlora_tp_step::kTimeRing);
+        if (cudaEventElapsedTime(&gap, st.t_end_r[prev], t_begin) != cudaSuccess) gap = -1.f;
+        (void)cudaGetLastError();
+      }
       std::fprintf(stderr, "[tlora_tp rank %d] layout+wait %.3f fwd-enqueue %.3f bwd-enqueue %.3f "
-                   "sync %.3f aimd %.3f device %.3f ms\n", st.rank, ms_(h0, h1), ms_(h1, h2),
-                   ms_(h2, h3), ms_(h3, h4), ms_(h4, clk::now()), (double)ms);
+                   "sync %.3f aimd %.3f device %.3f gap-before %.3f ms\n", st.rank, ms_(h0, h1),
+                   ms_(h1, h2), ms_(h2, h3), ms_(h3, h4), ms_(h4, clk::now()), (double)ms,
+                   (double)gap);
     }
     if (stats) {
       stats->nano_used = lo.map.n;
