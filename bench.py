@@ -500,6 +500,39 @@ def trace_summary(trace, step_ms):
                     "stream after the side / comm streams"}
 
 
+GEMM_SOURCES = ("lora_gemm2.cuh", "lora_gemm.cuh", "sm100_ptx.cuh", "tlora_plan.hpp")
+
+
+def gemm_sources_sha():
+    """sha256 over the fused GEMM's kernel + plan sources (ties profiles/traffic.json's ncu
+    capture to the kernel that runs now)."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in GEMM_SOURCES:
+        h.update((ROOT / "paper_2602_07263_b200" / "csrc" / f).read_bytes())
+    return h.hexdigest()
+
+
+def traffic_info():
+    """(traffic, algorithmic, source) of the fused GEMM from the committed ncu capture."""
+    tp = ROOT / "profiles" / "traffic.json"
+    if not tp.exists():
+        return None, None, "no capture"
+    try:
+        tj = json.loads(tp.read_text())
+    except Exception:
+        return None, None, "unreadable profiles/traffic.json"
+    src = "profiles/traffic.json (ncu dram bytes, mean per fused-GEMM launch"
+    if tj.get("commit"):
+        src += f", captured at commit {tj['commit']}"
+    if tj.get("gemm_sources_sha256"):
+        same = tj["gemm_sources_sha256"] == gemm_sources_sha()
+        src += ("; GEMM kernel sources identical to this build" if same else
+                "; GEMM kernel sources CHANGED since the capture")
+    return (tj.get("dram_bytes_per_launch_mean", tj.get("fwd_bytes_per_launch")),
+            tj.get("algorithmic_bytes_per_launch_mean"), src + ")")
+
+
 def roofline_block(cnt, ms6, fl6, timing):
     """Roofline of the dominant kernel family (the fused base+LoRA GEMM: fwd + dX) from the
     live per-launch CUDA-event times and algorithmic FLOPs of one step."""
@@ -518,22 +551,12 @@ def roofline_block(cnt, ms6, fl6, timing):
         "tflops": round(fl6[i] / (ms6[i] / 1e3) / 1e12, 1) if ms6[i] > 0 else None,
         "share_of_gemm_time": round(ms6[i] / total_ms, 4) if total_ms > 0 else None}
         for i in range(6)}
-    traffic = traffic_alg = commit = None
-    tp = ROOT / "profiles" / "traffic.json"
-    if tp.exists():
-        try:
-            tj = json.loads(tp.read_text())
-            traffic = tj.get("dram_bytes_per_launch_mean", tj.get("fwd_bytes_per_launch"))
-            traffic_alg = tj.get("algorithmic_bytes_per_launch_mean")
-            commit = tj.get("commit")
-        except Exception:
-            traffic = None
+    traffic, traffic_alg, traffic_src = traffic_info()
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
             "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak else None,
             "frac_of_burst": round(achieved / float(peaks["bf16_tflops"]), 4),
             "timing": timing, "traffic": traffic, "traffic_algorithmic_bytes": traffic_alg,
-            "traffic_source": "profiles/traffic.json (ncu dram bytes, mean per fused-GEMM launch"
-                              + (f", captured at commit {commit})" if commit else ")"),
+            "traffic_source": traffic_src,
             "kernel": "lora_gemm2_kernel (2-CTA fused base+LoRA GEMM: fwd + dX)",
             "peak_source": peaks["source"] + " sustained bf16", "per_launch": per_launch}
 
@@ -853,15 +876,7 @@ def run_ours(args, rank, world, local_rank):
         "tflops": round(fl6[i] / (ms6[i] / 1e3) / 1e12, 1) if ms6[i] > 0 else None,
         "share_of_gemm_time": round(ms6[i] / total_ms, 4) if total_ms > 0 else None}
         for i in range(6)}
-    traffic = traffic_alg = None
-    tp = ROOT / "profiles" / "traffic.json"
-    if tp.exists():
-        try:
-            tj = json.loads(tp.read_text())
-            traffic = tj.get("dram_bytes_per_launch_mean", tj.get("fwd_bytes_per_launch"))
-            traffic_alg = tj.get("algorithmic_bytes_per_launch_mean")
-        except Exception:
-            traffic = None
+    traffic, traffic_alg, traffic_src = traffic_info()
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 4) if peak else None,
                 "frac_of_burst": round(achieved / float(peaks["bf16_tflops"]), 4),
@@ -869,7 +884,7 @@ def run_ours(args, rank, world, local_rank):
                            "as the LAST timed step; per-launch durations of that step x steps") if used_graph else
                           "CUDA-event brackets around every launch of the timed region",
                 "traffic": traffic, "traffic_algorithmic_bytes": traffic_alg,
-                "traffic_source": "profiles/traffic.json (ncu dram bytes, mean per fused-GEMM launch)",
+                "traffic_source": traffic_src,
                 "kernel": "lora_gemm2_kernel (2-CTA fused base+LoRA GEMM: fwd + dX)",
                 "peak_source": peaks["source"] + " sustained bf16", "per_launch": per_launch}
 

@@ -22,6 +22,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 from paper_2602_07263_b200.workload import INPUT_GROUP, config  # noqa: E402
+from bench import gemm_sources_sha  # noqa: E402
 
 
 def main():
@@ -80,6 +81,7 @@ def main():
            "source": f"{src.name}: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
                      "--clock-control none (cache flushed per launch)",
            "commit": sys.argv[2] if len(sys.argv) > 2 else None,
+           "gemm_sources_sha256": gemm_sources_sha(),
            "note": "the launches are tensor-pipe bound (~90% tensor active, DRAM ~20% of peak); "
                    "the L2 panel raster (48 MB budget) minimises DRAM bytes among the budgets "
                    "swept (8..64 MB: 6.2 .. 2.35 GB for gate fwd); the re-reads do not bind",
