@@ -651,8 +651,12 @@ int tlora_tp_create(const tlora_tp_desc* desc, tlora_comm* comm, tlora_tp_step**
     st->ranks.assign(D.ranks, D.ranks + st->S);
     st->batch.assign(D.batch, D.batch + st->S);
     st->seq.assign(D.seq_len, D.seq_len + st->S);
-    st->ce = (D.flags & TLORA_TP_COPY_ENGINE) && st->P > 1;
-    st->fused = (D.flags & TLORA_TP_FUSED_RS) && st->P > 1;
+    // TLORA_TP_CE_SELF=1: keep the copy-engine and fused reduce-scatter data paths at P = 1
+    // (pushes to this rank's own buffers; single-GPU test coverage of those paths)
+    const char* ce_self_env = std::getenv("TLORA_TP_CE_SELF");
+    const bool multi = st->P > 1 || (ce_self_env && ce_self_env[0] == '1');
+    st->ce = (D.flags & TLORA_TP_COPY_ENGINE) && multi;
+    st->fused = (D.flags & TLORA_TP_FUSED_RS) && multi;
     const int32_t P = st->P;
     int64_t base = 0, ext = 0;
     for (int32_t p = 0; p < st->NP; ++p) {

@@ -204,7 +204,10 @@ class TPLayerSetStep:
         # Epochs advance identically on all ranks (same gather sequence). Buffer reuse is
         # ordered by the step structure: a rank pushes into a buffer only after it consumed
         # a later flag of that peer, raised after the peer's last read of the buffer.
-        self.ce_ag = P > 1 and os.environ.get("TLORA_TP_CE_AG", "1") != "0"
+        # (TLORA_TP_CE_SELF=1 keeps it at P = 1: pushes to this rank's own buffers, the
+        # single-GPU test coverage of the copy-engine data path)
+        self.ce_ag = ((P > 1 or os.environ.get("TLORA_TP_CE_SELF") == "1")
+                      and os.environ.get("TLORA_TP_CE_AG", "1") != "0")
         self.ag_hdl = {}
         if self.ce_ag:
             import torch.distributed._symmetric_memory as symm_mem

@@ -4,6 +4,7 @@ per-launch driver it replaces, the AIMD controller driven by its own measured st
 as uploaded, the masked optimizer for jobs absent from a step, and the pure-C++ host
 (tests/cpp/step_main) matching the Python-driven executor bit for bit."""
 import math
+import os
 import subprocess
 import sys
 from pathlib import Path
@@ -265,3 +266,25 @@ def test_tp_executor_matches_python_tp_driver_multi_gpu():
                        capture_output=True, text=True, timeout=900)
     print(p.stdout[-3000:])
     assert p.returncode == 0 and "TP_EXEC_CHECK PASS" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+@pytest.mark.parametrize("script,env", [
+    ("tp_exec_check.py", {"TP_NANO": "3"}),
+    ("tp_check.py", {"TP_NANO": "3", "TP_FUSED_RS": "1"}),
+])
+def test_tp_data_paths_single_gpu(script, env):
+    """The tensor-parallel data paths on ONE GPU (world 1, TLORA_TP_CE_SELF=1): copy-engine
+    all-gathers / slot-sum reduce-scatters and the fused GEMM + reduce-scatter epilogue push
+    into this rank's own buffers. tp_exec_check: the C++ TP step == the Python TP driver
+    (bitwise activations); tp_check: the Python TP driver == the unsharded layer."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    e = dict(os.environ, TLORA_TP_CE_SELF="1", **env)
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node=1", "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), str(ROOT / "tests" / script)],
+                       capture_output=True, text=True, timeout=900, env=e)
+    print(p.stdout[-3000:])
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
