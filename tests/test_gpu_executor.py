@@ -19,7 +19,7 @@ import oracle as O  # noqa: E402
 
 from paper_2602_07263_b200.runner import LayerSetStep  # noqa: E402
 from paper_2602_07263_b200.step import TrainingStep, sample_weights  # noqa: E402
-from paper_2602_07263_b200.workload import Job, Workload, config  # noqa: E402
+from paper_2602_07263_b200.workload import INPUT_GROUP, Job, Workload, config  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -288,3 +288,59 @@ def test_tp_data_paths_single_gpu(script, env):
                        capture_output=True, text=True, timeout=900, env=e)
     print(p.stdout[-3000:])
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+def test_executor_layer_stack_vs_oracle():
+    """A 2-layer x 4-projection stack through the executor at N = 3 (nano-major layout,
+    chained schedule, side-stream gradients) against the double oracle with bf16-emulated
+    intermediates (oracle/tlora_oracle.c: fused_forward / fused_backward, pinned to the
+    reference's goldens): per (layer, projection) the H stash and dA / dB of every job, the
+    last layer's Y and layer 0's dX. Tolerances as SURVEY §8(c) / test_gpu_step_parity."""
+    wl = MINI
+    st = TrainingStep(wl, device=0, nano_fixed=3, graphs=False)
+    st.init_random(wl.seed, keep_weights=True)
+    s = st.run()
+    torch.cuda.synchronize()
+    assert s.nano_used == 3
+    n_used, t0, ns, _ = st.layout(3)
+    slots = np.full(st.T, -1, np.int32)
+    for i in range(n_used):
+        row = int(t0[i])
+        for sl, j in enumerate(wl.jobs):
+            rows = int(ns[i, sl]) * j.seq_len
+            slots[row:row + rows] = sl
+            row += rows
+    assert (slots >= 0).all()
+    f64 = lambda t: t.double().cpu().numpy()  # noqa: E731
+
+    def check(what, got, ref, tol):
+        got = np.asarray(got, np.float64)
+        mx = np.abs(got - ref).max() / max(1.0, np.abs(ref).max())
+        fr = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+        assert mx <= tol[0] and fr <= tol[1], (what, mx, fr)
+
+    last = wl.layers - 1
+    for key in st.keys:
+        L, name = key
+        lay = st.layers[key]
+        W, ab = st.weights[key]
+        X, dY = f64(st.X[0][INPUT_GROUP.get(name, name)]), f64(st.dY[0][name])
+        A = [f64(a) for a, _ in ab]
+        B = [f64(b) for _, b in ab]
+        Y, H = O.fused_forward(X, f64(W), A, B, slots, round_bf16=True, want_h=True)
+        dX, dA, dB = O.fused_backward(X, f64(W), A, B, slots, dY, round_bf16=True,
+                                      want_dx=(L == 0))
+        Hd = f64(st.H[key])
+        cum = np.concatenate([[0], np.cumsum([j.rank for j in wl.jobs])])
+        for sl, j in enumerate(wl.jobs):
+            rows = slots == sl
+            off = lay.offsets[sl]
+            check(f"H {key} {sl}", Hd[rows, off:off + j.rank], H[rows, cum[sl]:cum[sl] + j.rank],
+                  (1e-2, 4e-3))
+            gA, gB = lay.read_grad(sl)
+            check(f"dA {key} {sl}", f64(gA), dA[sl], (2e-2, 8e-3))
+            check(f"dB {key} {sl}", f64(gB), dB[sl], (2e-2, 8e-3))
+        if L == last:
+            check(f"Y {name}", f64(st.Y[name]), Y, (1e-2, 4e-3))
+        if L == 0:
+            check(f"dX {name}", f64(st.dX[name]), dX, (1e-2, 4e-3))
