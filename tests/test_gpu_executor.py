@@ -299,6 +299,7 @@ def test_executor_layer_stack_vs_oracle():
     wl = MINI
     st = TrainingStep(wl, device=0, nano_fixed=3, graphs=False)
     st.init_random(wl.seed, keep_weights=True)
+    st.enable_optimizer()  # (the step's AdamW runs after the gradients this test reads)
     s = st.run()
     torch.cuda.synchronize()
     assert s.nano_used == 3
