@@ -305,7 +305,7 @@ def run_executor(args, rank, world, local_rank):
         if last:  # the LAST timed step runs eagerly with CUDA events around every launch
             capi.call("tlora_profile_begin")
         s_ = st.run(eager=last, stream=stream)
-        traj.append([s_.nano_used, round(s_.ms, 3)])
+        traj.append([s_.nano_used, round(s_.ms, 3) if s_.ms >= 0 else None])
         n_launch += s_.launches  # kernels of the step (a replay counts its captured kernels)
         if s_.replayed_graph:
             graph_launches += 1
@@ -441,6 +441,9 @@ def run_executor(args, rank, world, local_rank):
                    "projections": wl.projections, "parallelism": f"dp{world}",
                    "driver": "C++ step executor (tlora_step_run: libtlora.so)",
                    "nano_batches": nano_desc, "aimd_trajectory_n_ms": traj,
+                   "trajectory_note": "per timed step [N used, the library's own event time of "
+                                      "its latest completed step]; null = with a fixed N the "
+                                      "host runs ahead and no step had completed yet",
                    "dp_allreduce": None if world == 1 else (
                        "sharded optimizer: per key reduce-scatter (fp32) -> AdamW on this rank's "
                        "packed-row shard -> all-gather (bf16 operands), nccl via tlora_comm"
@@ -1124,7 +1127,7 @@ def run_tp_exec(args, rank, world, local_rank):
             evs.append(torch.cuda.Event(enable_timing=True))
             evs[-1].record(stream)
         s_ = ex.run(stream, trace=trace_all)
-        traj.append([s_.nano_used, round(s_.ms, 3)])
+        traj.append([s_.nano_used, round(s_.ms, 3) if s_.ms >= 0 else None])
         launches += s_.launches
     e1.record(stream)
     torch.cuda.synchronize()
@@ -1165,6 +1168,9 @@ def run_tp_exec(args, rank, world, local_rank):
                    "nano_batches": ("AIMD every step" if args.nano_batches <= 0
                                     else f"fixed N={args.nano_batches}"),
                    "aimd_trajectory_n_ms": traj, "untimed_steps_before_timing": settle,
+                   "trajectory_note": "per timed step [N used, the library's own event time of "
+                                      "its latest completed step]; null = with a fixed N the "
+                                      "host runs ahead and no step had completed yet",
                    "algorithmic_tflop_per_step": round(flops / 1e12, 3),
                    "achieved_tflops_aggregate": round(flops / (ms_per_step / 1e3) / 1e12, 1)},
         "gpu_launches": int(launches),

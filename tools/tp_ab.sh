@@ -7,7 +7,7 @@ summ() { python - "$1" "$2" <<'PY'
 import json, sys
 lines = [l for l in open(sys.argv[1]).read().splitlines() if l.startswith("{")]
 d = json.loads(lines[-1]) if lines else {}
-tr = [x[1] for x in (d.get("config") or {}).get("aimd_trajectory_n_ms", []) if x[1] > 0]
+tr = [x[1] for x in (d.get("config") or {}).get("aimd_trajectory_n_ms", []) if x[1] and x[1] > 0]
 print(sys.argv[2], d.get("value"), d.get("ms_per_step"), (d.get("clocks") or {}).get("sm_mhz"),
       "lib_ms", tr[:4], "traced", (d.get("pipeline_monitor") or {}).get("t_iter_event_s"), flush=True)
 PY
