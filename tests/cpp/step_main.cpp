@@ -218,7 +218,7 @@ int bench(int argc, char** argv) {
     const auto st = tr.step(0, s);
     tokens += st.tokens;
     traj += (i ? "," : "") + std::string("[") + std::to_string(st.nano_used) + "," +
-            std::to_string(st.ms) + "]";
+            (st.ms >= 0.f ? std::to_string(st.ms) : std::string("null")) + "]";
   }
   cudaEventRecord(e1, s);
   cudaEventSynchronize(e1);
