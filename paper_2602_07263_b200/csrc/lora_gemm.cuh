@@ -67,6 +67,13 @@ struct GemmArgs {
   // 2-CTA fused GEMM: dynamic tile scheduler (self-resetting global ticket; null = static
   // round-robin). Only read from args (the main tiles' GemmArgs) of a launch.
   int32_t* tile_counter;
+  // 2-CTA fused GEMM, EPI_BF16 main tiles: tail split-K (tlora_capi.cu tail_split). A tile
+  // with pad = 1 + 2*slot accumulates the first K half and writes its fp32 partial to
+  // split_ws[slot] (256 x 256), then raises split_flags[slot*8 + cta*4 + warp]; the tile
+  // with pad = 2 + 2*slot accumulates the rest (+ the LoRA K-extension), waits for those
+  // flags, adds the partial and stores as usual (one bf16 rounding), and clears them.
+  float* split_ws;
+  int32_t* split_flags;
 };
 
 template <int BN, int STAGES>

@@ -332,6 +332,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           continue;
         }
       }
+      // tail split-K roles (GemmArgs::split_ws): 1 = partial writer, 2 = finisher
+      const int role = (EPI == EPI_BF16 && !sec && td.pad > 0) ? 2 - (td.pad & 1) : 0;
+      float* part = nullptr;
+      int32_t* flag = nullptr;
+      if (role) {
+        const int slot = (td.pad - 1) >> 1;
+        part = args.split_ws + ((size_t)slot * kBM2 + 128 * rank + ew * 32 + lane) * kBN2;
+        flag = args.split_flags + slot * 8 + (int)rank * 4 + ew;
+        if (role == 2) {  // the writer warp of the same rows has published its partial
+          int f;
+          do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(flag) : "memory");
+            if (f != 0) break;
+            __nanosleep(32);
+          } while (true);
+        }
+      }
 #pragma unroll 1
       for (int c = 0; c < ncols; c += 32) {
         uint32_t v[32];
@@ -342,10 +359,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = 0u;
         }
+        if (role == 1) {
+          float4* w = reinterpret_cast<float4*>(part + c);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            __stcg(w + q, make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                      __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+          continue;
+        }
+        if (role == 2) {
+          const float4* r4 = reinterpret_cast<const float4*>(part + c);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 pv = __ldcg(r4 + q);
+            v[4 * q] = __float_as_uint(pv.x + __uint_as_float(v[4 * q]));
+            v[4 * q + 1] = __float_as_uint(pv.y + __uint_as_float(v[4 * q + 1]));
+            v[4 * q + 2] = __float_as_uint(pv.z + __uint_as_float(v[4 * q + 2]));
+            v[4 * q + 3] = __float_as_uint(pv.w + __uint_as_float(v[4 * q + 3]));
+          }
+        }
         if (sec)
           epi_store32<EPI_BF16_MASK>(args2, 0, row, td.n0 + c, v, lo, hi);
         else
           epi_store32<EPI>(args, td.split, row, td.n0 + c, v, 0, 0x7fffffff);
+      }
+      if (role == 1) {  // every lane's partial row is written before the flag
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(1) : "memory");
+      } else if (role == 2) {
+        __syncwarp();
+        if (lane == 0) *reinterpret_cast<volatile int32_t*>(flag) = 0;  // for the next launch
       }
       if (!empty_k) {
         tc_fence_before();

@@ -8,10 +8,12 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <atomic>
 #include <mutex>
@@ -214,6 +216,7 @@ struct Gemm2Secondary {
   CUtensorMap a, b;
   GemmArgs args;
   double flops;
+  const std::vector<tlora::PlanTile>* host = nullptr;  // the same tiles, host copy
 };
 
 // Dynamic tile scheduler tickets for the fused GEMM (lora_gemm2_kernel): a per-device pool
@@ -758,6 +761,13 @@ struct tlora_plan {
   // plan's lifetime. Calls on ONE plan are serialised on one stream (tlora.h).
   mutable std::mutex scratch_mu;
   mutable DevBuf<char> scratch[3];  // 0 partial planes, 1 dH, 2 gather
+  // tail split-K tile tables of the fused fwd / dX launches (tail_split), per (launch,
+  // CTA pairs, secondary-tile signature); built on first eager use
+  struct SplitTable {
+    DevBuf<TileDesc> tiles;
+    int n = 0, q = 0;
+  };
+  mutable std::map<std::tuple<int, int, int64_t>, std::unique_ptr<SplitTable>> split_tables;
 };
 
 namespace {
@@ -1600,6 +1610,7 @@ Gemm2Secondary make_lowrank2(tlora_layer* layer, const tlora_plan* plan, int whi
   g.a = tmap_k(A, K, T, 128);
   g.b = tmap_k(which == 0 ? layer->AT.p : layer->Bcat.p, K, R, 64);
   g.flops = 2.0 * (double)plan->P.tok_rank * K;
+  g.host = &plan->P.tiles[launch];
   return g;
 }
 
@@ -1611,6 +1622,161 @@ void launch_lowrank_pairs(tlora_layer* layer, const Gemm2Secondary& sec, int kin
   g.flops = 0.0;
   launch_gemm2<tlora::EPI_BF16, TLORA_GEMM2_STAGES>(g.a, g.b, g.a, g.b, none, layer->sm_count, s,
                                                     kind, flops, &g);
+}
+
+// ------------------------------------------------------------------ tail split-K
+// A persistent fused GEMM launch walks its tiles round-robin over the CTA pairs, so its
+// last wave is partial (C2 fwd up: 3072 tiles = 41.5 waves of 74 pairs) and the pairs
+// without a tile idle at the end. With TLORA_TAIL_SPLIT=1 the last q main tiles of a
+// launch are split in two along K: the first half writes an fp32 partial, the second half
+// (with the LoRA K-extension) adds it in its epilogue (GemmArgs::split_ws; deterministic,
+// one bf16 rounding). q minimises the round-robin makespan of the launch's tile costs
+// (k-blocks; the secondary tiles of the chained schedule included), and is 0 unless the
+// model gains >= 1%. All first halves precede all second halves in the tile order, so
+// a waiting second half never blocks a first half of its own pair.
+bool tail_split_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("TLORA_TAIL_SPLIT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+constexpr int kSplitSlots = 128;  // >= CTA pairs of any launch (q <= pairs)
+
+struct SplitWs {
+  float* ws = nullptr;
+  int32_t* flags = nullptr;
+};
+
+// One workspace per (device, stream): fused GEMM launches on one stream are serialised.
+const SplitWs* split_ws(int dev, cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SplitWs> pool;
+  std::lock_guard<std::mutex> lk(mu);
+  auto& w = pool[{dev, s}];
+  if (!w.ws) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    TL_CUDA(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;
+    TL_CUDA(cudaMalloc(&w.ws, (size_t)kSplitSlots * tlora::kBM2 * tlora::kBN2 * sizeof(float)));
+    TL_CUDA(cudaMalloc(&w.flags, (size_t)kSplitSlots * 8 * sizeof(int32_t)));
+    TL_CUDA(cudaMemset(w.flags, 0, (size_t)kSplitSlots * 8 * sizeof(int32_t)));
+    TL_CUDA(cudaDeviceSynchronize());
+  }
+  return &w;
+}
+
+double main_tile_cost(const tlora::PlanTile& t) {
+  return (double)(t.ke0 - t.kb0 + std::max(0, t.ke1 - t.kb1)) / tlora::kBK;
+}
+double sec_tile_cost(const tlora::PlanTile& t) {
+  // A-operand streaming bounds a narrow secondary tile (~0.45 of a full-N k-block)
+  return (double)(t.ke0 - t.kb0) / tlora::kBK * std::max(t.pad / 256.0, 0.45);
+}
+
+const tlora_plan::SplitTable* plan_split(const tlora_plan* plan, int launch, int pairs,
+                                         const Gemm2Secondary* sec, cudaStream_t s) {
+  const auto& M = plan->P.tiles[launch];
+  int64_t sig = 0;
+  std::vector<double> sc;
+  if (sec && sec->host)
+    for (const auto& t : *sec->host) {
+      sc.push_back(sec_tile_cost(t));
+      sig = sig * 1000003 + (int64_t)(t.ke0 - t.kb0) * 517 + t.pad;
+    }
+  const auto key = std::make_tuple(launch, pairs, sig);
+  std::lock_guard<std::mutex> lk(plan->scratch_mu);
+  auto it = plan->split_tables.find(key);
+  if (it != plan->split_tables.end()) return it->second.get();
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  TL_CUDA(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return nullptr;
+  const int n = (int)M.size();
+  constexpr double kFix = 4.0;  // partial write / read per half, in k-block units
+  std::vector<double> load(pairs);
+  auto makespan = [&](int q) {
+    std::fill(load.begin(), load.end(), 0.0);
+    int idx = 0;
+    for (int i = 0; i < n - q; ++i) load[idx++ % pairs] += main_tile_cost(M[i]);
+    for (int h = 0; h < 2; ++h)
+      for (int i = n - q; i < n; ++i) {
+        const auto& t = M[i];
+        const int nk = (t.ke0 - t.kb0) / tlora::kBK;
+        const double c0 = (double)(nk / 2);
+        load[idx++ % pairs] += (h == 0 ? c0 : main_tile_cost(t) - c0) + kFix;
+      }
+    for (double c : sc) load[idx++ % pairs] += c;
+    return *std::max_element(load.begin(), load.end());
+  };
+  const double base = makespan(0);
+  int best_q = 0;
+  double best = base;
+  const int qmax = std::min({n, pairs, kSplitSlots});
+  for (int q = 1; q <= qmax; ++q) {
+    bool ok = true;  // both halves need >= 1 k-block
+    for (int i = n - q; i < n && ok; ++i) ok = (M[i].ke0 - M[i].kb0) / tlora::kBK >= 2;
+    if (!ok) break;
+    const double m = makespan(q);
+    if (m < best) {
+      best = m;
+      best_q = q;
+    }
+  }
+  if (best > 0.99 * base) best_q = 0;
+  if (std::getenv("TLORA_TAIL_SPLIT_DEBUG"))
+    std::fprintf(stderr, "[tail_split] launch %d tiles %d + %zu secondary, %d pairs: q = %d, "
+                 "modelled makespan %.1f -> %.1f k-blocks\n", launch, n, sc.size(), pairs, best_q,
+                 base, best_q ? best : base);
+  auto tab = std::make_unique<tlora_plan::SplitTable>();
+  tab->q = best_q;
+  if (best_q > 0) {
+    std::vector<TileDesc> out;
+    out.reserve(n + best_q);
+    auto desc = [](const tlora::PlanTile& t) {
+      return TileDesc{t.m0, t.n0, t.kb0, t.ke0, t.kb1, t.ke1, t.split, t.pad};
+    };
+    for (int i = 0; i < n - best_q; ++i) out.push_back(desc(M[i]));
+    for (int h = 0; h < 2; ++h)
+      for (int j = 0; j < best_q; ++j) {
+        TileDesc d = desc(M[n - best_q + j]);
+        const int mid = d.kb0 + ((d.ke0 - d.kb0) / tlora::kBK / 2) * tlora::kBK;
+        if (h == 0) {  // first K half, no K-extension: the partial writer
+          d.ke0 = mid;
+          d.kb1 = d.ke1 = 0;
+          d.pad = 1 + 2 * j;
+        } else {  // the rest + the LoRA K-extension: the finisher
+          d.kb0 = mid;
+          d.pad = 2 + 2 * j;
+        }
+        out.push_back(d);
+      }
+    tab->n = (int)out.size();
+    tab->tiles.alloc(out.size());
+    TL_CUDA(cudaMemcpy(tab->tiles.p, out.data(), out.size() * sizeof(TileDesc),
+                       cudaMemcpyHostToDevice));
+  }
+  auto* ret = tab.get();
+  plan->split_tables.emplace(key, std::move(tab));
+  return ret;
+}
+
+// Swap a fused fwd / dX launch's main tiles for its split table (no-op unless enabled and
+// the model gains).
+void apply_tail_split(tlora_layer* layer, const tlora_plan* plan, int launch, GemmArgs& a,
+                      const Gemm2Secondary* sec, cudaStream_t s) {
+  if (!tail_split_on() || a.num_tiles == 0 || dyn_sched(layer->device)) return;
+  const int total = a.num_tiles + (sec ? sec->args.num_tiles : 0);
+  const int pairs = std::min(2 * total, sm_budget(layer->device, layer->sm_count, true) / 2 * 2) / 2;
+  if (pairs < 2) return;
+  const tlora_plan::SplitTable* t = plan_split(plan, launch, pairs, sec, s);
+  if (!t || t->q == 0) return;
+  const SplitWs* w = split_ws(layer->device, s);
+  if (!w) return;
+  a.tiles = t->tiles.p;
+  a.num_tiles = t->n;
+  a.split_ws = w->ws;
+  a.split_flags = w->flags;
 }
 
 // Y = X·W + H·Bᵀcatᵀ: 2-CTA fused GEMM, K-extension over each tile's packed-rank window.
@@ -1632,9 +1798,11 @@ void run_fwd_gemm(tlora_layer* layer, const tlora_plan* plan, const void* X, con
   const CUtensorMap mb0 = tmap_k(layer->Wt16.p, d, k, 128);
   const CUtensorMap ma1 = tmap_k(H, R, T, 128);
   const CUtensorMap mb1 = tmap_k(layer->BcatT.p, R, k, 128);
-  if (y_dtype == TLORA_BF16)
+  if (y_dtype == TLORA_BF16) {
+    apply_tail_split(layer, plan, TLORA_L_FWD, a, sec, s);
     launch_gemm2<tlora::EPI_BF16, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s,
                                                       TLORA_L_FWD, flops, sec);
+  }
   else
     launch_gemm2<tlora::EPI_F32, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s,
                                                      TLORA_L_FWD, flops, sec);
@@ -1684,6 +1852,7 @@ void run_dx(tlora_layer* layer, const tlora_plan* plan, const void* dY, const vo
   const CUtensorMap mb0 = tmap_k(layer->W16.p, k, d, 128);
   const CUtensorMap ma1 = tmap_k(dH, R, T, 128);
   const CUtensorMap mb1 = tmap_k(layer->Acat.p, R, d, 128);
+  apply_tail_split(layer, plan, TLORA_L_DX, a, sec, s);
   launch_gemm2<tlora::EPI_BF16, TLORA_GEMM2_STAGES>(ma0, mb0, ma1, mb1, a, layer->sm_count, s,
                                                     TLORA_L_DX,
                                                     2.0 * T * d * k + 2.0 * (double)plan->P.tok_rank * d,
