@@ -56,6 +56,19 @@ while True:
 """
 
 
+def gpu_energy_mj(device: int):
+    """NVML's total-energy counter of this CUDA device (mJ since driver load), or None."""
+    try:
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(device).uuid)
+        h = pynvml.nvmlDeviceGetHandleByUUID(uuid.encode())
+        return int(pynvml.nvmlDeviceGetTotalEnergyConsumption(h))
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """SM clock, power and clock-event (throttle) reasons sampled every ~50 ms from NVML by
     a separate sampler process (so a busy driver thread cannot starve it), started before
@@ -299,6 +312,7 @@ def run_executor(args, rank, world, local_rank):
     nv0 = nvlink_bytes() if world > 1 and rank == 0 else None
     if world > 1:
         dist.barrier()
+    en0, tw0 = gpu_energy_mj(local_rank), time.time()
     e0.record(stream)
     for i in range(args.steps):
         last = i == args.steps - 1 and os.environ.get("TLORA_BENCH_PROF", "1") != "0"
@@ -311,9 +325,17 @@ def run_executor(args, rank, world, local_rank):
             graph_launches += 1
     e1.record(stream)
     torch.cuda.synchronize()
+    en1, tw1 = gpu_energy_mj(local_rank), time.time()
     if world > 1:
         dist.barrier()
     nvl = nvlink_delta(nv0, nvlink_bytes(), args.steps) if nv0 is not None else None
+    energy = None
+    if en0 is not None and en1 is not None and en1 > en0:
+        jps = (en1 - en0) / 1e3 / args.steps
+        energy = {"joules_per_step": round(jps, 3), "tokens_per_joule": round(wl.tokens / jps, 1),
+                  "avg_power_w": round((en1 - en0) / 1e3 / max(tw1 - tw0, 1e-9), 1),
+                  "source": "NVML total-energy counter of this rank's GPU around the timed "
+                            "region (host wall clock for the power)"}
     cnt = (C.c_int32 * 6)()
     ms6 = (C.c_double * 6)()
     fl6 = (C.c_double * 6)()
@@ -469,6 +491,7 @@ def run_executor(args, rank, world, local_rank):
         "nvlink": nvl,
         "cpu_baseline": cpu,
         "cpu_baseline_oracle_f32": cpu_f32,
+        "energy": energy,
         "clocks": clk,
     }
 
