@@ -294,9 +294,11 @@ def run_executor(args, rank, world, local_rank):
     torch.cuda.synchronize()
     # untimed settle steps (>= 1 s under load); every rank runs the same count
     t_clk0 = time.time()
+    en_settle, n_settle = gpu_energy_mj(local_rank), 0
     while True:
         for _ in range(3):
             st.run(stream=stream)
+            n_settle += 1
         el = torch.tensor([time.time() - t_clk0], device="cuda", dtype=torch.float64)
         if world > 1:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
@@ -312,7 +314,6 @@ def run_executor(args, rank, world, local_rank):
     nv0 = nvlink_bytes() if world > 1 and rank == 0 else None
     if world > 1:
         dist.barrier()
-    en0, tw0 = gpu_energy_mj(local_rank), time.time()
     e0.record(stream)
     for i in range(args.steps):
         last = i == args.steps - 1 and os.environ.get("TLORA_BENCH_PROF", "1") != "0"
@@ -330,12 +331,16 @@ def run_executor(args, rank, world, local_rank):
         dist.barrier()
     nvl = nvlink_delta(nv0, nvlink_bytes(), args.steps) if nv0 is not None else None
     energy = None
-    if en0 is not None and en1 is not None and en1 > en0:
-        jps = (en1 - en0) / 1e3 / args.steps
+    if en_settle is not None and en1 is not None and en1 > en_settle:
+        # the counter's update granularity is coarse next to a ~0.2 s timed region, so the
+        # window is the >= 1 s of settle steps (the same replayed step) + the timed steps
+        nst = n_settle + args.steps
+        jps = (en1 - en_settle) / 1e3 / nst
         energy = {"joules_per_step": round(jps, 3), "tokens_per_joule": round(wl.tokens / jps, 1),
-                  "avg_power_w": round((en1 - en0) / 1e3 / max(tw1 - tw0, 1e-9), 1),
-                  "source": "NVML total-energy counter of this rank's GPU around the timed "
-                            "region (host wall clock for the power)"}
+                  "avg_power_w": round((en1 - en_settle) / 1e3 / max(tw1 - t_clk0, 1e-9), 1),
+                  "steps_in_window": nst,
+                  "source": "NVML total-energy counter of this rank's GPU over the settle + "
+                            "timed steps (host wall clock for the power)"}
     cnt = (C.c_int32 * 6)()
     ms6 = (C.c_double * 6)()
     fl6 = (C.c_double * 6)()
