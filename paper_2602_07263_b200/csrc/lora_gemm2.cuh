@@ -21,6 +21,10 @@
 
 namespace tlora {
 
+#ifndef TLORA_TAIL_SPLIT_KERNEL
+#define TLORA_TAIL_SPLIT_KERNEL 1  // 0: compile the fused GEMM without the split-K epilogue
+#endif
+
 constexpr int kBM2 = 256;  // rows per CTA pair
 constexpr int kBN2 = 256;
 
@@ -333,7 +337,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         }
       }
       // tail split-K roles (GemmArgs::split_ws): 1 = partial writer, 2 = finisher
+#if TLORA_TAIL_SPLIT_KERNEL
       const int role = (EPI == EPI_BF16 && !sec && td.pad > 0) ? 2 - (td.pad & 1) : 0;
+#else
+      constexpr int role = 0;
+#endif
       float* part = nullptr;
       int32_t* flag = nullptr;
       if (role) {
