@@ -14,6 +14,7 @@
 // Restated independently in oracle/tlora_oracle.c (orc_nano_assign).
 #pragma once
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <numeric>
 #include <set>
@@ -103,6 +104,71 @@ inline NanoMap nano_assign(const std::vector<int32_t>& batch, const std::vector<
   }
   // which samples: job s's first nano_slot[0][s] samples go to nano 0, the next ones to
   // nano 1, ... — every (nano, job) pair is one contiguous range of the job's samples
+  for (int32_t s = 0; s < S; ++s) {
+    size_t q = (size_t)first[s];
+    for (int32_t i = 0; i < m.n; ++i)
+      for (int32_t c = 0; c < m.nano_slot[(size_t)i * S + s]; ++c) m.sample_nano[q++] = i;
+  }
+  return m;
+}
+
+// Ramped variant for a pipeline whose boundary traffic is exposed only at its ends (the
+// tensor-parallel step: nano 0's all-gather before any compute, the last nano's reduce-
+// scatter after it): nano-batch i gets a share of the samples proportional to
+// min(g^i, g^(n-1-i)), so the first and last nano-batches are small and each one's traffic
+// still hides behind its neighbour's compute while g <= compute / traffic. Samples are
+// placed heaviest first on the nano-batch with the least load per unit of its share (ties:
+// lower nano); (nano, job) ranges stay contiguous as in nano_assign. g <= 1 or n < 3 is
+// nano_assign itself.
+inline NanoMap nano_assign_ramp(const std::vector<int32_t>& batch,
+                                const std::vector<int64_t>& weight, int32_t n_req, double g) {
+  NanoMap m = nano_assign(batch, weight, n_req);  // validation, n, uniform fallback
+  if (g <= 1.0 || m.n < 3) return m;
+  const int32_t S = (int32_t)batch.size();
+  int64_t total = 0;
+  for (int32_t b : batch) total += b;
+  // shares -> integer counts (largest remainder), every nano-batch >= 1 sample
+  std::vector<double> share(m.n);
+  double ssum = 0.0;
+  for (int32_t i = 0; i < m.n; ++i) {
+    share[i] = std::pow(g, (double)std::min(i, m.n - 1 - i));
+    ssum += share[i];
+  }
+  std::vector<int32_t> cnt(m.n, 1);
+  int64_t left = total - m.n;
+  std::vector<std::pair<double, int32_t>> rem;
+  for (int32_t i = 0; i < m.n; ++i) {
+    const double want = share[i] / ssum * (double)total - 1.0;
+    const int32_t f = want > 0.0 ? (int32_t)std::floor(want) : 0;
+    cnt[i] += f;
+    left -= f;
+    rem.push_back({-(want - f), i});
+  }
+  std::sort(rem.begin(), rem.end());
+  for (size_t r = 0; left > 0 && r < rem.size(); ++r, --left) ++cnt[rem[r].second];
+  for (int32_t i = 0; left > 0; i = (i + 1) % m.n, --left) ++cnt[i];
+  m.per_nano = cnt;
+  std::fill(m.nano_slot.begin(), m.nano_slot.end(), 0);
+  std::vector<int32_t> order(S);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int32_t a, int32_t b) { return weight[a] > weight[b]; });
+  std::vector<int32_t> room = cnt;
+  std::vector<int64_t> load(m.n, 0);
+  for (int32_t s : order)
+    for (int32_t q = 0; q < batch[s]; ++q) {
+      int32_t best = -1;
+      for (int32_t i = 0; i < m.n; ++i) {
+        if (room[i] == 0) continue;
+        // least load per share: load_i / cnt_i < load_b / cnt_b, in integers
+        if (best < 0 || (__int128)load[i] * cnt[best] < (__int128)load[best] * cnt[i]) best = i;
+      }
+      ++m.nano_slot[(size_t)best * S + s];
+      --room[best];
+      load[best] += weight[s];
+    }
+  std::vector<int64_t> first(S, 0);
+  for (int32_t s = 1; s < S; ++s) first[s] = first[s - 1] + batch[s - 1];
   for (int32_t s = 0; s < S; ++s) {
     size_t q = (size_t)first[s];
     for (int32_t i = 0; i < m.n; ++i)

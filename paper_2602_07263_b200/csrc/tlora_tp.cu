@@ -284,7 +284,12 @@ Layout& tlora_tp_step::layout(int32_t n) {
   auto it = layouts.find(n);
   if (it != layouts.end()) return *it->second;
   auto lo = std::make_unique<Layout>();
-  lo->map = tlora::nano_assign(batch, weight, n);
+  // TLORA_TP_RAMP=g (> 1): ramped nano-batch sizes (tlora_nano.hpp nano_assign_ramp)
+  static const double ramp = [] {
+    const char* e = std::getenv("TLORA_TP_RAMP");
+    return e ? std::atof(e) : 0.0;
+  }();
+  lo->map = tlora::nano_assign_ramp(batch, weight, n, ramp);
   int64_t t0 = 0;
   for (int32_t i = 0; i < lo->map.n; ++i) {
     Nano nb;
