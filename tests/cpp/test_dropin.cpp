@@ -22,6 +22,7 @@
 #include "lora_fleet/nano_pipeline.hpp"
 #include "lora_fleet/ssm_plan.hpp"
 #include "lora_fleet/trainer.hpp"
+#include "../../paper_2602_07263_b200/csrc/tlora_nano.hpp"
 
 using namespace lora_fleet;
 
@@ -436,6 +437,47 @@ void gpu_persistent_fused_layer() {
   }
 }
 
+void cpu_nano_ramp() {  // tlora_nano.hpp nano_assign_ramp (TLORA_TP_RAMP)
+  const std::vector<int32_t> b = {1, 2, 4, 8, 1, 2, 4, 8, 1, 2, 4, 8, 1, 2, 4, 8};
+  const std::vector<int32_t> r = {8, 16, 32, 64, 128, 24, 48, 96, 8, 16, 32, 64, 128, 24, 48, 96};
+  std::vector<int64_t> w;
+  for (int32_t x : r) w.push_back(1024LL * (100000 + 30 * x));
+  for (int32_t n : {1, 2, 3, 4, 5, 7}) {
+    const auto u = tlora::nano_assign(b, w, n);
+    const auto g1 = tlora::nano_assign_ramp(b, w, n, 1.0);  // g <= 1: the uniform map
+    CHECK(g1.per_nano == u.per_nano && g1.nano_slot == u.nano_slot);
+    const auto m = tlora::nano_assign_ramp(b, w, n, 2.0);
+    CHECK(m.n == std::min(n, 60));
+    int64_t tot = 0;
+    for (int32_t c : m.per_nano) {
+      CHECK(c >= 1);
+      tot += c;
+    }
+    CHECK(tot == 60);
+    if (m.n >= 3) {  // small ends, larger middle
+      CHECK(m.per_nano.front() < m.per_nano[(size_t)m.n / 2]);
+      CHECK(m.per_nano.back() < m.per_nano[(size_t)m.n / 2]);
+    }
+    // per nano, the slot counts add up to its count; per slot, to the job's batch; and a
+    // job's samples are enumerated nano by nano (contiguous (nano, job) ranges)
+    for (int32_t i = 0; i < m.n; ++i) {
+      int32_t c = 0;
+      for (size_t s = 0; s < b.size(); ++s) c += m.nano_slot[(size_t)i * b.size() + s];
+      CHECK(c == m.per_nano[(size_t)i]);
+    }
+    size_t q = 0;
+    for (size_t s = 0; s < b.size(); ++s) {
+      int32_t c = 0, prev = 0;
+      for (int32_t i = 0; i < m.n; ++i) c += m.nano_slot[(size_t)i * b.size() + s];
+      CHECK(c == b[s]);
+      for (int32_t k = 0; k < b[s]; ++k, ++q) {
+        CHECK(m.sample_nano[q] >= prev);
+        prev = m.sample_nano[q];
+      }
+    }
+  }
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -448,6 +490,7 @@ int main(int argc, char** argv) {
     cases.push_back({"communicator argument errors", cpu_comm_arguments});
     cases.push_back({"projection-level layer set", cpu_projection_layer_set});
     cases.push_back({"trainer descriptor errors, host schedule", cpu_trainer_errors});
+    cases.push_back({"ramped nano-batch map", cpu_nano_ramp});
   }
   if (mode == "gpu" || mode == "all") {
     cases.push_back({"fused_forward matches the materialized oracle", gpu_matches_oracle});
