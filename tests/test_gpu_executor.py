@@ -345,3 +345,17 @@ def test_executor_layer_stack_vs_oracle():
             check(f"Y {name}", f64(st.Y[name]), Y, (1e-2, 4e-3))
         if L == 0:
             check(f"dX {name}", f64(st.dX[name]), dX, (1e-2, 4e-3))
+
+
+def test_tail_split_knob_parity():
+    """TLORA_TAIL_SPLIT=1 (off by default: split-K of each fused launch's last partial wave)
+    keeps the benched C2 step inside the fp32-restatement tolerances and the executor
+    bitwise equal to the Python driver (both see the same split tables). Subprocess: the
+    knob is read once per process."""
+    e = dict(os.environ, TLORA_TAIL_SPLIT="1")
+    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-x",
+                        str(ROOT / "tests" / "test_gpu_step_parity.py") + "::test_c2_benched_step_full_size",
+                        str(ROOT / "tests" / "test_gpu_executor.py") + "::test_executor_matches_python_driver_bitwise"],
+                       capture_output=True, text=True, timeout=900, env=e, cwd=str(ROOT))
+    print(p.stdout[-2000:])
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
