@@ -290,20 +290,19 @@ def test_tp_data_paths_single_gpu(script, env):
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
 
 
-def test_executor_layer_stack_vs_oracle():
-    """A 2-layer x 4-projection stack through the executor at N = 3 (nano-major layout,
-    chained schedule, side-stream gradients) against the double oracle with bf16-emulated
+def _executor_vs_oracle(wl, nano):
+    """One executor step of `wl` at N = nano against the double oracle with bf16-emulated
     intermediates (oracle/tlora_oracle.c: fused_forward / fused_backward, pinned to the
-    reference's goldens): per (layer, projection) the H stash and dA / dB of every job, the
-    last layer's Y and layer 0's dX. Tolerances as SURVEY §8(c) / test_gpu_step_parity."""
-    wl = MINI
-    st = TrainingStep(wl, device=0, nano_fixed=3, graphs=False)
+    reference's goldens) on the executor's own token -> slot map: per (layer, projection)
+    the H stash and dA / dB of every job, the last layer's Y and layer 0's dX. Tolerances
+    as SURVEY §8(c) / test_gpu_step_parity."""
+    st = TrainingStep(wl, device=0, nano_fixed=nano, graphs=False)
     st.init_random(wl.seed, keep_weights=True)
     st.enable_optimizer()  # (the step's AdamW runs after the gradients this test reads)
     s = st.run()
     torch.cuda.synchronize()
-    assert s.nano_used == 3
-    n_used, t0, ns, _ = st.layout(3)
+    assert s.nano_used == min(nano, sum(j.batch for j in wl.jobs))
+    n_used, t0, ns, _ = st.layout(nano)
     slots = np.full(st.T, -1, np.int32)
     for i in range(n_used):
         row = int(t0[i])
@@ -345,6 +344,21 @@ def test_executor_layer_stack_vs_oracle():
             check(f"Y {name}", f64(st.Y[name]), Y, (1e-2, 4e-3))
         if L == 0:
             check(f"dX {name}", f64(st.dX[name]), dX, (1e-2, 4e-3))
+
+
+def test_executor_layer_stack_vs_oracle():
+    """A 2-layer x 4-projection stack (4 jobs, ranks 8-200, ragged T) through the executor
+    at N = 3: nano-major layout, chained schedule, side-stream gradients."""
+    _executor_vs_oracle(MINI, 3)
+
+
+@pytest.mark.parametrize("cell,nano", [((1024, 8, 4096, 5), 3), ((2048, 16, 4096, 6), 4),
+                                       ((1024, 32, 2048, 7), 5), ((2048, 12, 3000, 8), 1)])
+def test_executor_c5_cells_vs_oracle(cell, nano):
+    """C5 heterogeneity cells (ranks 4-256, Zipf-skewed ragged token counts, one sample per
+    job) through the executor: the rank-aware map puts whole jobs into nano-batches."""
+    from paper_2602_07263_b200.workload import c5_cell
+    _executor_vs_oracle(c5_cell(*cell), nano)
 
 
 def test_tail_split_knob_parity():
