@@ -225,6 +225,23 @@ def test_executor_data_parallel_multi_gpu():
     assert p.returncode == 0 and "STEP_DP_CHECK PASS" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
 
 
+def test_executor_data_parallel_path_single_gpu():
+    """tests/step_dp_check.py at world 1: the executor's data-parallel schedule (per-key
+    all-reduce on the comm stream, then the sharded optimizer's reduce-scatter / row-shard
+    AdamW / all-gather + transpose) runs over a 1-rank NCCL communicator on one GPU — the
+    driver's 1-GPU suite covers that code path, not only the >= 2-GPU runs."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node=1", "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), str(ROOT / "tests" / "step_dp_check.py")],
+                       capture_output=True, text=True, timeout=600)
+    print(p.stdout[-3000:])
+    assert p.returncode == 0 and "STEP_DP_CHECK PASS" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
+
+
 def test_traced_step_timeline():
     """TLORA_RUN_TRACE: every op of the schedule gets its completion time on its own stream;
     times are ordered along each stream, cross-stream waits are respected (a GRADS op ends
