@@ -56,6 +56,15 @@ while True:
 """
 
 
+def workload_config(wl, world: int) -> dict:
+    """The benched workload, named identically by both arms (ours and --impl reference) for
+    the same workload and N; implementation details go in each line's own keys."""
+    return {"workload": f"{wl.name}: {wl.notes}", "layers_per_step": wl.layers,
+            "tokens_per_gpu": wl.tokens,
+            "jobs": [[j.job_id, j.rank, j.tokens] for j in wl.jobs],
+            "projections": [list(p) for p in wl.projections], "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)"}
+
 def gpu_energy_mj(device: int):
     """NVML's total-energy counter of this CUDA device (mJ since driver load), or None."""
     try:
@@ -462,11 +471,8 @@ def run_executor(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded normal activations/grads, random-init W and adapters)",
-        "config": {"workload": f"{wl.name}: {wl.notes}", "layers_per_step": wl.layers,
-                   "tokens_per_gpu": wl.tokens,
-                   "jobs": [[j.job_id, j.rank, j.tokens] for j in wl.jobs],
-                   "projections": wl.projections, "parallelism": f"dp{world}",
-                   "driver": "C++ step executor (tlora_step_run: libtlora.so)",
+        "config": workload_config(wl, world),
+        "run": {"driver": "C++ step executor (tlora_step_run: libtlora.so)",
                    "nano_batches": nano_desc, "aimd_trajectory_n_ms": traj,
                    "trajectory_note": "per timed step [N used, the library's own event time of "
                                       "its latest completed step]; null = with a fixed N the "
@@ -479,7 +485,6 @@ def run_executor(args, rank, world, local_rank):
                        "nano-batch, on the executor's comm stream"),
                    "cuda_graph": not args.no_graph and world == 1,
                    "graph_replays_timed": graph_launches,
-                   "l2": "inputs larger than L2 (X/dY/W per step >> 126 MB)",
                    "algorithmic_tflop_per_step": round(flops_step / 1e12, 3),
                    "achieved_tflops_step": round(flops_step / (ms_per_step / 1e3) / 1e12, 1)},
         "e2e": {"value": round(tokens / (e2e_ms / 1e3), 1), "unit": "tokens/s",
@@ -1233,8 +1238,8 @@ def run_reference(args, rank, world):
         "ms_per_step": round(ms_per_step, 3) if ms_per_step else None, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": res["dtype"],
         "data": "synthetic (seeded)",
-        "config": {"workload": f"{wl.name}: {wl.notes}", "sample": res["sample"],
-                   "tokens_per_step": res.get("tokens_per_repeat"),
+        "config": workload_config(wl, world),
+        "sample": {"what": res["sample"], "tokens_per_step": res.get("tokens_per_repeat"),
                    "tokens_per_thread": res.get("tokens_per_thread"), "threads": threads},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": res["cores"],
                          "kind": res["kind"], "sample": res["sample"]},

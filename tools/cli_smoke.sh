@@ -2,7 +2,7 @@
 # Every bench.py variant a user may call still runs and prints a JSON line (1 GPU).
 OUT=$1
 mkdir -p "$OUT"
-run() { local name=$1; shift; timeout 600 python bench.py "$@" > "$OUT/$name.log" 2>&1; echo "$name rc=$? $(grep -h '^{' "$OUT/$name.log" | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read() or "{}"); print(d.get("value"), d.get("ms_per_step"), (d.get("config") or {}).get("driver") or (d.get("config") or {}).get("nano_batches"))' 2>&1)"; }
+run() { local name=$1; shift; timeout 600 python bench.py "$@" > "$OUT/$name.log" 2>&1; echo "$name rc=$? $(grep -h '^{' "$OUT/$name.log" | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read() or "{}"); print(d.get("value"), d.get("ms_per_step"), (d.get("run") or d.get("config") or {}).get("driver"))' 2>&1)"; }
 run host_cpp --host cpp --steps 5 --warmup 3 --no-cpu-baseline
 run driver_py --driver python --steps 5 --warmup 3 --no-cpu-baseline
 run aimd_timed --nano-batches 0 --steps 8 --warmup 3 --no-cpu-baseline
