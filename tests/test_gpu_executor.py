@@ -390,3 +390,29 @@ def test_tail_split_knob_parity():
                        capture_output=True, text=True, timeout=900, env=e, cwd=str(ROOT))
     print(p.stdout[-2000:])
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
+
+
+def _random_workload(seed):
+    rs = np.random.RandomState(seed)
+    nproj = int(rs.randint(1, 4))
+    projs = []
+    for name in [f"p{i}" for i in range(nproj)]:  # each its own input group
+        d = int(rs.choice([64, 136, 256, 392, 512]))
+        k = int(rs.choice([64, 200, 256, 512, 768]))
+        projs.append((str(name), d, k))
+    lim = min(min(d, k) for _, d, k in projs)
+    jobs = []
+    for j in range(int(rs.randint(1, 7))):
+        r = int(min(lim, rs.choice([1, 3, 8, 16, 40, 64, 128, 200])))
+        jobs.append(Job(f"r{j}", r, int(rs.randint(1, 4)), int(rs.choice([1, 7, 64, 128, 300]))))
+    return Workload(f"rand{seed}", projs, jobs, layers=int(rs.randint(1, 3)), seed=seed)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("TLORA_RANDOM_CASES", "24"))))
+def test_executor_random_workloads_vs_oracle(seed):
+    """Seeded random layer sets (1-3 projections with d, k down to 64 and not multiples of
+    64, 1-6 jobs with ranks 1-200, sequence lengths 1-300, 1-2 layers) through the
+    executor at a random N (1-5, also above the sample count) against the double oracle."""
+    wl = _random_workload(seed)
+    nano = int(np.random.RandomState(1000 + seed).randint(1, 6))
+    _executor_vs_oracle(wl, nano)
